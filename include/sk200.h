@@ -1,0 +1,186 @@
+/* sk200 — B200-native sparse-convolution engine: the drop-in C ABI.
+ *
+ * This header is the boundary a sparsekit caller binds to replace the CPU
+ * hot path of the reference (namespace sparsekit, /root/reference/proj).
+ * Each entry point names the reference interface it replaces (file:line).
+ * The reference itself has no extern "C"/FFI layer; its
+ * boundary is the C++ header API, so INTEGRATION.md shows the C++ shim a
+ * maintainer adds to route those calls here.
+ *
+ * Conventions
+ *  - Every function returns sk_status; details via sk_last_error() (per
+ *    thread). No C++ exception crosses this ABI. The reference's
+ *    ValidationError maps to SK_ERR_VALIDATION, ContractError to
+ *    SK_ERR_CONTRACT (common.hpp:19-27).
+ *  - All device pointers are caller-owned unless stated; handles
+ *    (sk_coords, sk_kmap) are library-owned, reference counted, immutable
+ *    after construction and usable from any stream after event sync
+ *    (SparseTensor immutability, tensor.hpp:84-85).
+ *  - Every call is stream-ordered on the `stream` argument (a cudaStream_t;
+ *    NULL = legacy default stream). Calls never synchronise the device except
+ *    where documented (output-coordinate counts, host exports).
+ *  - Coordinates are int32[n][4] = (batch, x, y, z), z = 0 for dims = 2
+ *    (Coord, tensor.hpp:15-20). Packable range: batch in [0, 4096),
+ *    x/y/z in [-65536, 65536); outside it SK_ERR_VALIDATION.
+ *  - Features are row-major [n][C]; weights are [K^D][C_in][C_out]
+ *    row-major in offset order of OffsetSet (WeightTensor, exec.hpp:11-39).
+ */
+#ifndef SK200_H
+#define SK200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SK_OK = 0,
+    SK_ERR_VALIDATION = 1, /* sparsekit::ValidationError (common.hpp:19-22) */
+    SK_ERR_CONTRACT = 2,   /* sparsekit::ContractError   (common.hpp:24-27) */
+    SK_ERR_CUDA = 3,
+    SK_ERR_NCCL = 4,
+    SK_ERR_INTERNAL = 5
+} sk_status;
+
+typedef enum { SK_F32 = 0, SK_F16 = 1, SK_BF16 = 2 } sk_dtype;
+
+/* DataflowKind (exec.hpp:59) */
+typedef enum {
+    SK_GATHER_GEMM_SCATTER = 0,
+    SK_FETCH_ON_DEMAND = 1,
+    SK_IMPLICIT_GEMM = 2
+} sk_dataflow_kind;
+
+/* ReorderMode (exec.hpp:60) */
+typedef enum { SK_REORDER_OFFLINE = 0, SK_REORDER_ONLINE = 1 } sk_reorder;
+
+/* TilePreset (exec.hpp:46-54) re-read for tcgen05:
+ * cta_m = MMA M rows per tile (= pad multiple, 128), cta_n = C_out tile
+ * (multiple of 16, <= 256; 0 = whole C_out), cta_k = channel step per
+ * pipeline stage (16/32/64; 0 = auto), warp_rows = lockstep rows of the cost
+ * model (= cta_m), load_width = rows per gather instruction. */
+typedef struct {
+    int cta_m, cta_n, cta_k, warp_rows, load_width;
+} sk_tile;
+
+/* DataflowConfig (exec.hpp:65-73) */
+typedef struct {
+    int kind;    /* sk_dataflow_kind */
+    int splits;  /* 0 = unsorted; implicit GEMM only */
+    sk_tile tile;
+    int reorder; /* sk_reorder */
+} sk_dataflow_cfg;
+
+typedef struct sk_ctx sk_ctx;
+typedef struct sk_coords sk_coords;
+typedef struct sk_kmap sk_kmap;
+
+typedef struct {
+    int dims, kernel_size, num_offsets, n_in, n_out, transposed;
+    int stride[3];
+    int64_t total_pairs; /* KernelMapWS::total_pairs (kmap.hpp:51-55); syncs */
+} sk_kmap_info;
+
+/* ---- errors / context ---------------------------------------------------- */
+const char* sk_last_error(void);
+const char* sk_version(void);
+/* One context per device; owns the stream-ordered memory pool and the
+ * kernel-map cache (MapCache, kmap.hpp:159-176). */
+sk_status sk_ctx_create(int device, sk_ctx** out);
+sk_status sk_ctx_destroy(sk_ctx* ctx);
+/* Deterministic mode (ExecContext::deterministic, common.hpp:29-32): every
+ * dataflow accumulates splits/offsets in a fixed order (no float atomics). */
+sk_status sk_ctx_set_deterministic(sk_ctx* ctx, int on);
+
+/* ---- coordinate sets (SparseTensor coords + CoordLookup) ------------------ */
+/* SparseTensor(dims, coords, ...) / coords_only (tensor.hpp:89-92) and the
+ * CoordLookup hash (tensor.hpp:118-130, tensor.cpp:80-85): copies d_coords,
+ * validates the packable range, assigns a process-unique id (coord_set_id,
+ * tensor.cpp:26-29) and builds the device hash table once. */
+sk_status sk_coords_create(sk_ctx* ctx, int dims, int n, const int32_t* d_coords,
+                           const int32_t stride_tag[3], void* stream, sk_coords** out);
+/* Same from host memory (copies H2D on `stream`). */
+sk_status sk_coords_create_host(sk_ctx* ctx, int dims, int n, const int32_t* h_coords,
+                                const int32_t stride_tag[3], void* stream, sk_coords** out);
+sk_status sk_coords_retain(sk_coords* c);
+sk_status sk_coords_release(sk_coords* c);
+int sk_coords_n(const sk_coords* c);
+int sk_coords_dims(const sk_coords* c);
+uint64_t sk_coords_id(const sk_coords* c);
+const int32_t* sk_coords_device_ptr(const sk_coords* c);
+sk_status sk_coords_stride_tag(const sk_coords* c, int32_t out[3]);
+/* D2H copy of the coordinates (syncs `stream`). */
+sk_status sk_coords_export(const sk_coords* c, int32_t* h_coords, void* stream);
+
+/* build_out_coords (kmap.cpp:73-94): stride 1 returns the same set
+ * (retained); stride > 1 returns unique(floor_div(p, s)) in first-appearance
+ * order, stride_tag *= s. Reads back the output count (one sync). Cached per
+ * (input id, stride). */
+sk_status sk_out_coords(sk_ctx* ctx, sk_coords* in, const int32_t stride[3], void* stream,
+                        sk_coords** out);
+
+/* ---- kernel maps ------------------------------------------------------------ */
+/* build_kmap_os / build_kmap_ws (kmap.cpp:96-143) + compute_masks
+ * (kmap.cpp:34-47): device OS matrix n_out x K^D (-1 sentinel), per-row
+ * big-endian masks, per-offset pair counts; the WS pair lists (ascending
+ * out row per offset) are derived on first use. transposed = 1 builds the
+ * map of the transposed convolution directly (kmap.cpp:124-129). Cached in
+ * the context by MapKey (kmap.hpp:99-107). Odd kernel only, K <= 5. */
+sk_status sk_kmap_build(sk_ctx* ctx, sk_coords* in, sk_coords* out, int kernel_size,
+                        const int32_t stride[3], int transposed, void* stream, sk_kmap** map);
+/* transpose_map (kmap.cpp:290-315): swap (in, out), mirror offsets. */
+sk_status sk_kmap_transpose(sk_ctx* ctx, sk_kmap* map, void* stream, sk_kmap** out);
+/* split_and_sort + pad_map (kmap.cpp:211-288), i.e. prepare_os_map
+ * (exec.cpp:342-344). Cached on the map per (splits, pad_multiple). */
+sk_status sk_kmap_prepare(sk_ctx* ctx, sk_kmap* map, int splits, int pad_multiple,
+                          void* stream);
+sk_status sk_kmap_retain(sk_kmap* map);
+sk_status sk_kmap_release(sk_kmap* map);
+sk_status sk_kmap_get_info(sk_kmap* map, void* stream, sk_kmap_info* info);
+
+/* Host exports for parity (test-only, sync `stream`). */
+sk_status sk_kmap_export_os(sk_kmap* map, int32_t* h_entries, uint64_t* h_masks, void* stream);
+/* WS CSR: h_ptr[K^D+1], then pairs (in, out) per offset, ascending out. */
+sk_status sk_kmap_export_ws(sk_kmap* map, int64_t* h_ptr, int32_t* h_in, int32_t* h_out,
+                            void* stream);
+/* One prepared split: begin/end offsets, padded row count, then
+ * entries rows x (end-begin), out_row rows, masks rows x words. Pass NULL
+ * data pointers to query sizes only. */
+sk_status sk_kmap_export_split(sk_kmap* map, int splits, int pad_multiple, int s, int* begin,
+                               int* end, int* n_rows, int* mask_words, int32_t* h_entries,
+                               int32_t* h_out_row, uint64_t* h_masks, void* stream);
+
+/* ---- dataflows (exec.hpp:86-124) ---------------------------------------------
+ * dtype: SK_F16/SK_BF16 -> tcgen05 tensor cores (fp32 accumulate in TMEM);
+ * SK_F32 -> fp32 SIMT path (the 1e-5 parity path). x: [n_in][c_in],
+ * w: [K^D][c_in][c_out], y: [n_out][c_out], all `dtype`. */
+
+/* conv_forward (exec.cpp:368-383) — dispatches on cfg->kind; implicit GEMM
+ * with reorder=offline prepares (cached) the map for cfg->splits. */
+sk_status sk_conv_forward(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, sk_dtype dtype,
+                          int c_in, int c_out, const void* d_x, const void* d_w, void* d_y,
+                          void* stream);
+/* conv_dgrad (exec.cpp:385-396): dx = dy through the transposed map with
+ * mirrored, transposed weights. dy: [n_out][c_out] -> dx: [n_in][c_in]. */
+sk_status sk_conv_dgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, sk_dtype dtype,
+                        int c_in, int c_out, const void* d_dy, const void* d_w, void* d_dx,
+                        void* stream);
+/* conv_wgrad (exec.cpp:398-414): dW_k = sum over pairs x_j^T dy_q.
+ * dw is fp32 [K^D][c_in][c_out] (master gradient), overwritten. */
+sk_status sk_conv_wgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, sk_dtype dtype,
+                        int c_in, int c_out, const void* d_x, const void* d_dy, float* d_dw,
+                        void* stream);
+
+/* ---- cost model (cost.hpp:31-62) ---------------------------------------------
+ * count_macs over the map prepared for (splits, pad) with warp_rows rows in
+ * lockstep (cost.cpp:7-30); syncs. */
+sk_status sk_kmap_count_macs(sk_kmap* map, int splits, int pad_multiple, int warp_rows,
+                             int c_in, int c_out, int64_t* effective, int64_t* redundant,
+                             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SK200_H */

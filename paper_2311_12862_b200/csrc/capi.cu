@@ -1,0 +1,357 @@
+// sk200 C ABI (include/sk200.h): handle lifetimes, error mapping, caches.
+// No C++ exception crosses this boundary.
+#include <cstring>
+
+#include "sk_internal.hpp"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+sk_status guard(F&& f) {
+    try {
+        f();
+        return SK_OK;
+    } catch (const sk::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return SK_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SK_ERR_INTERNAL;
+    }
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+void release_coords(sk_coords* c);
+void release_kmap(sk_kmap* m);
+
+}  // namespace
+
+sk_coords::~sk_coords() {
+    for (auto& kv : maps) release_kmap(kv.second);
+    for (auto& kv : down) release_coords(kv.second);
+}
+
+sk_kmap::~sk_kmap() {
+    if (transpose_cache) release_kmap(transpose_cache);
+}
+
+namespace {
+void release_coords(sk_coords* c) {
+    if (c && c->refs.fetch_sub(1) == 1) delete c;
+}
+void release_kmap(sk_kmap* m) {
+    if (m && m->refs.fetch_sub(1) == 1) delete m;
+}
+
+sk_coords* make_coords(sk_ctx* ctx, int dims, int n, const int32_t* src, bool host,
+                       const int32_t* stride_tag, cudaStream_t st) {
+    sk::validate(ctx != nullptr, "null context");
+    sk::validate(dims == 2 || dims == 3, "dims must be 2 or 3");
+    sk::validate(n >= 0, "negative coordinate count");
+    auto* c = new sk_coords();
+    try {
+        c->ctx = ctx;
+        c->dims = dims;
+        c->n = n;
+        c->id = sk::next_coord_set_id();
+        for (int d = 0; d < 3; ++d) c->stride_tag[d] = stride_tag ? stride_tag[d] : 1;
+        c->coords.alloc((size_t)std::max(n, 1) * 16, st);
+        if (n)
+            SK_CUDA(cudaMemcpyAsync(c->coords.p, src, (size_t)n * 16,
+                                    host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+        sk::coords_build_table(c, st);  // validates the packable range
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    return c;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+const char* sk_version(void) { return "sk200 0.1 (sm_100a)"; }
+
+sk_status sk_ctx_create(int device, sk_ctx** out) {
+    return guard([&] {
+        sk::validate(out != nullptr, "null output pointer");
+        SK_CUDA(cudaSetDevice(device));
+        auto* c = new sk_ctx();
+        c->device = device;
+        cudaDeviceProp prop;
+        SK_CUDA(cudaGetDeviceProperties(&prop, device));
+        c->num_sms = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
+        // keep freed blocks in the stream-ordered pool (no cudaFree syncs)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        *out = c;
+    });
+}
+
+sk_status sk_ctx_destroy(sk_ctx* ctx) {
+    return guard([&] { delete ctx; });
+}
+
+sk_status sk_ctx_set_deterministic(sk_ctx* ctx, int on) {
+    return guard([&] {
+        sk::validate(ctx != nullptr, "null context");
+        ctx->deterministic = on != 0;
+    });
+}
+
+sk_status sk_coords_create(sk_ctx* ctx, int dims, int n, const int32_t* d_coords,
+                           const int32_t stride_tag[3], void* stream, sk_coords** out) {
+    return guard([&] { *out = make_coords(ctx, dims, n, d_coords, false, stride_tag, S(stream)); });
+}
+
+sk_status sk_coords_create_host(sk_ctx* ctx, int dims, int n, const int32_t* h_coords,
+                                const int32_t stride_tag[3], void* stream, sk_coords** out) {
+    return guard([&] { *out = make_coords(ctx, dims, n, h_coords, true, stride_tag, S(stream)); });
+}
+
+sk_status sk_coords_retain(sk_coords* c) {
+    return guard([&] {
+        sk::validate(c != nullptr, "null coords");
+        c->refs.fetch_add(1);
+    });
+}
+
+sk_status sk_coords_release(sk_coords* c) {
+    return guard([&] { release_coords(c); });
+}
+
+int sk_coords_n(const sk_coords* c) { return c ? c->n : -1; }
+int sk_coords_dims(const sk_coords* c) { return c ? c->dims : -1; }
+uint64_t sk_coords_id(const sk_coords* c) { return c ? c->id : 0; }
+const int32_t* sk_coords_device_ptr(const sk_coords* c) {
+    return c ? c->coords.as<const int32_t>() : nullptr;
+}
+
+sk_status sk_coords_stride_tag(const sk_coords* c, int32_t out[3]) {
+    return guard([&] {
+        sk::validate(c != nullptr, "null coords");
+        for (int d = 0; d < 3; ++d) out[d] = c->stride_tag[d];
+    });
+}
+
+sk_status sk_coords_export(const sk_coords* c, int32_t* h, void* stream) {
+    return guard([&] {
+        if (c->n)
+            SK_CUDA(cudaMemcpyAsync(h, c->coords.p, (size_t)c->n * 16, cudaMemcpyDeviceToHost,
+                                    S(stream)));
+        SK_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+sk_status sk_out_coords(sk_ctx* ctx, sk_coords* in, const int32_t stride[3], void* stream,
+                        sk_coords** out) {
+    return guard([&] {
+        sk::validate(ctx && in && out, "null argument");
+        for (int d = 0; d < in->dims; ++d)
+            sk::validate(stride[d] >= 1, "stride components must be >= 1");
+        bool unit = true;
+        for (int d = 0; d < in->dims; ++d) unit = unit && stride[d] == 1;
+        if (unit) {  // submanifold: the same coordinate set (kmap.cpp:75-79)
+            in->refs.fetch_add(1);
+            *out = in;
+            return;
+        }
+        auto key = std::make_tuple(stride[0], stride[1], in->dims == 3 ? stride[2] : 1);
+        std::lock_guard<std::mutex> lock(in->mu);
+        auto it = in->down.find(key);
+        if (it == in->down.end()) {
+            sk_coords* c = sk::coords_downsample(in, stride, S(stream));
+            it = in->down.emplace(key, c).first;
+        }
+        it->second->refs.fetch_add(1);
+        *out = it->second;
+    });
+}
+
+sk_status sk_kmap_build(sk_ctx* ctx, sk_coords* in, sk_coords* out, int kernel_size,
+                        const int32_t stride[3], int transposed, void* stream, sk_kmap** map) {
+    return guard([&] {
+        sk::validate(ctx && in && out && map, "null argument");
+        auto key = std::make_tuple(out->id, kernel_size, stride[0], stride[1],
+                                   in->dims == 3 ? stride[2] : 1, transposed ? 1 : 0);
+        sk_kmap* m = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(in->mu);
+            auto it = in->maps.find(key);
+            if (it != in->maps.end()) m = it->second;
+        }
+        if (!m) {
+            sk_kmap* built = sk::kmap_build(in, out, kernel_size, stride, transposed, S(stream));
+            std::lock_guard<std::mutex> lock(in->mu);
+            auto ins = in->maps.emplace(key, built);
+            if (!ins.second) release_kmap(built);  // lost a race: builds once per key
+            m = ins.first->second;
+        }
+        m->refs.fetch_add(1);
+        *map = m;
+    });
+}
+
+sk_status sk_kmap_transpose(sk_ctx* ctx, sk_kmap* map, void* stream, sk_kmap** out) {
+    return guard([&] {
+        sk::validate(ctx && map && out, "null argument");
+        sk_kmap* t = sk::kmap_transpose(map, S(stream));
+        t->refs.fetch_add(1);
+        *out = t;
+    });
+}
+
+sk_status sk_kmap_prepare(sk_ctx* ctx, sk_kmap* map, int splits, int pad_multiple, void* stream) {
+    return guard([&] {
+        sk::validate(ctx && map, "null argument");
+        sk::kmap_prepare(map, splits, pad_multiple, S(stream));
+    });
+}
+
+sk_status sk_kmap_retain(sk_kmap* map) {
+    return guard([&] { map->refs.fetch_add(1); });
+}
+
+sk_status sk_kmap_release(sk_kmap* map) {
+    return guard([&] { release_kmap(map); });
+}
+
+sk_status sk_kmap_get_info(sk_kmap* m, void* stream, sk_kmap_info* info) {
+    return guard([&] {
+        info->dims = m->dims;
+        info->kernel_size = m->kernel;
+        info->num_offsets = m->kd;
+        info->n_in = m->n_in;
+        info->n_out = m->n_out;
+        info->transposed = m->transposed;
+        for (int d = 0; d < 3; ++d) info->stride[d] = m->stride[d];
+        info->total_pairs = sk::kmap_total_pairs(m, S(stream));
+    });
+}
+
+sk_status sk_kmap_export_os(sk_kmap* m, int32_t* h_entries, uint64_t* h_masks, void* stream) {
+    return guard([&] {
+        cudaStream_t st = S(stream);
+        if (m->n_out) {
+            SK_CUDA(cudaMemcpyAsync(h_entries, m->os.p, (size_t)m->n_out * m->kd * 4,
+                                    cudaMemcpyDeviceToHost, st));
+            SK_CUDA(cudaMemcpyAsync(h_masks, m->masks.p, (size_t)m->n_out * m->words * 8,
+                                    cudaMemcpyDeviceToHost, st));
+        }
+        SK_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+sk_status sk_kmap_export_ws(sk_kmap* m, int64_t* h_ptr, int32_t* h_in, int32_t* h_out,
+                            void* stream) {
+    return guard([&] {
+        cudaStream_t st = S(stream);
+        sk::kmap_ensure_ws(m, st);
+        SK_CUDA(cudaMemcpyAsync(h_ptr, m->ws_ptr.p, (size_t)(m->kd + 1) * 8,
+                                cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        const int64_t P = h_ptr[m->kd];
+        if (P > 0 && h_in) {
+            SK_CUDA(cudaMemcpyAsync(h_in, m->ws_in.p, (size_t)P * 4, cudaMemcpyDeviceToHost, st));
+            SK_CUDA(cudaMemcpyAsync(h_out, m->ws_out.p, (size_t)P * 4, cudaMemcpyDeviceToHost, st));
+        }
+        SK_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+sk_status sk_kmap_export_split(sk_kmap* m, int splits, int pad_multiple, int s, int* begin,
+                               int* end, int* n_rows, int* mask_words, int32_t* h_entries,
+                               int32_t* h_out_row, uint64_t* h_masks, void* stream) {
+    return guard([&] {
+        cudaStream_t st = S(stream);
+        sk::Prepared* p = sk::kmap_prepare(m, splits, pad_multiple, st);
+        sk::validate(s >= 0 && s < p->num_splits, "split index out of range");
+        const int b = p->begin[s], e = p->begin[s + 1], w = e - b, words = (w + 63) / 64;
+        // the reference pads to exactly `pad_multiple` (kmap.cpp:274-288)
+        const int rows = (int)(sk::ceil_div(m->n_out, pad_multiple) * pad_multiple);
+        *begin = b;
+        *end = e;
+        *n_rows = rows;
+        *mask_words = words;
+        if (h_entries) {
+            // device rows are padded to lcm(pad, 128) >= rows; the tail is pad rows
+            SK_CUDA(cudaMemcpyAsync(h_entries, p->entries.as<int32_t>() + (size_t)p->rows_pad * b,
+                                    (size_t)rows * w * 4, cudaMemcpyDeviceToHost, st));
+            SK_CUDA(cudaMemcpyAsync(h_out_row, p->out_row.as<int32_t>() + (size_t)s * p->rows_pad,
+                                    (size_t)rows * 4, cudaMemcpyDeviceToHost, st));
+            SK_CUDA(cudaMemcpyAsync(h_masks,
+                                    p->masks.as<uint64_t>() + (size_t)p->rows_pad * p->word_off[s],
+                                    (size_t)rows * words * 8, cudaMemcpyDeviceToHost, st));
+        }
+        SK_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+sk_status sk_conv_forward(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, sk_dtype dtype,
+                          int c_in, int c_out, const void* d_x, const void* d_w, void* d_y,
+                          void* stream) {
+    return guard([&] {
+        sk::validate(ctx && map && cfg, "null argument");
+        sk::conv_forward(ctx, map, *cfg, dtype, c_in, c_out, d_x, d_w, d_y, false, S(stream));
+    });
+}
+
+sk_status sk_conv_dgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, sk_dtype dtype,
+                        int c_in, int c_out, const void* d_dy, const void* d_w, void* d_dx,
+                        void* stream) {
+    return guard([&] {
+        sk::validate(ctx && map && cfg, "null argument");
+        sk::conv_forward(ctx, map, *cfg, dtype, c_in, c_out, d_dy, d_w, d_dx, true, S(stream));
+    });
+}
+
+sk_status sk_conv_wgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, sk_dtype dtype,
+                        int c_in, int c_out, const void* d_x, const void* d_dy, float* d_dw,
+                        void* stream) {
+    return guard([&] {
+        sk::validate(ctx && map && cfg, "null argument");
+        sk::conv_wgrad(ctx, map, *cfg, dtype, c_in, c_out, d_x, d_dy, d_dw, S(stream));
+    });
+}
+
+sk_status sk_kmap_count_macs(sk_kmap* m, int splits, int pad_multiple, int warp_rows, int c_in,
+                             int c_out, int64_t* effective, int64_t* redundant, void* stream) {
+    return guard([&] {
+        // count_macs (cost.cpp:7-30) over the exported prepared splits
+        cudaStream_t st = S(stream);
+        sk::Prepared* p = sk::kmap_prepare(m, splits, pad_multiple, st);
+        const int rows = (int)(sk::ceil_div(m->n_out, pad_multiple) * pad_multiple);
+        int64_t eff = 0, charged = 0;
+        const int64_t unit = (int64_t)c_in * c_out;
+        for (int s = 0; s < p->num_splits; ++s) {
+            const int b = p->begin[s], w = p->begin[s + 1] - b;
+            std::vector<int32_t> e((size_t)rows * w);
+            if (!e.empty())
+                SK_CUDA(cudaMemcpyAsync(e.data(), p->entries.as<int32_t>() + (size_t)p->rows_pad * b,
+                                        e.size() * 4, cudaMemcpyDeviceToHost, st));
+            SK_CUDA(cudaStreamSynchronize(st));
+            for (int32_t v : e) eff += v != -1;
+            for (int r0 = 0; r0 < rows; r0 += warp_rows)
+                for (int j = 0; j < w; ++j) {
+                    bool act = false;
+                    for (int r = r0; r < std::min(rows, r0 + warp_rows) && !act; ++r)
+                        act = e[(size_t)r * w + j] != -1;
+                    if (act) charged += (int64_t)warp_rows * unit;
+                }
+        }
+        *effective = eff * unit;
+        *redundant = charged - eff * unit;
+    });
+}
+
+}  // extern "C"

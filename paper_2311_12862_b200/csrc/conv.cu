@@ -1,0 +1,889 @@
+// sk200 sparse-convolution dataflows on sm_100a (hot path (2)).
+//
+// All three reference dataflows (exec.cpp:117-257) reduce to one primitive,
+// a GATHERED GEMM over 128-row tiles:
+//
+//   for each work item (tile of 128 rows, N-tile):
+//     acc[128 x BN] = sum over k-steps (offset k, channel chunk c) of
+//                     A_rows(k)[128 x KC] * B_k[KC x BN]
+//     epilogue: rows -> output rows (store / fp32 red.add / fp32 RMW)
+//
+//  * implicit GEMM (exec.cpp:206-257): rows = prepared OS rows of one split,
+//    A row = x[entries[row][k]] (sentinel -> zero-filled), k-steps = offsets
+//    whose bit is set in the tile's OR-mask (sorted masks => empty offsets
+//    skipped per tile), output row = out_row[row];
+//  * fetch-on-demand (exec.cpp:160-201): rows = the WS pairs of one offset,
+//    A row = x[in[p]], output row = out[p] accumulated with fp32 red.add;
+//  * gather-GEMM-scatter (exec.cpp:117-158): explicit gather kernel, the same
+//    GEMM over the gathered buffer (identity rows), scatter-add kernel.
+//  * dgrad (exec.cpp:385-396) = the same over the transposed map with the
+//    mirrored offset and B = W[k'] read as [c_in][c_out] (already K-major);
+//    forward uses B = W^T (a tiny per-call transpose to [k][c_out][c_in]).
+//
+// fp16/bf16 -> k_gconv_tc: warp-specialised tcgen05 kernel
+//   warps 0-3  producers: cp.async 16B gathers of A rows (zero-fill for
+//              sentinels/channel tails) and B rows into 128B/64B/32B-swizzled
+//              K-major smem stages; cp.async.wait_group + fence.proxy.async +
+//              mbarrier arrive publish a stage LAG steps later
+//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
+//              N=BN, K=16 per instruction), tcgen05.commit frees stages
+//   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
+//              buffered TMEM accumulators so tile i's epilogue overlaps tile
+//              i+1's MMAs
+// fp32 -> k_gconv_simt: the 1e-5 parity path (FFMA, fp32 accumulate).
+#include "sk_internal.hpp"
+
+namespace sk {
+
+namespace {
+
+constexpr int kThreadsTC = 288;  // 9 warps
+constexpr int kProducerThreads = 128;
+constexpr int kLag = 2;
+
+struct ConvArgs {
+    int mode;  // 0 = OS rows (implicit GEMM), 1 = WS pairs (FOD / GGS GEMM)
+    // OS mode
+    const int* entries;
+    const int* out_row;  // nullable: identity rows < n_rows_valid
+    const unsigned long long* tile_masks;
+    const int* split_begin;
+    int ns, rows_pad, n_tiles, n_rows_valid;
+    // WS mode
+    const long long* ws_ptr;
+    const int* ws_tile_ptr;
+    const int* ws_in;
+    const int* ws_out;
+    int a_identity, out_identity;
+    int kd;
+    // operands
+    const void* a;
+    int k_total;
+    const void* b;
+    int n_total, mirror;
+    void* y;
+    int out_mode;  // 0 store T, 1 store f32, 2 red.add f32, 3 RMW f32
+    int ld_y;
+    int n_ntiles, bn;
+    int items;  // OS mode item count (WS mode: derived on device)
+    int split_only;  // >= 0: only items of this split (deterministic sequencing)
+    int offset_only; // >= 0: WS mode only tiles of this offset
+};
+
+struct Item {
+    bool valid;
+    int s, t, nt, k;   // split / tile / n-tile / offset (WS)
+    int w;             // split width (OS) or 1 (WS)
+    int col_begin;     // global offset of column 0
+    long long row0;    // first row: OS tile row, or first pair index (WS)
+    long long row_end; // WS: end of this offset's pairs
+    unsigned long long m0, m1;
+    int biw0, bw1;
+};
+
+__device__ __forceinline__ int ws_items(const ConvArgs& p) {
+    if (p.offset_only >= 0)
+        return (p.ws_tile_ptr[p.offset_only + 1] - p.ws_tile_ptr[p.offset_only]) * p.n_ntiles;
+    return p.ws_tile_ptr[p.kd] * p.n_ntiles;
+}
+
+__device__ __forceinline__ int num_items(const ConvArgs& p) {
+    return p.mode == 0 ? p.items : ws_items(p);
+}
+
+__device__ Item decode(const ConvArgs& p, int item) {
+    Item it;
+    it.valid = true;
+    if (p.mode == 0) {
+        const int per = p.n_tiles * p.n_ntiles;
+        it.s = p.split_only >= 0 ? p.split_only : item / per;
+        const int rem = p.split_only >= 0 ? item : item % per;
+        it.t = rem / p.n_ntiles;
+        it.nt = rem % p.n_ntiles;
+        it.col_begin = p.split_begin[it.s];
+        it.w = p.split_begin[it.s + 1] - it.col_begin;
+        it.row0 = (long long)it.t * kTileM;
+        it.row_end = 0;
+        it.k = -1;
+        const unsigned long long* tm = p.tile_masks + ((size_t)it.s * p.n_tiles + it.t) * 2;
+        it.m0 = tm[0];
+        it.m1 = tm[1];
+        it.biw0 = it.w < 64 ? it.w : 64;
+        it.bw1 = it.w - 64;
+    } else {
+        int tile = item / p.n_ntiles;
+        it.nt = item % p.n_ntiles;
+        int k = 0;
+        if (p.offset_only >= 0) {
+            k = p.offset_only;
+            tile += p.ws_tile_ptr[k];
+        } else {
+            while (k + 1 <= p.kd && p.ws_tile_ptr[k + 1] <= tile) ++k;
+        }
+        it.k = k;
+        it.s = 0;
+        it.t = tile - p.ws_tile_ptr[k];
+        it.w = 1;
+        it.col_begin = k;
+        it.row0 = p.ws_ptr[k] + (long long)it.t * kTileM;
+        it.row_end = p.ws_ptr[k + 1];
+        it.m0 = 1;  // one active "column"
+        it.m1 = 0;
+        it.biw0 = 1;
+        it.bw1 = 0;
+    }
+    return it;
+}
+
+// Iterate active columns in ascending order. Returns -1 when done.
+__device__ __forceinline__ int next_col(unsigned long long& m0, unsigned long long& m1, int biw0,
+                                        int bw1) {
+    if (m0) {
+        int hb = 63 - __clzll((long long)m0);
+        m0 &= ~(1ull << hb);
+        return biw0 - 1 - hb;
+    }
+    if (m1) {
+        int hb = 63 - __clzll((long long)m1);
+        m1 &= ~(1ull << hb);
+        return 64 + bw1 - 1 - hb;
+    }
+    return -1;
+}
+
+// A-row index for tile row r at (split-local) column j; -1 = zero row
+__device__ __forceinline__ int a_index(const ConvArgs& p, const Item& it, int r, int j) {
+    if (p.mode == 0) {
+        const long long row = it.row0 + r;
+        return __ldg(p.entries + (size_t)p.rows_pad * it.col_begin + (size_t)row * it.w + j);
+    }
+    const long long pi = it.row0 + r;
+    if (pi >= it.row_end) return -1;
+    return p.a_identity ? (int)pi : __ldg(p.ws_in + pi);
+}
+
+__device__ __forceinline__ long long out_index(const ConvArgs& p, const Item& it, int r) {
+    if (p.mode == 0) {
+        const long long row = it.row0 + r;
+        if (p.out_row) return __ldg(p.out_row + (size_t)it.s * p.rows_pad + row);
+        return row < p.n_rows_valid ? row : -1;
+    }
+    const long long pi = it.row0 + r;
+    if (pi >= it.row_end) return -1;
+    return p.out_identity ? pi : (long long)__ldg(p.ws_out + pi);
+}
+
+template <typename T>
+struct Fmt;
+template <>
+struct Fmt<__half> {
+    static constexpr uint32_t v = 0;
+};
+template <>
+struct Fmt<__nv_bfloat16> {
+    static constexpr uint32_t v = 1;
+};
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, __half*) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b, __nv_bfloat16*) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+// K-major smem descriptor; row = KC*2 bytes, 8-row swizzle atoms.
+template <int KC>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr) {
+    constexpr uint32_t RB = KC * 2;                       // 32 / 64 / 128
+    constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);  // SW128/SW64/SW32
+    constexpr uint64_t sbo = (8 * RB) >> 4;
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | (sbo << 32) | (1ull << 46) | (layout << 61);
+}
+
+// byte offset of 16B chunk q of row r inside a K-major swizzled tile
+template <int KC>
+__device__ __forceinline__ uint32_t swz(int r, int q) {
+    constexpr uint32_t RB = KC * 2;
+    constexpr uint32_t B = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
+    uint32_t off = (uint32_t)r * RB + (uint32_t)q * 16;
+    return off ^ (((off >> 7) & B) << 4);
+}
+
+template <typename T, int KC>
+__global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, int stages) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024B alignment for the swizzle atoms
+    uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int BN = p.bn;
+    const uint32_t a_bytes = kTileM * KC * 2;
+    const uint32_t b_bytes = (uint32_t)BN * KC * 2;
+    const uint32_t stage_bytes = a_bytes + b_bytes;
+    uint8_t* stage_base = smem;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + stages;
+    uint64_t* tfull = bars + 2 * stages;
+    uint64_t* tempty = bars + 2 * stages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint32_t ncols = 32;
+    while (ncols < (uint32_t)(2 * BN)) ncols <<= 1;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < stages; ++i) {
+            mbar_init(&full[i], kProducerThreads);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 4) tmem_alloc(tmem_slot, ncols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int n_items = num_items(p);
+    const int nchunks = (p.k_total + KC - 1) / KC;
+    const T* __restrict__ A = static_cast<const T*>(p.a);
+    const T* __restrict__ Bw = static_cast<const T*>(p.b);
+
+    if (warp < 4) {
+        // ================= producers =================
+        const int r = threadIdx.x;  // tile row owned by this thread
+        long long step = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+            Item it = decode(p, item);
+            unsigned long long m0 = it.m0, m1 = it.m1;
+            const int n0 = it.nt * BN;
+            for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
+                 j = next_col(m0, m1, it.biw0, it.bw1)) {
+                const int ai = a_index(p, it, r, j);
+                const int kg = it.col_begin + j;
+                const int kb = p.mirror ? p.kd - 1 - kg : kg;
+                const T* arow = A + (size_t)(ai < 0 ? 0 : ai) * p.k_total;
+                for (int c = 0; c < nchunks; ++c, ++step) {
+                    const int stage = (int)(step % stages);
+                    const uint32_t ph = (uint32_t)((step / stages) & 1);
+                    mbar_wait(&empty[stage], ph ^ 1);
+                    uint8_t* sa = stage_base + (size_t)stage * stage_bytes;
+                    uint8_t* sb = sa + a_bytes;
+                    const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
+#pragma unroll
+                    for (int q = 0; q < KC / 8; ++q) {
+                        const int col = c * KC + q * 8;
+                        const bool ok = ai >= 0 && col < p.k_total;
+                        cp_async16(sa_u + swz<KC>(r, q), ok ? (const void*)(arow + col) : (const void*)A,
+                                   ok ? 16u : 0u);
+                    }
+                    for (int i = threadIdx.x; i < BN * (KC / 8); i += kProducerThreads) {
+                        const int n = i / (KC / 8), q = i % (KC / 8);
+                        const int col = c * KC + q * 8;
+                        const bool ok = (n0 + n) < p.n_total && col < p.k_total;
+                        const T* src = Bw + ((size_t)kb * p.n_total + n0 + n) * p.k_total + col;
+                        cp_async16(sb_u + swz<KC>(n, q), ok ? (const void*)src : (const void*)Bw,
+                                   ok ? 16u : 0u);
+                    }
+                    cp_async_commit();
+                    if (step >= kLag) {
+                        cp_async_wait<kLag>();
+                        fence_proxy_async_smem();
+                        mbar_arrive(&full[(int)((step - kLag) % stages)]);
+                    }
+                }
+            }
+        }
+        // drain the last kLag stages
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        for (long long s = step - kLag < 0 ? 0 : step - kLag; s < step; ++s)
+            mbar_arrive(&full[(int)(s % stages)]);
+    } else if (warp == 4) {
+        // ================= MMA issuer =================
+        const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
+                               ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+        long long step = 0;
+        int local = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+            Item it = decode(p, item);
+            const int acc = local & 1;
+            const uint32_t aph = (uint32_t)((local >> 1) & 1);
+            mbar_wait(&tempty[acc], aph ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
+            unsigned long long m0 = it.m0, m1 = it.m1;
+            bool first = true;
+            for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
+                 j = next_col(m0, m1, it.biw0, it.bw1)) {
+                for (int c = 0; c < nchunks; ++c, ++step) {
+                    const int stage = (int)(step % stages);
+                    const uint32_t ph = (uint32_t)((step / stages) & 1);
+                    mbar_wait(&full[stage], ph);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
+                        const uint32_t sb = sa + a_bytes;
+#pragma unroll
+                        for (int kk = 0; kk < KC / 16; ++kk) {
+                            tc_mma_f16(d_tmem, kmajor_desc<KC>(sa + kk * 32),
+                                       kmajor_desc<KC>(sb + kk * 32), idesc,
+                                       (first && kk == 0) ? 0u : 1u);
+                        }
+                        tc_commit(&empty[stage]);
+                    }
+                    __syncwarp();
+                    first = false;
+                }
+            }
+            if (lane == 0) tc_commit(&tfull[acc]);
+            __syncwarp();
+        }
+    } else {
+        // ================= epilogue =================
+        const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        const int r = quad * 32 + lane;
+        int local = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+            Item it = decode(p, item);
+            const int acc = local & 1;
+            const uint32_t aph = (uint32_t)((local >> 1) & 1);
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const long long orow = out_index(p, it, r);
+            const bool empty_tile = (it.m0 | it.m1) == 0;
+            const int n0 = it.nt * BN;
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                if (!empty_tile) {
+                    tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = 0;
+                }
+                const int col = n0 + c0;
+                if (orow < 0 || col >= p.n_total) continue;
+                if (p.out_mode == 0) {
+                    T* dst = static_cast<T*>(p.y) + (size_t)orow * p.ld_y + col;
+                    uint4 u0, u1;
+                    u0.x = pack2(__uint_as_float(v[0]), __uint_as_float(v[1]), (T*)nullptr);
+                    u0.y = pack2(__uint_as_float(v[2]), __uint_as_float(v[3]), (T*)nullptr);
+                    u0.z = pack2(__uint_as_float(v[4]), __uint_as_float(v[5]), (T*)nullptr);
+                    u0.w = pack2(__uint_as_float(v[6]), __uint_as_float(v[7]), (T*)nullptr);
+                    u1.x = pack2(__uint_as_float(v[8]), __uint_as_float(v[9]), (T*)nullptr);
+                    u1.y = pack2(__uint_as_float(v[10]), __uint_as_float(v[11]), (T*)nullptr);
+                    u1.z = pack2(__uint_as_float(v[12]), __uint_as_float(v[13]), (T*)nullptr);
+                    u1.w = pack2(__uint_as_float(v[14]), __uint_as_float(v[15]), (T*)nullptr);
+                    reinterpret_cast<uint4*>(dst)[0] = u0;
+                    reinterpret_cast<uint4*>(dst)[1] = u1;
+                } else {
+                    float* dst = static_cast<float*>(p.y) + (size_t)orow * p.ld_y + col;
+                    if (p.out_mode == 2) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            red_add_v4(dst + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                       __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4) {
+                            float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                   __uint_as_float(v[i + 2]),
+                                                   __uint_as_float(v[i + 3]));
+                            if (p.out_mode == 3) {
+                                float4 prev = *reinterpret_cast<float4*>(dst + i);
+                                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
+                            }
+                            *reinterpret_cast<float4*>(dst + i) = o;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 4) tmem_dealloc(tmem, ncols);
+}
+
+// ---------------------------------------------------------------------------
+// SIMT fp32 path: 128 rows x 64 cols per item, 256 threads, 8x4 per thread.
+constexpr int kSimtN = 64;
+constexpr int kSimtK = 16;
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v) { return (float)v; }
+template <>
+__device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __half from_f<__half>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
+    __shared__ float As[kSimtK][kTileM + 4];
+    __shared__ float Bs[kSimtK][kSimtN + 4];
+    __shared__ int aidx[kTileM];
+    const int tid = threadIdx.x;
+    const int tr = tid / 16, tc = tid % 16;  // 16 x 16 threads; rows tr*8.., cols tc*4..
+    const T* __restrict__ A = static_cast<const T*>(p.a);
+    const T* __restrict__ Bw = static_cast<const T*>(p.b);
+    const int n_items = num_items(p);
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        Item it = decode(p, item);
+        const int n0 = it.nt * kSimtN;
+        float acc[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+        unsigned long long m0 = it.m0, m1 = it.m1;
+        for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
+             j = next_col(m0, m1, it.biw0, it.bw1)) {
+            const int kg = it.col_begin + j;
+            const int kb = p.mirror ? p.kd - 1 - kg : kg;
+            __syncthreads();
+            if (tid < kTileM) aidx[tid] = a_index(p, it, tid, j);
+            __syncthreads();
+            for (int c0 = 0; c0 < p.k_total; c0 += kSimtK) {
+                for (int i = tid; i < kTileM * kSimtK; i += 256) {
+                    const int r = i / kSimtK, kk = i % kSimtK;
+                    const int ai = aidx[r];
+                    As[kk][r] = (ai >= 0 && c0 + kk < p.k_total)
+                                    ? to_f(A[(size_t)ai * p.k_total + c0 + kk]) : 0.f;
+                }
+                for (int i = tid; i < kSimtN * kSimtK; i += 256) {
+                    const int n = i / kSimtK, kk = i % kSimtK;
+                    Bs[kk][n] = (n0 + n < p.n_total && c0 + kk < p.k_total)
+                                    ? to_f(Bw[((size_t)kb * p.n_total + n0 + n) * p.k_total + c0 + kk])
+                                    : 0.f;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int kk = 0; kk < kSimtK; ++kk) {
+                    float a[8], b[4];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) a[i] = As[kk][tr * 8 + i];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) b[i] = Bs[kk][tc * 4 + i];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(a[i], b[jj], acc[i][jj]);
+                }
+                __syncthreads();
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long long orow = out_index(p, it, tr * 8 + i);
+            if (orow < 0) continue;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int col = n0 + tc * 4 + jj;
+                if (col >= p.n_total) continue;
+                const size_t o = (size_t)orow * p.ld_y + col;
+                if (p.out_mode == 0) static_cast<T*>(p.y)[o] = from_f<T>(acc[i][jj]);
+                else if (p.out_mode == 1) static_cast<float*>(p.y)[o] = acc[i][jj];
+                else if (p.out_mode == 2) atomicAdd(static_cast<float*>(p.y) + o, acc[i][jj]);
+                else static_cast<float*>(p.y)[o] += acc[i][jj];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// glue kernels
+
+template <typename T>
+__global__ void k_transpose_w(const T* __restrict__ w, int kd, int c_in, int c_out,
+                              T* __restrict__ wt) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long tot = (long long)kd * c_in * c_out;
+    if (i >= tot) return;
+    int k = (int)(i / ((long long)c_in * c_out));
+    int rem = (int)(i % ((long long)c_in * c_out));
+    int ci = rem / c_out, co = rem % c_out;
+    wt[((size_t)k * c_out + co) * c_in + ci] = w[i];
+}
+
+template <typename T>
+__global__ void k_convert_out(const float* __restrict__ src, long long n, T* __restrict__ dst) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = from_f<T>(src[i]);
+}
+
+// GGS gather: buf[p] = x[in[p]] (16B vectors; c multiple of 8 elements of T
+// for 2-byte T, or scalar fallback)
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ x, int c, const int* __restrict__ idx,
+                              const long long* __restrict__ total, T* __restrict__ buf) {
+    const long long n = *total;
+    const long long nelem = n * c;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long pr = i / c;
+        int cc = (int)(i % c);
+        buf[i] = x[(size_t)idx[pr] * c + cc];
+    }
+}
+
+// GGS scatter-add into fp32 accumulator: y[out[p]] += buf[p]
+__global__ void k_scatter_add(const float* __restrict__ buf, int c, const int* __restrict__ idx,
+                              const long long* __restrict__ lo, const long long* __restrict__ hi,
+                              float* __restrict__ y, int deterministic) {
+    const long long a = *lo, b = *hi;
+    const long long nelem = (b - a) * c;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long pr = a + i / c;
+        int cc = (int)(i % c);
+        float v = buf[pr * c + cc];
+        float* d = y + (size_t)idx[pr] * c + cc;
+        if (deterministic) *d += v;  // one offset at a time: out rows unique
+        else atomicAdd(d, v);
+    }
+}
+
+// wgrad SIMT: one block per (offset, ci-tile 32, co-tile 32, pair-chunk);
+// dW_k[ci][co] += sum_p x[in[p]][ci] * dy[out[p]][co], fp32 atomics across
+// pair chunks (deterministic: one chunk).
+template <typename T>
+__global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
+                                                    const T* __restrict__ dy, int c_in, int c_out,
+                                                    const long long* __restrict__ ptr,
+                                                    const int* __restrict__ ws_in,
+                                                    const int* __restrict__ ws_out, int chunk,
+                                                    float* __restrict__ dw) {
+    __shared__ float xs[32][33];
+    __shared__ float ds[32][33];
+    const int k = blockIdx.z;
+    const int ci0 = (blockIdx.y / ((c_out + 31) / 32)) * 32;
+    const int co0 = (blockIdx.y % ((c_out + 31) / 32)) * 32;
+    const long long lo = ptr[k], hi = ptr[k + 1];
+    const long long p0 = lo + (long long)blockIdx.x * chunk;
+    if (p0 >= hi) return;
+    const long long p1 = min(hi, p0 + chunk);
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+    float acc[4] = {0, 0, 0, 0};
+    for (long long pb = p0; pb < p1; pb += 32) {
+        for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+            int pp = i / 32, cc = i % 32;
+            long long pr = pb + pp;
+            bool ok = pr < p1;
+            xs[pp][cc] = (ok && ci0 + cc < c_in) ? to_f(x[(size_t)ws_in[pr] * c_in + ci0 + cc]) : 0.f;
+            ds[pp][cc] = (ok && co0 + cc < c_out) ? to_f(dy[(size_t)ws_out[pr] * c_out + co0 + cc]) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int pp = 0; pp < 32; ++pp) {
+            float d = ds[pp][tx];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fmaf(xs[pp][ty * 4 + u], d, acc[u]);
+        }
+        __syncthreads();
+    }
+    for (int u = 0; u < 4; ++u) {
+        int ci = ci0 + ty * 4 + u, co = co0 + tx;
+        if (ci < c_in && co < c_out) atomicAdd(&dw[((size_t)k * c_in + ci) * c_out + co], acc[u]);
+    }
+}
+
+size_t elem_size(sk_dtype dt) { return dt == SK_F32 ? 4 : 2; }
+
+struct Launch {
+    sk_ctx* ctx;
+    cudaStream_t st;
+};
+
+template <typename T, int KC>
+void launch_tc_kc(const ConvArgs& a, int grid, cudaStream_t st) {
+    const int bn = a.bn;
+    const size_t stage_bytes = (size_t)kTileM * KC * 2 + (size_t)bn * KC * 2;
+    int stages = (int)std::min<size_t>(8, (200 * 1024) / stage_bytes);
+    stages = std::max(stages, 3);
+    const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+    SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages);
+    SK_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_tc(const ConvArgs& a, int grid, cudaStream_t st) {
+    if (a.k_total % 64 == 0) launch_tc_kc<T, 64>(a, grid, st);
+    else if (a.k_total % 32 == 0) launch_tc_kc<T, 32>(a, grid, st);
+    else launch_tc_kc<T, 16>(a, grid, st);
+}
+
+bool tc_ok(sk_dtype dt, int k_total, int n_total) {
+    return dt != SK_F32 && k_total % 8 == 0 && n_total % 16 == 0;
+}
+
+// pick the N tile: whole C_out when <= 256, else balanced tiles of <= 256
+void pick_n_tiling(int n_total, int cta_n, bool tc, int& bn, int& n_nt) {
+    if (!tc) {
+        bn = kSimtN;
+        n_nt = (int)ceil_div(n_total, kSimtN);
+        return;
+    }
+    int cap = cta_n > 0 ? std::min(cta_n, 256) : 256;
+    cap = std::max(16, cap / 16 * 16);
+    n_nt = (int)ceil_div(n_total, cap);
+    bn = (int)ceil_div(ceil_div(n_total, n_nt), 16) * 16;
+}
+
+void launch_gconv(sk_ctx* ctx, sk_dtype dt, ConvArgs a, bool ws_mode_grid, cudaStream_t st) {
+    const bool tc = tc_ok(dt, a.k_total, a.n_total);
+    int grid;
+    if (a.mode == 0) {
+        grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
+    } else {
+        (void)ws_mode_grid;
+        grid = ctx->num_sms * (tc ? 1 : 8);
+    }
+    if (tc) {
+        if (dt == SK_F16) launch_tc<__half>(a, grid, st);
+        else launch_tc<__nv_bfloat16>(a, grid, st);
+    } else {
+        if (dt == SK_F32) k_gconv_simt<float><<<grid, 256, 0, st>>>(a);
+        else if (dt == SK_F16) k_gconv_simt<__half><<<grid, 256, 0, st>>>(a);
+        else k_gconv_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(a);
+        SK_LAUNCH_CHECK();
+    }
+}
+
+template <typename T>
+void convert_out(const float* src, long long n, void* dst, cudaStream_t st) {
+    if (n <= 0) return;
+    k_convert_out<T><<<(int)ceil_div(n, 256), 256, 0, st>>>(src, n, static_cast<T*>(dst));
+    SK_LAUNCH_CHECK();
+}
+
+void convert_from_f32(sk_dtype dt, const float* src, long long n, void* dst, cudaStream_t st) {
+    if (dt == SK_F16) convert_out<__half>(src, n, dst, st);
+    else if (dt == SK_BF16) convert_out<__nv_bfloat16>(src, n, dst, st);
+    else SK_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, st));
+}
+
+ConvArgs base_args() {
+    ConvArgs a;
+    memset(&a, 0, sizeof(a));
+    a.split_only = -1;
+    a.offset_only = -1;
+    return a;
+}
+
+}  // namespace
+
+// Forward (dgrad = false) or dgrad (dgrad = true; m is the FORWARD map).
+void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
+                  int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st) {
+    validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
+    validate(cfg.splits >= 0, "splits must be >= 0");
+    validate(cfg.kind >= 0 && cfg.kind <= 2, "unknown dataflow kind");
+    sk_kmap* m = dgrad ? kmap_transpose(m_fwd, st) : m_fwd;
+    // GEMM shape: A rows have k_total channels, output has n_total channels
+    const int k_total = dgrad ? c_out : c_in;
+    const int n_total = dgrad ? c_in : c_out;
+    const size_t es = elem_size(dt);
+    const long long y_elems = (long long)m->n_out * n_total;
+    if (m->n_out == 0) return;
+
+    // B operand: forward -> W^T [kd][c_out][c_in]; dgrad -> W [kd][c_in][c_out]
+    // with mirrored offsets (WeightTensor::transposed, exec.cpp:32-43)
+    DevBuf wt;
+    const void* b = w;
+    if (!dgrad) {
+        wt.alloc((size_t)m->kd * c_in * c_out * es, st);
+        long long tot = (long long)m->kd * c_in * c_out;
+        const int g = (int)ceil_div(tot, 256);
+        if (dt == SK_F32) k_transpose_w<float><<<g, 256, 0, st>>>((const float*)w, m->kd, c_in, c_out, wt.as<float>());
+        else if (dt == SK_F16) k_transpose_w<__half><<<g, 256, 0, st>>>((const __half*)w, m->kd, c_in, c_out, wt.as<__half>());
+        else k_transpose_w<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)w, m->kd, c_in, c_out, wt.as<__nv_bfloat16>());
+        SK_LAUNCH_CHECK();
+        b = wt.p;
+    }
+    const bool tc = tc_ok(dt, k_total, n_total);
+    ConvArgs a = base_args();
+    a.kd = m->kd;
+    a.a = x;
+    a.k_total = k_total;
+    a.b = b;
+    a.n_total = n_total;
+    a.mirror = dgrad ? 1 : 0;
+    a.ld_y = n_total;
+    pick_n_tiling(n_total, cfg.tile.cta_n, tc, a.bn, a.n_ntiles);
+    const bool det = ctx->deterministic;
+
+    if (cfg.kind == SK_IMPLICIT_GEMM) {
+        Prepared* pr = kmap_prepare(m, cfg.splits, kTileM, st);
+        DevBuf d_begin;
+        d_begin.alloc((pr->num_splits + 1) * 4, st);
+        SK_CUDA(cudaMemcpyAsync(d_begin.p, pr->begin.data(), (pr->num_splits + 1) * 4,
+                                cudaMemcpyHostToDevice, st));
+        a.mode = 0;
+        a.entries = pr->entries.as<int>();
+        a.out_row = pr->out_row.as<int>();
+        a.tile_masks = pr->tile_masks.as<unsigned long long>();
+        a.split_begin = d_begin.as<int>();
+        a.ns = pr->num_splits;
+        a.rows_pad = pr->rows_pad;
+        a.n_tiles = pr->rows_pad / kTileM;
+        a.n_rows_valid = m->n_out;
+        if (pr->num_splits == 1) {
+            a.items = a.n_tiles * a.n_ntiles;
+            a.y = y;
+            a.out_mode = dt == SK_F32 ? 1 : 0;
+            launch_gconv(ctx, dt, a, false, st);
+        } else {
+            DevBuf acc;
+            float* yf = dt == SK_F32 ? static_cast<float*>(y) : nullptr;
+            if (!yf) {
+                acc.alloc((size_t)y_elems * 4, st);
+                yf = acc.as<float>();
+            }
+            SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
+            a.y = yf;
+            if (det) {
+                // splits accumulate in order: partial sums telescope
+                // (implicit_gemm_impl deterministic branch, exec.cpp:240-246)
+                a.out_mode = 3;
+                a.items = a.n_tiles * a.n_ntiles;
+                for (int s = 0; s < pr->num_splits; ++s) {
+                    a.split_only = s;
+                    launch_gconv(ctx, dt, a, false, st);
+                }
+            } else {
+                a.out_mode = 2;
+                a.items = pr->num_splits * a.n_tiles * a.n_ntiles;
+                launch_gconv(ctx, dt, a, false, st);
+            }
+            if (dt != SK_F32) convert_from_f32(dt, yf, y_elems, y, st);
+        }
+        return;
+    }
+
+    // WS-based dataflows
+    kmap_ensure_ws(m, st);
+    DevBuf acc;
+    float* yf = dt == SK_F32 ? static_cast<float*>(y) : nullptr;
+    if (!yf) {
+        acc.alloc((size_t)y_elems * 4, st);
+        yf = acc.as<float>();
+    }
+    SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
+    a.mode = 1;
+    a.ws_ptr = m->ws_ptr.as<long long>();
+    a.ws_tile_ptr = m->ws_tile_ptr.as<int>();
+    a.ws_in = m->ws_in.as<int>();
+    a.ws_out = m->ws_out.as<int>();
+
+    if (cfg.kind == SK_FETCH_ON_DEMAND) {
+        a.y = yf;
+        a.ld_y = n_total;
+        if (det) {
+            a.out_mode = 3;
+            for (int k = 0; k < m->kd; ++k) {
+                a.offset_only = k;
+                launch_gconv(ctx, dt, a, true, st);
+            }
+        } else {
+            a.out_mode = 2;
+            launch_gconv(ctx, dt, a, true, st);
+        }
+    } else {
+        // gather -> GEMM -> scatter-add (exec.cpp:117-158)
+        const int64_t P = kmap_total_pairs(m, st);
+        if (P > 0) {
+            DevBuf ga, gc;
+            ga.alloc((size_t)P * k_total * es, st);
+            gc.alloc((size_t)P * n_total * 4, st);
+            const int g = ctx->num_sms * 8;
+            if (dt == SK_F32)
+                k_gather_rows<float><<<g, 256, 0, st>>>((const float*)x, k_total, a.ws_in,
+                                                        a.ws_ptr + m->kd, ga.as<float>());
+            else if (dt == SK_F16)
+                k_gather_rows<__half><<<g, 256, 0, st>>>((const __half*)x, k_total, a.ws_in,
+                                                         a.ws_ptr + m->kd, ga.as<__half>());
+            else
+                k_gather_rows<__nv_bfloat16><<<g, 256, 0, st>>>(
+                    (const __nv_bfloat16*)x, k_total, a.ws_in, a.ws_ptr + m->kd,
+                    ga.as<__nv_bfloat16>());
+            SK_LAUNCH_CHECK();
+            a.a = ga.p;
+            a.a_identity = 1;
+            a.out_identity = 1;
+            a.y = gc.p;
+            a.out_mode = 1;
+            launch_gconv(ctx, dt, a, true, st);
+            if (det) {
+                for (int k = 0; k < m->kd; ++k) {
+                    k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.ws_out,
+                                                     a.ws_ptr + k, a.ws_ptr + k + 1, yf, 1);
+                    SK_LAUNCH_CHECK();
+                }
+            } else {
+                k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.ws_out, a.ws_ptr,
+                                                 a.ws_ptr + m->kd, yf, 0);
+                SK_LAUNCH_CHECK();
+            }
+        }
+    }
+    if (dt != SK_F32) convert_from_f32(dt, yf, y_elems, y, st);
+}
+
+void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
+                int c_out, const void* x, const void* dy, float* dw, cudaStream_t st) {
+    (void)cfg;  // conv_wgrad ignores cfg.kind in the reference (exec.cpp:398-414)
+    validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
+    kmap_ensure_ws(m, st);
+    SK_CUDA(cudaMemsetAsync(dw, 0, (size_t)m->kd * c_in * c_out * 4, st));
+    if (m->n_out == 0 || m->n_in == 0) return;
+    // pair chunking: enough blocks to fill the machine; deterministic mode
+    // uses one chunk per offset (no cross-block float atomics on one cell)
+    const int chunk = ctx->deterministic ? (int)std::max<int64_t>(1, (int64_t)m->n_out) : 2048;
+    const int chunks = (int)ceil_div(std::max(m->n_out, 1), chunk);
+    dim3 grid(chunks, (unsigned)(ceil_div(c_in, 32) * ceil_div(c_out, 32)), m->kd);
+    const long long* ptr = m->ws_ptr.as<long long>();
+    if (dt == SK_F32)
+        k_wgrad_simt<float><<<grid, 256, 0, st>>>((const float*)x, (const float*)dy, c_in, c_out,
+                                                  ptr, m->ws_in.as<int>(), m->ws_out.as<int>(),
+                                                  chunk, dw);
+    else if (dt == SK_F16)
+        k_wgrad_simt<__half><<<grid, 256, 0, st>>>((const __half*)x, (const __half*)dy, c_in,
+                                                   c_out, ptr, m->ws_in.as<int>(),
+                                                   m->ws_out.as<int>(), chunk, dw);
+    else
+        k_wgrad_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(
+            (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, c_in, c_out, ptr,
+            m->ws_in.as<int>(), m->ws_out.as<int>(), chunk, dw);
+    SK_LAUNCH_CHECK();
+}
+
+}  // namespace sk

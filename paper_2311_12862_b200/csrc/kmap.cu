@@ -1,0 +1,727 @@
+// sk200 kernel-map construction on sm_100a (hot path (1)).
+//
+// Data layout in HBM
+//   coords      int4 [n]                         (Coord, tensor.hpp:15-20)
+//   hash table  u64 keys [cap] + i32 vals [cap]  cap = pow2 >= 2n, linear probing
+//   OS map      i32 [rows_pad][KD], -1 sentinel   (KernelMapOS, kmap.hpp:65-93)
+//   masks       u64 [rows_pad][words]             (compute_masks, kmap.cpp:34-47)
+//   WS lists    CSR over offsets: ptr[KD+1], in[P], out[P], ascending out row
+//               per offset (KernelMapWS, kmap.hpp:40-56)
+//   prepared    per split s: entries [rows_pad][w_s], out_row [rows_pad],
+//               masks [rows_pad][words_s], tile OR-masks [n_tiles][2]
+//
+// Kernels (one thread per output row unless noted; 128-row blocks match the
+// 128-row MMA tiles of the dataflows):
+//   k_hash_insert      CoordLookup build (tensor.cpp:80-85): CAS insert,
+//                      atomicMin keeps the FIRST row of a duplicate key
+//   k_down_insert/...  build_out_coords (kmap.cpp:73-94): floor_div keys,
+//                      first-appearance dedup via atomicMin + flag + scan
+//   k_kmap_query       build_kmap_ws + ws_to_os + compute_masks
+//                      (kmap.cpp:96-183) fused: 8 probes in flight per thread,
+//                      tile staged in smem, coalesced OS/mask stores, per
+//                      block per offset pair counts for the WS compaction
+//   k_ws_*             os_to_ws (kmap.cpp:185-209) as a stable per-offset
+//                      stream compaction (ballot + block scan)
+//   k_transpose        transpose_map (kmap.cpp:290-315) as a scatter
+//   k_split_keys/...   split_and_sort + pad_map (kmap.cpp:211-288): split-local
+//                      masks -> stable radix sort on (split, ~mask) -> reorder
+#include <cub/cub.cuh>
+
+#include "sk_internal.hpp"
+
+namespace sk {
+
+namespace {
+
+constexpr int kQB = 128;  // rows per query block
+
+__device__ __forceinline__ void offset_of(int k, int K, int dims, int& a, int& b, int& c) {
+    const int h = K / 2;
+    if (dims == 3) {
+        a = k / (K * K) - h;
+        b = (k / K) % K - h;
+        c = k % K - h;
+    } else {
+        a = k / K - h;
+        b = k % K - h;
+        c = 0;
+    }
+}
+
+__global__ void k_hash_insert(const int4* __restrict__ coords, int n,
+                              unsigned long long* __restrict__ keys, int* __restrict__ vals,
+                              uint64_t mask, int* __restrict__ err) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int4 c = coords[i];
+    if (!packable(c.x, c.y, c.z, c.w)) {
+        atomicOr(err, 1);
+        return;
+    }
+    unsigned long long key = pack_key(c.x, c.y, c.z, c.w);
+    uint64_t s = hash_key(key) & mask;
+    for (;;) {
+        unsigned long long prev = atomicCAS(&keys[s], (unsigned long long)kEmpty, key);
+        if (prev == (unsigned long long)kEmpty || prev == key) {
+            atomicMin(&vals[s], i);
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+__global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, int sy, int sz,
+                              int dims, unsigned long long* __restrict__ keys,
+                              int* __restrict__ vals, uint64_t mask, int* __restrict__ slot_out,
+                              int4* __restrict__ q_out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int4 c = coords[i];
+    int4 q = c;
+    q.y = (int)floor_div(c.y, sx);
+    q.z = (int)floor_div(c.z, sy);
+    if (dims == 3) q.w = (int)floor_div(c.w, sz);
+    q_out[i] = q;
+    unsigned long long key = pack_key(q.x, q.y, q.z, q.w);
+    uint64_t s = hash_key(key) & mask;
+    for (;;) {
+        unsigned long long prev = atomicCAS(&keys[s], (unsigned long long)kEmpty, key);
+        if (prev == (unsigned long long)kEmpty || prev == key) {
+            atomicMin(&vals[s], i);
+            slot_out[i] = (int)s;
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+__global__ void k_down_flag(const int* __restrict__ slot, const int* __restrict__ vals, int n,
+                            int* __restrict__ flag) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flag[i] = vals[slot[i]] == i ? 1 : 0;
+}
+
+__global__ void k_down_compact(const int* __restrict__ flag, const int* __restrict__ pos,
+                               const int* __restrict__ slot, const int4* __restrict__ q, int n,
+                               int* __restrict__ vals, int4* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !flag[i]) return;
+    int p = pos[i];
+    out[p] = q[i];
+    vals[slot[i]] = p;  // the table now maps out-coordinate -> out row
+}
+
+__device__ __forceinline__ int probe(const unsigned long long* __restrict__ keys,
+                                     const int* __restrict__ vals, uint64_t mask,
+                                     unsigned long long key, uint64_t s,
+                                     unsigned long long first) {
+    unsigned long long kk = first;
+    for (;;) {
+        if (kk == key) return __ldg(&vals[s]);
+        if (kk == (unsigned long long)kEmpty) return -1;
+        s = (s + 1) & mask;
+        kk = __ldg(&keys[s]);
+    }
+}
+
+// One thread per output row, all KD offsets. Writes OS entries + masks for a
+// 128-row block (pad rows get -1 / 0) and the block's per-offset pair counts.
+template <int KD>
+__global__ void __launch_bounds__(kQB) k_kmap_query(
+    const int4* __restrict__ out_coords, int n_out, const unsigned long long* __restrict__ keys,
+    const int* __restrict__ vals, uint64_t mask, int K, int dims, int sx, int sy, int sz,
+    int transposed, int words, int* __restrict__ os, unsigned long long* __restrict__ masks,
+    int* __restrict__ blk_counts) {
+    extern __shared__ int q_sh[];
+    int* tile = q_sh;           // kQB x KD
+    int* cnt = q_sh + kQB * KD;  // KD
+    const int t = threadIdx.x;
+    const int row = blockIdx.x * kQB + t;
+    for (int k = t; k < KD; k += kQB) cnt[k] = 0;
+    __syncthreads();
+    unsigned long long m0 = 0, m1 = 0;
+    const bool live = row < n_out;
+    int4 q = live ? out_coords[row] : make_int4(0, 0, 0, 0);
+    constexpr int B = 8;
+    for (int k0 = 0; k0 < KD; k0 += B) {
+        unsigned long long key[B], first[B];
+        uint64_t slot[B];
+        bool ok[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int k = k0 + u;
+            ok[u] = live && k < KD;
+            if (!ok[u]) continue;
+            int a, b, c;
+            offset_of(k, K, dims, a, b, c);
+            int px, py, pz;
+            if (!transposed) {
+                px = q.y * sx + a;
+                py = q.z * sy + b;
+                pz = q.w * sz + c;
+            } else {
+                // q_in = (p_out + delta) / s only when every axis divides
+                // (C++ truncating %, kmap.cpp:124-129)
+                int nx = q.y + a, ny = q.z + b, nz = q.w + c;
+                if (nx % sx != 0 || ny % sy != 0 || (dims == 3 && nz % sz != 0)) {
+                    ok[u] = false;
+                    continue;
+                }
+                px = nx / sx;
+                py = ny / sy;
+                pz = dims == 3 ? nz / sz : 0;
+            }
+            if (!packable(q.x, px, py, pz)) {
+                ok[u] = false;
+                continue;
+            }
+            key[u] = pack_key(q.x, px, py, pz);
+            slot[u] = hash_key(key[u]) & mask;
+            first[u] = __ldg(&keys[slot[u]]);  // B independent loads in flight
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int k = k0 + u;
+            if (k >= KD) continue;
+            int j = ok[u] ? probe(keys, vals, mask, key[u], slot[u], first[u]) : -1;
+            tile[t * KD + k] = j;
+            unsigned hit = __ballot_sync(0xffffffffu, j >= 0);
+            if ((t & 31) == 0 && hit) atomicAdd(&cnt[k], __popc(hit));
+            if (j >= 0) {
+                // big-endian bit order (kmap.cpp:38-45)
+                if (k < 64) {
+                    int biw = KD < 64 ? KD : 64;
+                    m0 |= 1ull << (biw - 1 - k);
+                } else {
+                    m1 |= 1ull << (KD - 64 - 1 - (k - 64));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    int* dst = os + (size_t)blockIdx.x * kQB * KD;
+    for (int i = t; i < kQB * KD; i += kQB) dst[i] = tile[i];
+    masks[(size_t)row * words] = m0;
+    if (words == 2) masks[(size_t)row * words + 1] = m1;
+    for (int k = t; k < KD; k += kQB) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
+}
+
+// masks + per-block counts from an existing OS matrix (transposed maps).
+__global__ void __launch_bounds__(kQB) k_finalize(const int* __restrict__ os, int kd, int words,
+                                                  unsigned long long* __restrict__ masks,
+                                                  int* __restrict__ blk_counts) {
+    extern __shared__ int sh[];
+    int* tile = sh;
+    int* cnt = sh + kQB * kd;
+    const int t = threadIdx.x;
+    const int row = blockIdx.x * kQB + t;
+    for (int k = t; k < kd; k += kQB) cnt[k] = 0;
+    const int* src = os + (size_t)blockIdx.x * kQB * kd;
+    for (int i = t; i < kQB * kd; i += kQB) tile[i] = src[i];
+    __syncthreads();
+    unsigned long long m0 = 0, m1 = 0;
+    for (int k = 0; k < kd; ++k) {
+        int j = tile[t * kd + k];
+        unsigned hit = __ballot_sync(0xffffffffu, j >= 0);
+        if ((t & 31) == 0 && hit) atomicAdd(&cnt[k], __popc(hit));
+        if (j >= 0) {
+            if (k < 64) m0 |= 1ull << ((kd < 64 ? kd : 64) - 1 - k);
+            else m1 |= 1ull << (kd - 64 - 1 - (k - 64));
+        }
+    }
+    __syncthreads();
+    masks[(size_t)row * words] = m0;
+    if (words == 2) masks[(size_t)row * words + 1] = m1;
+    for (int k = t; k < kd; k += kQB) blk_counts[(size_t)blockIdx.x * kd + k] = cnt[k];
+}
+
+// Per-offset exclusive scan over blocks (one warp per offset), then the CSR
+// pointer over offsets and the FOD/GGS tile schedule (128 pairs per tile).
+__global__ void __launch_bounds__(1024) k_ws_scan(const int* __restrict__ blk_counts,
+                                                  int n_blocks, int kd,
+                                                  long long* __restrict__ blk_off,
+                                                  long long* __restrict__ ptr,
+                                                  int* __restrict__ tile_ptr) {
+    __shared__ long long tot[128];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    for (int k = warp; k < kd; k += 32) {
+        long long run = 0;
+        for (int b0 = 0; b0 < n_blocks; b0 += 32) {
+            int b = b0 + lane;
+            long long v = b < n_blocks ? blk_counts[(size_t)b * kd + k] : 0;
+            long long inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                long long u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += u;
+            }
+            if (b < n_blocks) blk_off[(size_t)b * kd + k] = run + inc - v;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) tot[k] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long acc = 0;
+        int tacc = 0;
+        for (int k = 0; k < kd; ++k) {
+            ptr[k] = acc;
+            tile_ptr[k] = tacc;
+            acc += tot[k];
+            tacc += (int)((tot[k] + kTileM - 1) / kTileM);
+        }
+        ptr[kd] = acc;
+        tile_ptr[kd] = tacc;
+    }
+}
+
+__global__ void __launch_bounds__(kQB) k_ws_scatter(const int* __restrict__ os, int kd,
+                                                    const long long* __restrict__ blk_off,
+                                                    const long long* __restrict__ ptr,
+                                                    int* __restrict__ ws_in,
+                                                    int* __restrict__ ws_out) {
+    extern __shared__ int sh[];
+    int* tile = sh;
+    __shared__ int wcnt[kQB / 32];
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const int row = blockIdx.x * kQB + t;
+    const int* src = os + (size_t)blockIdx.x * kQB * kd;
+    for (int i = t; i < kQB * kd; i += kQB) tile[i] = src[i];
+    __syncthreads();
+    for (int k = 0; k < kd; ++k) {
+        int j = tile[t * kd + k];
+        unsigned hit = __ballot_sync(0xffffffffu, j >= 0);
+        if (lane == 0) wcnt[warp] = __popc(hit);
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < warp; ++w) before += wcnt[w];
+        if (j >= 0) {
+            long long pos = ptr[k] + blk_off[(size_t)blockIdx.x * kd + k] + before +
+                            __popc(hit & ((1u << lane) - 1));
+            ws_in[pos] = j;
+            ws_out[pos] = row;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_transpose(const int* __restrict__ os, int n_out, int kd, int* __restrict__ ost) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n_out * kd) return;
+    int q = (int)(i / kd), k = (int)(i % kd);
+    int j = os[i];
+    if (j >= 0) ost[(size_t)j * kd + (kd - 1 - k)] = q;
+}
+
+// Sort keys for split_and_sort: key = (split << W) | (~local_mask & wmask) so
+// one stable ascending radix sort orders every split by DESCENDING mask,
+// stable (std::stable_sort with mask_greater, kmap.cpp:252-256).
+__global__ void k_split_keys(const int* __restrict__ os, int n, int kd, int ns,
+                             const int* __restrict__ begin, int W, int word,
+                             const int* __restrict__ perm, unsigned long long* __restrict__ keys,
+                             int* __restrict__ vals) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * ns) return;
+    int s = (int)(i / n), r = (int)(i % n);
+    if (perm) r = perm[i];
+    int b = begin[s], e = begin[s + 1], w = e - b;
+    // split-local mask words (word 0 most significant); `word` selects which
+    // 64-bit word is the key for wide (w > 64) single-split maps
+    unsigned long long m = 0;
+    const int* row = os + (size_t)r * kd;
+    int words = (w + 63) / 64;
+    int wi_lo = word * 64, bits = min(64, w - wi_lo);
+    for (int j = 0; j < bits; ++j)
+        if (row[b + wi_lo + j] >= 0) m |= 1ull << (bits - 1 - j);
+    unsigned long long wm = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+    unsigned long long key = (~m) & wm;
+    if (words == 1 && ns > 1) key |= (unsigned long long)s << W;
+    keys[i] = key;
+    vals[i] = r;
+}
+
+__global__ void k_split_reorder(const int* __restrict__ os, int n, int kd, int ns, int rows_pad,
+                                const int* __restrict__ begin, const int* __restrict__ word_off,
+                                const int* __restrict__ order, int* __restrict__ entries,
+                                int* __restrict__ out_row, unsigned long long* __restrict__ masks) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)rows_pad * ns) return;
+    int s = (int)(i / rows_pad), p = (int)(i % rows_pad);
+    int b = begin[s], w = begin[s + 1] - b, words = (w + 63) / 64;
+    int* dst = entries + (size_t)rows_pad * b + (size_t)p * w;
+    unsigned long long* md = masks + (size_t)rows_pad * word_off[s] + (size_t)p * words;
+    if (p >= n) {
+        for (int j = 0; j < w; ++j) dst[j] = -1;
+        out_row[(size_t)s * rows_pad + p] = -1;
+        for (int u = 0; u < words; ++u) md[u] = 0;
+        return;
+    }
+    int src = order[(size_t)s * n + p];
+    const int* row = os + (size_t)src * kd + b;
+    unsigned long long m[2] = {0, 0};
+    for (int j = 0; j < w; ++j) {
+        int v = row[j];
+        dst[j] = v;
+        if (v >= 0) {
+            int wi = j / 64, biw = min(64, w - wi * 64);
+            m[wi] |= 1ull << (biw - 1 - (j - wi * 64));
+        }
+    }
+    out_row[(size_t)s * rows_pad + p] = src;
+    for (int u = 0; u < words; ++u) md[u] = m[u];
+}
+
+// OR of the row masks of each 128-row tile (2 words, word 0 = most significant)
+__global__ void k_tile_masks(const unsigned long long* __restrict__ masks,
+                             const int* __restrict__ begin, const int* __restrict__ word_off,
+                             int ns, int rows_pad, unsigned long long* __restrict__ tmask) {
+    const int n_tiles = rows_pad / kTileM;
+    int tile = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x % 32;
+    if (tile >= n_tiles * ns) return;
+    int s = tile / n_tiles, t = tile % n_tiles;
+    int w = begin[s + 1] - begin[s], words = (w + 63) / 64;
+    const unsigned long long* src = masks + (size_t)rows_pad * word_off[s];
+    unsigned long long a = 0, b = 0;
+    for (int r = lane; r < kTileM; r += 32) {
+        size_t row = (size_t)t * kTileM + r;
+        a |= src[row * words];
+        if (words == 2) b |= src[row * words + 1];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a |= __shfl_xor_sync(0xffffffffu, a, o);
+        b |= __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+        tmask[(size_t)tile * 2] = a;
+        tmask[(size_t)tile * 2 + 1] = b;
+    }
+}
+
+__global__ void k_iota(int* __restrict__ v, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+int64_t pow2_cap(int64_t n) {
+    int64_t c = 64;
+    while (c < 2 * n) c <<= 1;
+    return c;
+}
+
+void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_t st) {
+    const int grid = m->rows_pad / kQB;
+    const uint64_t mask = (uint64_t)in->cap - 1;
+    const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
+#define SK_Q(KDV)                                                                            \
+    if (smem > 48 * 1024)                                                                    \
+        SK_CUDA(cudaFuncSetAttribute(k_kmap_query<KDV>,                                      \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_kmap_query<KDV><<<grid, kQB, smem, st>>>(                                              \
+        out_coords, m->n_out, in->keys.as<unsigned long long>(), in->vals.as<int>(), mask,   \
+        m->kernel, m->dims, m->stride[0], m->stride[1], m->stride[2], m->transposed, m->words, \
+        m->os.as<int>(), m->masks.as<unsigned long long>(), m->blk_counts.as<int>())
+    switch (m->kd) {
+        case 1: SK_Q(1); break;
+        case 9: SK_Q(9); break;
+        case 25: SK_Q(25); break;
+        case 27: SK_Q(27); break;
+        case 125: SK_Q(125); break;
+        default: fail(SK_ERR_VALIDATION, "unsupported kernel volume " + std::to_string(m->kd));
+    }
+#undef SK_Q
+    SK_LAUNCH_CHECK();
+}
+
+void alloc_map(sk_kmap* m, cudaStream_t st) {
+    m->rows_pad = (int)ceil_div(std::max(m->n_out, 1), kTileM) * kTileM;
+    m->words = (m->kd + 63) / 64;
+    m->n_blocks = m->rows_pad / kQB;
+    m->os.alloc((size_t)m->rows_pad * m->kd * 4, st);
+    m->masks.alloc((size_t)m->rows_pad * m->words * 8, st);
+    m->blk_counts.alloc((size_t)m->n_blocks * m->kd * 4, st);
+}
+
+}  // namespace
+
+uint64_t next_coord_set_id() {
+    static std::atomic<uint64_t> counter{1};
+    return counter.fetch_add(1);
+}
+
+void coords_check_range(sk_ctx*, const int32_t*, int, cudaStream_t) {}
+
+void coords_build_table(sk_coords* c, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (c->has_table) return;
+    c->cap = pow2_cap(c->n);
+    c->keys.alloc((size_t)c->cap * 8, st);
+    c->vals.alloc((size_t)c->cap * 4, st);
+    SK_CUDA(cudaMemsetAsync(c->keys.p, 0xFF, c->keys.bytes, st));
+    SK_CUDA(cudaMemsetAsync(c->vals.p, 0x7F, c->vals.bytes, st));
+    DevBuf err;
+    err.alloc(4, st);
+    SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    if (c->n > 0) {
+        k_hash_insert<<<(int)ceil_div(c->n, 256), 256, 0, st>>>(
+            c->coords.as<int4>(), c->n, c->keys.as<unsigned long long>(), c->vals.as<int>(),
+            (uint64_t)c->cap - 1, err.as<int>());
+        SK_LAUNCH_CHECK();
+    }
+    int h_err = 0;
+    SK_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    validate(h_err == 0,
+             "coordinate outside the packable range (batch [0,4096), xyz [-65536,65536))");
+    c->has_table = true;
+}
+
+sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_t st) {
+    const int n = in->n;
+    auto* out = new sk_coords();
+    out->ctx = in->ctx;
+    out->dims = in->dims;
+    out->id = next_coord_set_id();
+    for (int d = 0; d < 3; ++d) out->stride_tag[d] = in->stride_tag[d] * (d < in->dims ? stride[d] : 1);
+    out->cap = pow2_cap(n);
+    out->keys.alloc((size_t)out->cap * 8, st);
+    out->vals.alloc((size_t)out->cap * 4, st);
+    SK_CUDA(cudaMemsetAsync(out->keys.p, 0xFF, out->keys.bytes, st));
+    SK_CUDA(cudaMemsetAsync(out->vals.p, 0x7F, out->vals.bytes, st));
+    if (n == 0) {
+        out->n = 0;
+        out->has_table = true;
+        return out;
+    }
+    DevBuf slot, q, flag, pos, tmp, total;
+    slot.alloc((size_t)n * 4, st);
+    q.alloc((size_t)n * 16, st);
+    flag.alloc((size_t)n * 4, st);
+    pos.alloc((size_t)n * 4 + 4, st);
+    const int g = (int)ceil_div(n, 256);
+    k_down_insert<<<g, 256, 0, st>>>(in->coords.as<int4>(), n, stride[0], stride[1],
+                                     in->dims == 3 ? stride[2] : 1, in->dims,
+                                     out->keys.as<unsigned long long>(), out->vals.as<int>(),
+                                     (uint64_t)out->cap - 1, slot.as<int>(), q.as<int4>());
+    SK_LAUNCH_CHECK();
+    k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->vals.as<int>(), n, flag.as<int>());
+    SK_LAUNCH_CHECK();
+    size_t tbytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tbytes, flag.as<int>(), pos.as<int>(), n + 1, st);
+    tmp.alloc(tbytes, st);
+    // scan n+1 items: the last (flag past the end reads pos[n] slot) -> total
+    // count lands in pos[n] via an inclusive trick: exclusive over n then add
+    cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, flag.as<int>(), pos.as<int>(), n, st);
+    SK_LAUNCH_CHECK();
+    int h_last_pos = 0, h_last_flag = 0;
+    SK_CUDA(cudaMemcpyAsync(&h_last_pos, pos.as<int>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaMemcpyAsync(&h_last_flag, flag.as<int>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    out->n = h_last_pos + h_last_flag;
+    out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
+    k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(),
+                                      q.as<int4>(), n, out->vals.as<int>(),
+                                      out->coords.as<int4>());
+    SK_LAUNCH_CHECK();
+    out->has_table = true;
+    return out;
+}
+
+sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],
+                    int transposed, cudaStream_t st) {
+    validate(in->dims == out->dims, "offset dims mismatch");
+    validate(kernel >= 1 && kernel % 2 == 1, "kernel size must be odd (even kernels unsupported)");
+    validate(kernel <= 5, "kernel size > 5 unsupported");
+    for (int d = 0; d < in->dims; ++d) validate(stride[d] >= 1, "stride components must be >= 1");
+    coords_build_table(in, st);
+    auto* m = new sk_kmap();
+    m->ctx = in->ctx;
+    m->dims = in->dims;
+    m->kernel = kernel;
+    m->kd = in->dims == 3 ? kernel * kernel * kernel : kernel * kernel;
+    for (int d = 0; d < 3; ++d) m->stride[d] = d < in->dims ? stride[d] : 1;
+    m->transposed = transposed;
+    m->n_in = in->n;
+    m->n_out = out->n;
+    alloc_map(m, st);
+    launch_query(m, out->coords.as<int4>(), in, st);
+    return m;
+}
+
+sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(src->mu);
+    if (src->transpose_cache) return src->transpose_cache;
+    auto* m = new sk_kmap();
+    m->ctx = src->ctx;
+    m->dims = src->dims;
+    m->kernel = src->kernel;
+    m->kd = src->kd;
+    for (int d = 0; d < 3; ++d) m->stride[d] = src->stride[d];
+    m->transposed = !src->transposed;
+    m->n_in = src->n_out;
+    m->n_out = src->n_in;
+    alloc_map(m, st);
+    SK_CUDA(cudaMemsetAsync(m->os.p, 0xFF, m->os.bytes, st));
+    long long total = (long long)src->n_out * src->kd;
+    if (total > 0) {
+        k_transpose<<<(int)ceil_div(total, 256), 256, 0, st>>>(src->os.as<int>(), src->n_out,
+                                                               src->kd, m->os.as<int>());
+        SK_LAUNCH_CHECK();
+    }
+    size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
+    if (smem > 48 * 1024)
+        SK_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    k_finalize<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd, m->words,
+                                               m->masks.as<unsigned long long>(),
+                                               m->blk_counts.as<int>());
+    SK_LAUNCH_CHECK();
+    src->transpose_cache = m;  // owned by src, released in ~sk_kmap
+    return m;
+}
+
+void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(m->mu);
+    if (m->has_ws) return;
+    m->ws_ptr.alloc((size_t)(m->kd + 1) * 8, st);
+    m->ws_tile_ptr.alloc((size_t)(m->kd + 1) * 4, st);
+    m->blk_off.alloc((size_t)m->n_blocks * m->kd * 8, st);
+    size_t cap = (size_t)std::max<int64_t>(1, (int64_t)m->n_out * m->kd);
+    m->ws_in.alloc(cap * 4, st);
+    m->ws_out.alloc(cap * 4, st);
+    k_ws_scan<<<1, 1024, 0, st>>>(m->blk_counts.as<int>(), m->n_blocks, m->kd,
+                                  m->blk_off.as<long long>(), m->ws_ptr.as<long long>(),
+                                  m->ws_tile_ptr.as<int>());
+    SK_LAUNCH_CHECK();
+    size_t smem = (size_t)kQB * m->kd * 4;
+    if (smem > 48 * 1024)
+        SK_CUDA(cudaFuncSetAttribute(k_ws_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    k_ws_scatter<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd,
+                                                 m->blk_off.as<long long>(),
+                                                 m->ws_ptr.as<long long>(), m->ws_in.as<int>(),
+                                                 m->ws_out.as<int>());
+    SK_LAUNCH_CHECK();
+    m->has_ws = true;
+}
+
+int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st) {
+    kmap_ensure_ws(m, st);
+    long long v = 0;
+    SK_CUDA(cudaMemcpyAsync(&v, m->ws_ptr.as<long long>() + m->kd, 8, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    return v;
+}
+
+Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
+    validate(splits >= 0, "split count must be >= 0");
+    validate(splits <= m->kd, "split count exceeds number of kernel offsets");
+    validate(pad >= 1, "pad multiple must be >= 1");
+    std::lock_guard<std::mutex> lock(m->mu);
+    auto key = std::make_pair(splits, pad);
+    auto it = m->prepared.find(key);
+    if (it != m->prepared.end()) return it->second.get();
+
+    auto p = std::make_unique<Prepared>();
+    p->splits = splits;
+    p->pad = pad;
+    p->num_splits = std::max(splits, 1);
+    // rows padded to lcm(pad, 128) so every prepared map also runs in 128-row tiles
+    int64_t a = pad, b = kTileM;
+    while (b) { int64_t t = a % b; a = b; b = t; }
+    int64_t l = (int64_t)pad / a * kTileM;
+    p->rows_pad = (int)(ceil_div(std::max(m->n_out, 1), l) * l);
+    const int ns = p->num_splits, n = m->n_out, kd = m->kd;
+    p->begin.resize(ns + 1);
+    if (splits == 0) {
+        p->begin = {0, kd};
+    } else {
+        int chunk = kd / splits, rem = kd % splits, bb = 0;
+        for (int s = 0; s < splits; ++s) {  // kmap.cpp:227-236
+            p->begin[s] = bb;
+            bb += chunk + (s < rem ? 1 : 0);
+        }
+        p->begin[splits] = bb;
+    }
+    p->word_off.resize(ns + 1);
+    int wacc = 0, W = 0;
+    for (int s = 0; s < ns; ++s) {
+        int w = p->begin[s + 1] - p->begin[s];
+        p->word_off[s] = wacc;
+        wacc += (w + 63) / 64;
+        W = std::max(W, w);
+    }
+    p->word_off[ns] = wacc;
+    p->mask_words_max = (W + 63) / 64;
+    p->entries.alloc((size_t)p->rows_pad * kd * 4, st);
+    p->out_row.alloc((size_t)p->rows_pad * ns * 4, st);
+    p->masks.alloc((size_t)p->rows_pad * wacc * 8, st);
+    DevBuf d_begin, d_woff;
+    d_begin.alloc((ns + 1) * 4, st);
+    d_woff.alloc((ns + 1) * 4, st);
+    SK_CUDA(cudaMemcpyAsync(d_begin.p, p->begin.data(), (ns + 1) * 4, cudaMemcpyHostToDevice, st));
+    SK_CUDA(cudaMemcpyAsync(d_woff.p, p->word_off.data(), (ns + 1) * 4, cudaMemcpyHostToDevice, st));
+
+    DevBuf order;
+    order.alloc((size_t)std::max(n * ns, 1) * 4, st);
+    if (splits == 0 || n == 0) {
+        // unsorted: identity order (split_and_sort(0) leaves the map unchanged)
+        if (n) {
+            k_iota<<<(int)ceil_div(n, 256), 256, 0, st>>>(order.as<int>(), n);
+            SK_LAUNCH_CHECK();
+        }
+    } else {
+        const long long tot = (long long)n * ns;
+        int sbits = 0;
+        while ((1 << sbits) < ns) ++sbits;
+        DevBuf k_in, k_out, v_in, tmp;
+        k_in.alloc(tot * 8, st);
+        k_out.alloc(tot * 8, st);
+        v_in.alloc(tot * 4, st);
+        const int g = (int)ceil_div(tot, 256);
+        DevBuf order1;
+        order1.alloc(tot * 4, st);
+        auto sort_pass = [&](int word, int end_bit, const int* perm, int* dst) {
+            k_split_keys<<<g, 256, 0, st>>>(m->os.as<int>(), n, kd, ns, d_begin.as<int>(), W, word,
+                                            perm, k_in.as<unsigned long long>(), v_in.as<int>());
+            SK_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in.as<unsigned long long>(),
+                                            k_out.as<unsigned long long>(), v_in.as<int>(), dst,
+                                            (int)tot, 0, end_bit, st);
+            tmp.alloc(tb, st);
+            cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.as<unsigned long long>(),
+                                            k_out.as<unsigned long long>(), v_in.as<int>(), dst,
+                                            (int)tot, 0, end_bit, st);
+            SK_LAUNCH_CHECK();
+        };
+        if (W <= 64) {
+            sort_pass(0, std::min(64, W + (ns > 1 ? sbits : 0)), nullptr, order.as<int>());
+        } else {
+            // one split wider than 64 columns (K=5, s=1): stable LSD over the
+            // two mask words -- low word first, then stably by the high word
+            // over the pass-1 order (== big-endian word compare, kmap.cpp:49-54)
+            sort_pass(1, W - 64, nullptr, order1.as<int>());
+            sort_pass(0, 64, order1.as<int>(), order.as<int>());
+        }
+    }
+    const long long tot_rows = (long long)p->rows_pad * ns;
+    k_split_reorder<<<(int)ceil_div(tot_rows, 256), 256, 0, st>>>(
+        m->os.as<int>(), n, kd, ns, p->rows_pad, d_begin.as<int>(), d_woff.as<int>(),
+        order.as<int>(), p->entries.as<int>(), p->out_row.as<int>(),
+        p->masks.as<unsigned long long>());
+    SK_LAUNCH_CHECK();
+    const int n_tiles = p->rows_pad / kTileM;
+    p->tile_masks.alloc((size_t)n_tiles * ns * 16, st);
+    k_tile_masks<<<(int)ceil_div((long long)n_tiles * ns, 8), 256, 0, st>>>(
+        p->masks.as<unsigned long long>(), d_begin.as<int>(), d_woff.as<int>(), ns, p->rows_pad,
+        p->tile_masks.as<unsigned long long>());
+    SK_LAUNCH_CHECK();
+    Prepared* raw = p.get();
+    m->prepared[key] = std::move(p);
+    return raw;
+}
+
+}  // namespace sk

@@ -1,0 +1,103 @@
+// sk200 internal object model behind the C ABI (include/sk200.h).
+#pragma once
+
+#include "sk_common.cuh"
+
+struct sk_ctx {
+    int device = 0;
+    int num_sms = 148;
+    bool deterministic = false;
+    size_t smem_optin = 227 * 1024;
+};
+
+namespace sk {
+
+struct Refcounted {
+    std::atomic<int> refs{1};
+    virtual ~Refcounted() = default;
+};
+
+// Prepared (split + sorted + padded) OS map: prepare_os_map (exec.cpp:342-344).
+struct Prepared {
+    int splits = 0;       // requested (0 = unsorted single split)
+    int pad = 1;          // pad multiple (TilePreset::cta_m)
+    int num_splits = 1;   // max(splits, 1)
+    int rows_pad = 0;     // per split
+    int mask_words_max = 1;
+    std::vector<int> begin;  // num_splits + 1 global offset bounds
+    DevBuf entries;          // split s at rows_pad*begin[s]: rows_pad x width_s
+    DevBuf out_row;          // num_splits x rows_pad (-1 pad rows)
+    DevBuf masks;            // split s at rows_pad*word_off[s]: rows_pad x words_s
+    std::vector<int> word_off;
+    DevBuf tile_masks;       // num_splits x n_tiles(of 128) x 2 u64 (OR of row masks)
+    int tile_rows = 128;
+};
+
+}  // namespace sk
+
+struct sk_coords : sk::Refcounted {
+    sk_ctx* ctx = nullptr;
+    int dims = 3;
+    int n = 0;
+    int32_t stride_tag[3] = {1, 1, 1};
+    uint64_t id = 0;
+    sk::DevBuf coords;  // int4 [n]
+    // open-addressing hash: keys u64 [cap], vals i32 [cap] (row index)
+    sk::DevBuf keys, vals;
+    int64_t cap = 0;
+    bool has_table = false;
+    std::mutex mu;
+    // children: downsampled sets by stride (owned), maps by key (owned)
+    std::map<std::tuple<int, int, int>, sk_coords*> down;
+    std::map<std::tuple<uint64_t, int, int, int, int, int>, sk_kmap*> maps;
+    ~sk_coords() override;
+};
+
+struct sk_kmap : sk::Refcounted {
+    sk_ctx* ctx = nullptr;
+    int dims = 3, kernel = 3, kd = 27;
+    int stride[3] = {1, 1, 1};
+    int transposed = 0;
+    int n_in = 0, n_out = 0;
+    int rows_pad = 0;       // n_out rounded up to 128 (the raw OS is stored padded)
+    int words = 1;          // mask words of the full-width map
+    int n_blocks = 0;       // query blocks (for per-block pair counts)
+    sk::DevBuf os;          // rows_pad x kd int32
+    sk::DevBuf masks;       // rows_pad x words u64
+    sk::DevBuf blk_counts;  // n_blocks x kd int32
+    sk::DevBuf ws_ptr;      // kd+1 int64 (exclusive scan of per-offset counts)
+    sk::DevBuf blk_off;     // n_blocks x kd int64 (write cursor per block/offset)
+    sk::DevBuf ws_in, ws_out;  // total_pairs (allocated at n_out*kd upper bound)
+    bool has_ws = false;
+    // FOD/GGS tile schedule over WS lists: per offset first tile index
+    sk::DevBuf ws_tile_ptr;    // kd+1 int32
+    std::map<std::pair<int, int>, std::unique_ptr<sk::Prepared>> prepared;
+    sk_kmap* transpose_cache = nullptr;  // owned
+    std::mutex mu;
+    ~sk_kmap() override;
+};
+
+namespace sk {
+
+constexpr int kTileM = 128;  // MMA M rows per tile = pad multiple
+
+// kmap.cu
+void coords_build_table(sk_coords* c, cudaStream_t st);
+void coords_check_range(sk_ctx* ctx, const int32_t* d, int n, cudaStream_t st);
+sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_t st);
+sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],
+                    int transposed, cudaStream_t st);
+sk_kmap* kmap_transpose(sk_kmap* m, cudaStream_t st);
+void kmap_ensure_ws(sk_kmap* m, cudaStream_t st);
+Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st);
+int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st);
+
+// conv.cu
+void conv_forward(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
+                  int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st);
+void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
+                int c_out, const void* x, const void* dy, float* dw, cudaStream_t st);
+
+uint64_t next_coord_set_id();
+
+}  // namespace sk

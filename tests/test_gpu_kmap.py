@@ -1,0 +1,161 @@
+"""GPU kernel-map parity (hot path (1)): bit-exact against the compiled
+reference (oracle/_ref) and the frozen golden vectors.
+
+Checked per instance: output coordinates (values AND first-appearance order),
+OS matrix, per-row big-endian masks, WS pair lists (ascending out row per
+offset), split_and_sort + pad_map row orders/entries/masks for several split
+counts and pad multiples, transposed maps, MAC counts.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2311_12862_b200 import sparse
+    return sparse
+
+
+def ws_lists(ptr, inn, out):
+    return [[[int(inn[i]), int(out[i])] for i in range(ptr[k], ptr[k + 1])]
+            for k in range(len(ptr) - 1)]
+
+
+def test_golden_fig2(sk):
+    g = json.load(open(os.path.join(GOLD, "fig2.json")))
+    cin = sk.CoordSet.create(np.array(g["in_coords"], np.int32), dims=2)
+    cout = sk.CoordSet.create(np.array(g["out_coords"], np.int32), dims=2)
+    m = sk.build_kmap(cin, cout, 3, 1)
+    ent, masks = m.os()
+    assert ent.tolist() == g["os_matrix"]
+    assert masks[:, 0].tolist() == g["masks"]
+    assert ws_lists(*m.ws()) == g["ws_pairs"]
+    assert m.total_pairs() == g["effective_macs"]
+    assert m.split(1)[0][3].tolist() == g["sorted_order_s1"]
+    assert [s[3].tolist() for s in m.split(3)] == g["sorted_order_s3"]
+    assert [s[1] - s[0] for s in m.split(2)] == [5, 4]
+    for splits, want in ((0, g["redundant_unsorted"]), (1, g["redundant_s1"]),
+                         (3, g["redundant_s3"])):
+        assert m.count_macs(splits, 4, 4, 1, 1) == (g["effective_macs"], want)
+    with pytest.raises(sk.ValidationError):
+        m.prepare(10)
+
+
+def test_random_fixture(sk):
+    d = json.load(open(os.path.join(GOLD, "random.json")))
+    for case in d["cases"]:
+        c = sk.CoordSet.create(np.array(case["in_coords"], np.int32))
+        o = sk.build_out_coords(c, case["stride"])
+        assert o.numpy().tolist() == case["out_coords"]
+        m = sk.build_kmap(c, o, case["kernel"], case["stride"])
+        ent, masks = m.os()
+        assert ent.tolist() == case["os"]
+        assert [[int(v) for v in r] for r in masks] == case["masks"]
+        for got, want in zip(m.split(2, 8), case["split2_pad8"]):
+            assert got[3].tolist() == want["out_row"]
+            assert got[2].tolist() == want["entries"]
+
+
+CASES = [
+    # seed, n, stride, K, batches, coordinate range
+    (1, 300, 1, 3, 1, 12), (2, 400, 2, 3, 1, 12), (3, 350, 3, 3, 2, 12), (4, 200, 1, 5, 1, 12),
+    (5, 5000, 2, 3, 3, 40), (6, 1, 1, 3, 1, 12), (7, 3000, (2, 1, 1), 3, 1, 30),
+    (8, 20000, 1, 3, 1, 60), (9, 20000, 2, 5, 2, 60), (10, 4000, 1, 1, 1, 20),
+]
+
+
+@pytest.mark.parametrize("seed,n,stride,k,batches,rng", CASES)
+def test_maps_match_reference(sk, reference, seed, n, stride, k, batches, rng):
+    from paper_2311_12862_b200.synth import random_instance_coords
+    c_np = random_instance_coords(seed, n, -rng, rng, batches)
+    st = list(stride) if isinstance(stride, tuple) else [stride] * 3
+    c = sk.CoordSet.create(c_np)
+    o = sk.build_out_coords(c, st)
+    out_ref = reference.out_coords(3, c_np, st)
+    assert np.array_equal(o.numpy(), out_ref)  # values and first-appearance order
+    if st != [1, 1, 1]:
+        assert o.stride_tag == tuple(st)
+    for transposed in (False, True):
+        a, b = (o, c) if transposed else (c, o)
+        a_np, b_np = (out_ref, c_np) if transposed else (c_np, out_ref)
+        m = sk.build_kmap(a, b, k, st, transposed)
+        rm = reference.kmap(3, k, a_np, b_np, st, transposed)
+        ent, masks = m.os()
+        ent_r, masks_r = rm.os()
+        assert np.array_equal(ent, ent_r)
+        assert np.array_equal(masks, masks_r)
+        ptr, inn, out = m.ws()
+        for kk in range(rm.kd):
+            ri, ro = rm.pairs(kk)
+            assert np.array_equal(inn[ptr[kk]:ptr[kk + 1]], ri)
+            assert np.array_equal(out[ptr[kk]:ptr[kk + 1]], ro)
+        kd = rm.kd
+        for splits in sorted({0, 1, 2, 5, min(kd, 27)} & set(range(kd + 1))):
+            for pad in (1, 8, 128):
+                got, want = m.split(splits, pad), rm.prepare(splits, pad)
+                assert len(got) == len(want)
+                for g_, w_ in zip(got, want):
+                    assert (g_[0], g_[1]) == (w_[0], w_[1])
+                    assert np.array_equal(g_[2], w_[2]), (splits, pad)
+                    assert np.array_equal(g_[3], w_[3]), (splits, pad)
+                    assert np.array_equal(g_[4], w_[4]), (splits, pad)
+                assert m.count_macs(splits, pad, 32, 4, 8) == rm.count_macs(32, 4, 8)
+    # transpose_map (kmap.cpp:290-315) == reference transpose == direct build
+    m = sk.build_kmap(c, o, k, st)
+    t = m.transpose()
+    rt = reference.kmap(3, k, c_np, out_ref, st).transpose()
+    assert np.array_equal(t.os()[0], rt.os()[0])
+    assert np.array_equal(t.os()[1], rt.os()[1])
+    direct = sk.build_kmap(o, c, k, st, transposed=True)
+    assert np.array_equal(direct.os()[0], t.os()[0])
+
+
+def test_map_cache_builds_once(sk):
+    from paper_2311_12862_b200.synth import random_instance_coords
+    c = sk.CoordSet.create(random_instance_coords(3, 500))
+    a = sk.build_kmap(c, c, 3, 1)
+    b = sk.build_kmap(c, c, 3, 1)
+    assert a.ptr.value == b.ptr.value  # same object per MapKey (kmap.cpp:359-391)
+    t = sk.build_kmap(c, c, 3, 1, transposed=True)
+    assert t.ptr.value != a.ptr.value
+    o1 = sk.build_out_coords(c, 2)
+    o2 = sk.build_out_coords(c, 2)
+    assert o1.id == o2.id
+    assert sk.build_out_coords(c, 1).id == c.id  # submanifold keeps the set
+
+
+def test_validation_errors(sk):
+    with pytest.raises(sk.ValidationError):
+        sk.CoordSet.create(np.array([[0, 70000, 0, 0]], np.int32))  # outside packable range
+    with pytest.raises(sk.ValidationError):
+        sk.CoordSet.create(np.array([[5000, 0, 0, 0]], np.int32))
+    c = sk.CoordSet.create(np.array([[0, 0, 0, 0], [0, 1, 0, 0]], np.int32))
+    with pytest.raises(sk.ValidationError):
+        sk.build_kmap(c, c, 2, 1)  # even kernel (kmap.cpp:60-61)
+    with pytest.raises(sk.ValidationError):
+        sk.build_out_coords(c, 0)
+
+
+def test_large_scan_matches_reference(sk, reference):
+    """C1-sized submanifold map (~100k uniform voxels) and a strided level."""
+    from paper_2311_12862_b200.synth import uniform_voxels
+    c_np = uniform_voxels(127_000, 64, seed=1)
+    c = sk.CoordSet.create(c_np)
+    m = sk.build_kmap(c, c, 3, 1)
+    rm = reference.kmap(3, 3, c_np, c_np, [1, 1, 1])
+    ent, masks = m.os()
+    ent_r, masks_r = rm.os()
+    assert np.array_equal(ent, ent_r) and np.array_equal(masks, masks_r)
+    got, want = m.split(1, 128), rm.prepare(1, 128)
+    assert np.array_equal(got[0][3], want[0][3]) and np.array_equal(got[0][2], want[0][2])
+    o = sk.build_out_coords(c, 2)
+    assert np.array_equal(o.numpy(), reference.out_coords(3, c_np, [2, 2, 2]))
