@@ -48,6 +48,22 @@ void release_kmap(sk_kmap* m) {
     if (m && m->refs.fetch_sub(1) == 1) delete m;
 }
 
+// One prepared split as row-major rows_pad x w on the host (the device keeps
+// it tile-column-major, see kmap.cu k_split_reorder).
+std::vector<int32_t> split_rows_host(sk::Prepared* p, int s, cudaStream_t st) {
+    const int b = p->begin[s], w = p->begin[s + 1] - b;
+    std::vector<int32_t> dev((size_t)p->rows_pad * w), rows((size_t)p->rows_pad * w);
+    if (!dev.empty())
+        SK_CUDA(cudaMemcpyAsync(dev.data(), p->entries.as<int32_t>() + (size_t)p->rows_pad * b,
+                                dev.size() * 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < p->rows_pad; ++r)
+        for (int j = 0; j < w; ++j)
+            rows[(size_t)r * w + j] =
+                dev[((size_t)(r / sk::kTileM) * w + j) * sk::kTileM + (r % sk::kTileM)];
+    return rows;
+}
+
 sk_coords* make_coords(sk_ctx* ctx, int dims, int n, const int32_t* src, bool host,
                        const int32_t* stride_tag, cudaStream_t st) {
     sk::validate(ctx != nullptr, "null context");
@@ -284,9 +300,9 @@ sk_status sk_kmap_export_split(sk_kmap* m, int splits, int pad_multiple, int s, 
         *n_rows = rows;
         *mask_words = words;
         if (h_entries) {
+            std::vector<int32_t> e = split_rows_host(p, s, st);
+            std::memcpy(h_entries, e.data(), (size_t)rows * w * 4);
             // device rows are padded to lcm(pad, 128) >= rows; the tail is pad rows
-            SK_CUDA(cudaMemcpyAsync(h_entries, p->entries.as<int32_t>() + (size_t)p->rows_pad * b,
-                                    (size_t)rows * w * 4, cudaMemcpyDeviceToHost, st));
             SK_CUDA(cudaMemcpyAsync(h_out_row, p->out_row.as<int32_t>() + (size_t)s * p->rows_pad,
                                     (size_t)rows * 4, cudaMemcpyDeviceToHost, st));
             SK_CUDA(cudaMemcpyAsync(h_masks,
@@ -334,12 +350,9 @@ sk_status sk_kmap_count_macs(sk_kmap* m, int splits, int pad_multiple, int warp_
         int64_t eff = 0, charged = 0;
         const int64_t unit = (int64_t)c_in * c_out;
         for (int s = 0; s < p->num_splits; ++s) {
-            const int b = p->begin[s], w = p->begin[s + 1] - b;
-            std::vector<int32_t> e((size_t)rows * w);
-            if (!e.empty())
-                SK_CUDA(cudaMemcpyAsync(e.data(), p->entries.as<int32_t>() + (size_t)p->rows_pad * b,
-                                        e.size() * 4, cudaMemcpyDeviceToHost, st));
-            SK_CUDA(cudaStreamSynchronize(st));
+            const int w = p->begin[s + 1] - p->begin[s];
+            std::vector<int32_t> e = split_rows_host(p, s, st);
+            e.resize((size_t)rows * w);
             for (int32_t v : e) eff += v != -1;
             for (int r0 = 0; r0 < rows; r0 += warp_rows)
                 for (int j = 0; j < w; ++j) {

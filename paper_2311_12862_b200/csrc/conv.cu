@@ -20,80 +20,78 @@
 //    mirrored offset and B = W[k'] read as [c_in][c_out] (already K-major);
 //    forward uses B = W^T (a tiny per-call transpose to [k][c_out][c_in]).
 //
-// fp16/bf16 -> k_gconv_tc: warp-specialised tcgen05 kernel
-//   warps 0-3  producers: cp.async 16B gathers of A rows (zero-fill for
-//              sentinels/channel tails) and B rows into 128B/64B/32B-swizzled
-//              K-major smem stages; cp.async.wait_group + fence.proxy.async +
-//              mbarrier arrive publish a stage LAG steps later
-//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
-//              N=BN, K=16 per instruction), tcgen05.commit frees stages
-//   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
+// fp16/bf16 -> k_gconv_tc: warp-specialised, persistent tcgen05 kernel
+//   warp 0     producer: per k-step one TMA tile::gather4 per lane (4 rows
+//              each = the 128-row A tile, sentinel rows -> out-of-bounds
+//              coordinate -> TMA zero fill) + one 2D TMA tile for B, both
+//              into 128B/64B/32B-swizzled K-major stages completing on an
+//              mbarrier (expect_tx). The 128 row indices of each column step
+//              arrive by a 512B cp.async.bulk into a 16-slot smem ring,
+//              prefetched 12 column steps ahead.
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
+//              N=BN, K=16 per instruction); tcgen05.commit frees stages
+//   warps 2-5  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
 //              buffered TMEM accumulators so tile i's epilogue overlaps tile
 //              i+1's MMAs
 // fp32 -> k_gconv_simt: the 1e-5 parity path (FFMA, fp32 accumulate).
+#include <cuda.h>
+
 #include "sk_internal.hpp"
 
 namespace sk {
 
 namespace {
 
-constexpr int kThreadsTC = 288;  // 9 warps
-constexpr int kProducerThreads = 128;
-constexpr int kLag = 2;
+constexpr int kThreadsTC = 192;  // 6 warps: TMA producer, MMA, 4 x epilogue
+constexpr int kIdxRing = 16;     // index-column ring slots (512B each)
+constexpr int kIdxAhead = 12;    // column steps prefetched ahead (< kIdxRing)
 
 struct ConvArgs {
     int mode;  // 0 = OS rows (implicit GEMM), 1 = WS pairs (FOD / GGS GEMM)
-    // OS mode
+    // OS mode (prepared map, entries tile-column-major [tile][col][128])
     const int* entries;
-    const int* out_row;  // nullable: identity rows < n_rows_valid
+    const int* out_row;
     const unsigned long long* tile_masks;
     const int* split_begin;
     int ns, rows_pad, n_tiles, n_rows_valid;
-    // WS mode
-    const long long* ws_ptr;
+    // WS mode: per-offset pair lists padded to 128-pair tiles (-1 pads)
     const int* ws_tile_ptr;
-    const int* ws_in;
-    const int* ws_out;
+    const int* in_pad;
+    const int* out_pad;
     int a_identity, out_identity;
     int kd;
     // operands
     const void* a;
-    int k_total;
+    int k_total, n_rows_a;
     const void* b;
     int n_total, mirror;
     void* y;
     int out_mode;  // 0 store T, 1 store f32, 2 red.add f32, 3 RMW f32
     int ld_y;
     int n_ntiles, bn;
-    int items;  // OS mode item count (WS mode: derived on device)
-    int split_only;  // >= 0: only items of this split (deterministic sequencing)
-    int offset_only; // >= 0: WS mode only tiles of this offset
+    int items;        // OS mode item count (WS mode: derived on device)
+    int split_only;   // >= 0: only items of this split (deterministic sequencing)
+    int offset_only;  // >= 0: WS mode only tiles of this offset
 };
 
 struct Item {
-    bool valid;
     int s, t, nt, k;   // split / tile / n-tile / offset (WS)
     int w;             // split width (OS) or 1 (WS)
     int col_begin;     // global offset of column 0
-    long long row0;    // first row: OS tile row, or first pair index (WS)
-    long long row_end; // WS: end of this offset's pairs
+    long long row0;    // first row: OS tile row within the split, WS padded pair index
     unsigned long long m0, m1;
     int biw0, bw1;
 };
 
-__device__ __forceinline__ int ws_items(const ConvArgs& p) {
+__device__ __forceinline__ int num_items(const ConvArgs& p) {
+    if (p.mode == 0) return p.items;
     if (p.offset_only >= 0)
         return (p.ws_tile_ptr[p.offset_only + 1] - p.ws_tile_ptr[p.offset_only]) * p.n_ntiles;
     return p.ws_tile_ptr[p.kd] * p.n_ntiles;
 }
 
-__device__ __forceinline__ int num_items(const ConvArgs& p) {
-    return p.mode == 0 ? p.items : ws_items(p);
-}
-
 __device__ Item decode(const ConvArgs& p, int item) {
     Item it;
-    it.valid = true;
     if (p.mode == 0) {
         const int per = p.n_tiles * p.n_ntiles;
         it.s = p.split_only >= 0 ? p.split_only : item / per;
@@ -103,7 +101,6 @@ __device__ Item decode(const ConvArgs& p, int item) {
         it.col_begin = p.split_begin[it.s];
         it.w = p.split_begin[it.s + 1] - it.col_begin;
         it.row0 = (long long)it.t * kTileM;
-        it.row_end = 0;
         it.k = -1;
         const unsigned long long* tm = p.tile_masks + ((size_t)it.s * p.n_tiles + it.t) * 2;
         it.m0 = tm[0];
@@ -122,11 +119,10 @@ __device__ Item decode(const ConvArgs& p, int item) {
         }
         it.k = k;
         it.s = 0;
-        it.t = tile - p.ws_tile_ptr[k];
+        it.t = tile;
         it.w = 1;
         it.col_begin = k;
-        it.row0 = p.ws_ptr[k] + (long long)it.t * kTileM;
-        it.row_end = p.ws_ptr[k + 1];
+        it.row0 = (long long)tile * kTileM;
         it.m0 = 1;  // one active "column"
         it.m1 = 0;
         it.biw0 = 1;
@@ -135,7 +131,7 @@ __device__ Item decode(const ConvArgs& p, int item) {
     return it;
 }
 
-// Iterate active columns in ascending order. Returns -1 when done.
+// Active columns in ascending order (big-endian masks, kmap.cpp:38-45); -1 = done.
 __device__ __forceinline__ int next_col(unsigned long long& m0, unsigned long long& m1, int biw0,
                                         int bw1) {
     if (m0) {
@@ -151,27 +147,61 @@ __device__ __forceinline__ int next_col(unsigned long long& m0, unsigned long lo
     return -1;
 }
 
-// A-row index for tile row r at (split-local) column j; -1 = zero row
+// 128 A-row indices of one column step (contiguous, 512B aligned)
+__device__ __forceinline__ const int* idx_column(const ConvArgs& p, const Item& it, int j) {
+    if (p.mode == 0)
+        return p.entries + (size_t)p.rows_pad * it.col_begin +
+               ((size_t)it.t * it.w + j) * kTileM;
+    return p.in_pad + it.row0;
+}
+
 __device__ __forceinline__ int a_index(const ConvArgs& p, const Item& it, int r, int j) {
-    if (p.mode == 0) {
-        const long long row = it.row0 + r;
-        return __ldg(p.entries + (size_t)p.rows_pad * it.col_begin + (size_t)row * it.w + j);
-    }
-    const long long pi = it.row0 + r;
-    if (pi >= it.row_end) return -1;
-    return p.a_identity ? (int)pi : __ldg(p.ws_in + pi);
+    if (p.mode == 1 && p.a_identity) return (int)(it.row0 + r);
+    return __ldg(idx_column(p, it, j) + r);
 }
 
 __device__ __forceinline__ long long out_index(const ConvArgs& p, const Item& it, int r) {
     if (p.mode == 0) {
         const long long row = it.row0 + r;
-        if (p.out_row) return __ldg(p.out_row + (size_t)it.s * p.rows_pad + row);
-        return row < p.n_rows_valid ? row : -1;
+        return __ldg(p.out_row + (size_t)it.s * p.rows_pad + row);
     }
     const long long pi = it.row0 + r;
-    if (pi >= it.row_end) return -1;
-    return p.out_identity ? pi : (long long)__ldg(p.ws_out + pi);
+    return p.out_identity ? pi : (long long)__ldg(p.out_pad + pi);
 }
+
+// iterator over the column steps (item, active column) of this CTA
+struct Cursor {
+    int item, n_items, j;
+    Item it;
+    unsigned long long m0, m1;
+    bool done;
+    __device__ void load(const ConvArgs& p) {
+        while (item < n_items) {
+            it = decode(p, item);
+            m0 = it.m0;
+            m1 = it.m1;
+            j = next_col(m0, m1, it.biw0, it.bw1);
+            if (j >= 0) {
+                done = false;
+                return;
+            }
+            item += gridDim.x;
+        }
+        done = true;
+    }
+    __device__ void init(const ConvArgs& p, int n) {
+        n_items = n;
+        item = blockIdx.x;
+        load(p);
+    }
+    __device__ void advance(const ConvArgs& p) {
+        j = next_col(m0, m1, it.biw0, it.bw1);
+        if (j < 0) {
+            item += gridDim.x;
+            load(p);
+        }
+    }
+};
 
 template <typename T>
 struct Fmt;
@@ -203,40 +233,65 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
 }
 
-// K-major smem descriptor; row = KC*2 bytes, 8-row swizzle atoms.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm, int col, int r0,
+                                            int r1, int r2, int r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_tile2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                           uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// K-major smem descriptor; row = KC*2 bytes, 8-row swizzle atoms (SBO).
 template <int KC>
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr) {
-    constexpr uint32_t RB = KC * 2;                       // 32 / 64 / 128
+    constexpr uint32_t RB = KC * 2;                                  // 32 / 64 / 128
     constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);  // SW128/SW64/SW32
     constexpr uint64_t sbo = (8 * RB) >> 4;
     return (uint64_t)((saddr >> 4) & 0x3FFF) | (sbo << 32) | (1ull << 46) | (layout << 61);
 }
 
-// byte offset of 16B chunk q of row r inside a K-major swizzled tile
-template <int KC>
-__device__ __forceinline__ uint32_t swz(int r, int q) {
-    constexpr uint32_t RB = KC * 2;
-    constexpr uint32_t B = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
-    uint32_t off = (uint32_t)r * RB + (uint32_t)q * 16;
-    return off ^ (((off >> 7) & B) << 4);
-}
-
 template <typename T, int KC>
-__global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, int stages) {
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+               const ConvArgs p, int stages) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024B alignment for the swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int BN = p.bn;
     const uint32_t a_bytes = kTileM * KC * 2;
     const uint32_t b_bytes = (uint32_t)BN * KC * 2;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* stage_base = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+    int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(idx_ring + kIdxRing * kTileM);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;
-    uint64_t* tempty = bars + 2 * stages + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+    uint64_t* tempty = tfull + 2;
+    uint64_t* ifull = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ifull + kIdxRing);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -244,77 +299,81 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, in
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < stages; ++i) {
-            mbar_init(&full[i], kProducerThreads);
+            mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
         }
+        for (int i = 0; i < kIdxRing; ++i) mbar_init(&ifull[i], 1);
         fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
     }
-    if (warp == 4) tmem_alloc(tmem_slot, ncols);
+    if (warp == 1) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int n_items = num_items(p);
     const int nchunks = (p.k_total + KC - 1) / KC;
-    const T* __restrict__ A = static_cast<const T*>(p.a);
-    const T* __restrict__ Bw = static_cast<const T*>(p.b);
+    const bool use_ring = !(p.mode == 1 && p.a_identity);
 
-    if (warp < 4) {
-        // ================= producers =================
-        const int r = threadIdx.x;  // tile row owned by this thread
-        long long step = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-            Item it = decode(p, item);
-            unsigned long long m0 = it.m0, m1 = it.m1;
-            const int n0 = it.nt * BN;
-            for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
-                 j = next_col(m0, m1, it.biw0, it.bw1)) {
-                const int ai = a_index(p, it, r, j);
-                const int kg = it.col_begin + j;
-                const int kb = p.mirror ? p.kd - 1 - kg : kg;
-                const T* arow = A + (size_t)(ai < 0 ? 0 : ai) * p.k_total;
-                for (int c = 0; c < nchunks; ++c, ++step) {
-                    const int stage = (int)(step % stages);
-                    const uint32_t ph = (uint32_t)((step / stages) & 1);
-                    mbar_wait(&empty[stage], ph ^ 1);
-                    uint8_t* sa = stage_base + (size_t)stage * stage_bytes;
-                    uint8_t* sb = sa + a_bytes;
-                    const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
-#pragma unroll
-                    for (int q = 0; q < KC / 8; ++q) {
-                        const int col = c * KC + q * 8;
-                        const bool ok = ai >= 0 && col < p.k_total;
-                        cp_async16(sa_u + swz<KC>(r, q), ok ? (const void*)(arow + col) : (const void*)A,
-                                   ok ? 16u : 0u);
-                    }
-                    for (int i = threadIdx.x; i < BN * (KC / 8); i += kProducerThreads) {
-                        const int n = i / (KC / 8), q = i % (KC / 8);
-                        const int col = c * KC + q * 8;
-                        const bool ok = (n0 + n) < p.n_total && col < p.k_total;
-                        const T* src = Bw + ((size_t)kb * p.n_total + n0 + n) * p.k_total + col;
-                        cp_async16(sb_u + swz<KC>(n, q), ok ? (const void*)src : (const void*)Bw,
-                                   ok ? 16u : 0u);
-                    }
-                    cp_async_commit();
-                    if (step >= kLag) {
-                        cp_async_wait<kLag>();
-                        fence_proxy_async_smem();
-                        mbar_arrive(&full[(int)((step - kLag) % stages)]);
-                    }
-                }
+    if (warp == 0) {
+        // ============ producer: TMA gather4 (A) + 2D tile (B) + index prefetch ============
+        Cursor cur, pf;
+        cur.init(p, n_items);
+        pf.init(p, n_items);
+        long long cs_pf = 0;
+        auto issue_idx = [&]() {
+            if (lane == 0) {
+                const int slot = (int)(cs_pf % kIdxRing);
+                mbar_expect_tx(&ifull[slot], kTileM * 4);
+                bulk_g2s(smem_u32(idx_ring + slot * kTileM), idx_column(p, pf.it, pf.j),
+                         kTileM * 4, &ifull[slot]);
             }
+            pf.advance(p);
+            ++cs_pf;
+        };
+        if (use_ring)
+            for (int d = 0; d < kIdxAhead && !pf.done; ++d) issue_idx();
+        long long cs = 0, step = 0;
+        while (!cur.done) {
+            int r[4];
+            if (use_ring) {
+                const int slot = (int)(cs % kIdxRing);
+                mbar_wait(&ifull[slot], (uint32_t)((cs / kIdxRing) & 1));
+                int4 v = reinterpret_cast<const int4*>(idx_ring + slot * kTileM)[lane];
+                r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) r[u] = (int)(cur.it.row0 + lane * 4 + u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) r[u] = r[u] < 0 ? p.n_rows_a : r[u];  // OOB -> zero fill
+            const int kg = cur.it.col_begin + cur.j;
+            const int kb = p.mirror ? p.kd - 1 - kg : kg;
+            const int brow = kb * p.n_total + cur.it.nt * BN;
+            for (int c = 0; c < nchunks; ++c, ++step) {
+                const int stage = (int)(step % stages);
+                mbar_wait(&empty[stage], (uint32_t)(((step / stages) & 1) ^ 1));
+                const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
+                if (lane == 0) {
+                    mbar_expect_tx(&full[stage], stage_bytes);
+                    tma_tile2d(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+                }
+                __syncwarp();
+                tma_gather4(sa + (uint32_t)lane * 4 * KC * 2, &tm_a, c * KC, r[0], r[1], r[2], r[3],
+                            &full[stage]);
+            }
+            __syncwarp();
+            if (use_ring && !pf.done) issue_idx();
+            cur.advance(p);
+            ++cs;
         }
-        // drain the last kLag stages
-        cp_async_wait<0>();
-        fence_proxy_async_smem();
-        for (long long s = step - kLag < 0 ? 0 : step - kLag; s < step; ++s)
-            mbar_arrive(&full[(int)(s % stages)]);
-    } else if (warp == 4) {
-        // ================= MMA issuer =================
+    } else if (warp == 1) {
+        // ================= MMA issuer (one thread) =================
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
         long long step = 0;
@@ -322,8 +381,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, in
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             Item it = decode(p, item);
             const int acc = local & 1;
-            const uint32_t aph = (uint32_t)((local >> 1) & 1);
-            mbar_wait(&tempty[acc], aph ^ 1);
+            mbar_wait(&tempty[acc], (uint32_t)(((local >> 1) & 1) ^ 1));
             tc_fence_after();
             const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
             unsigned long long m0 = it.m0, m1 = it.m1;
@@ -332,18 +390,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, in
                  j = next_col(m0, m1, it.biw0, it.bw1)) {
                 for (int c = 0; c < nchunks; ++c, ++step) {
                     const int stage = (int)(step % stages);
-                    const uint32_t ph = (uint32_t)((step / stages) & 1);
-                    mbar_wait(&full[stage], ph);
+                    mbar_wait(&full[stage], (uint32_t)((step / stages) & 1));
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
                         const uint32_t sb = sa + a_bytes;
 #pragma unroll
-                        for (int kk = 0; kk < KC / 16; ++kk) {
+                        for (int kk = 0; kk < KC / 16; ++kk)
                             tc_mma_f16(d_tmem, kmajor_desc<KC>(sa + kk * 32),
                                        kmajor_desc<KC>(sb + kk * 32), idesc,
                                        (first && kk == 0) ? 0u : 1u);
-                        }
                         tc_commit(&empty[stage]);
                     }
                     __syncwarp();
@@ -354,17 +410,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, in
             __syncwarp();
         }
     } else {
-        // ================= epilogue =================
-        const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        // ================= epilogue (warps 2-5 -> TMEM lane quadrants 2,3,0,1) =================
+        const int quad = warp & 3;
         const int r = quad * 32 + lane;
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             Item it = decode(p, item);
+            const long long orow = out_index(p, it, r);  // issued before the wait
             const int acc = local & 1;
-            const uint32_t aph = (uint32_t)((local >> 1) & 1);
-            mbar_wait(&tfull[acc], aph);
+            mbar_wait(&tfull[acc], (uint32_t)((local >> 1) & 1));
             tc_fence_after();
-            const long long orow = out_index(p, it, r);
             const bool empty_tile = (it.m0 | it.m1) == 0;
             const int n0 = it.nt * BN;
             for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -420,7 +475,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_gconv_tc(const ConvArgs p, in
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 4) tmem_dealloc(tmem, ncols);
+    if (warp == 1) tmem_dealloc(tmem, ncols);
 }
 
 // ---------------------------------------------------------------------------
@@ -538,34 +593,37 @@ __global__ void k_convert_out(const float* __restrict__ src, long long n, T* __r
     if (i < n) dst[i] = from_f<T>(src[i]);
 }
 
-// GGS gather: buf[p] = x[in[p]] (16B vectors; c multiple of 8 elements of T
-// for 2-byte T, or scalar fallback)
+// GGS gather over the padded pair lists: buf[i] = x[in_pad[i]] (zeros for pads)
 template <typename T>
 __global__ void k_gather_rows(const T* __restrict__ x, int c, const int* __restrict__ idx,
-                              const long long* __restrict__ total, T* __restrict__ buf) {
-    const long long n = *total;
-    const long long nelem = n * c;
+                              const int* __restrict__ tile_total, T* __restrict__ buf) {
+    const long long nelem = (long long)(*tile_total) * kTileM * c;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
          i += (long long)gridDim.x * blockDim.x) {
         long long pr = i / c;
         int cc = (int)(i % c);
-        buf[i] = x[(size_t)idx[pr] * c + cc];
+        int j = idx[pr];
+        buf[i] = j >= 0 ? x[(size_t)j * c + cc] : from_f<T>(0.f);
     }
 }
 
-// GGS scatter-add into fp32 accumulator: y[out[p]] += buf[p]
+// GGS scatter-add into the fp32 accumulator: y[out_pad[i]] += buf[i] over the
+// padded tiles [tile_lo, tile_hi); deterministic = one offset per launch
+// (out rows unique within an offset, exec.cpp:140-146) with plain RMW.
 __global__ void k_scatter_add(const float* __restrict__ buf, int c, const int* __restrict__ idx,
-                              const long long* __restrict__ lo, const long long* __restrict__ hi,
+                              const int* __restrict__ tile_lo, const int* __restrict__ tile_hi,
                               float* __restrict__ y, int deterministic) {
-    const long long a = *lo, b = *hi;
+    const long long a = (long long)(*tile_lo) * kTileM, b = (long long)(*tile_hi) * kTileM;
     const long long nelem = (b - a) * c;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
          i += (long long)gridDim.x * blockDim.x) {
         long long pr = a + i / c;
         int cc = (int)(i % c);
+        int o = idx[pr];
+        if (o < 0) continue;
         float v = buf[pr * c + cc];
-        float* d = y + (size_t)idx[pr] * c + cc;
-        if (deterministic) *d += v;  // one offset at a time: out rows unique
+        float* d = y + (size_t)o * c + cc;
+        if (deterministic) *d += v;
         else atomicAdd(d, v);
     }
 }
@@ -616,36 +674,71 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
 
 size_t elem_size(sk_dtype dt) { return dt == SK_F32 ? 4 : 2; }
 
-struct Launch {
-    sk_ctx* ctx;
-    cudaStream_t st;
-};
+// ---- tensor maps (driver entry point resolved once through cudart) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess)
+            fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// 2D row-major [rows][cols] half tensor, box {kc, box_rows}, swizzle = kc*2 bytes
+CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, int kc,
+                      int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)std::max<long long>(rows, 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kc, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUtensorMapSwizzle sw = kc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : kc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = encode_fn()(&m, dt == SK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                             2, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
 
 template <typename T, int KC>
-void launch_tc_kc(const ConvArgs& a, int grid, cudaStream_t st) {
+void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
     const int bn = a.bn;
     const size_t stage_bytes = (size_t)kTileM * KC * 2 + (size_t)bn * KC * 2;
-    int stages = (int)std::min<size_t>(8, (200 * 1024) / stage_bytes);
-    stages = std::max(stages, 3);
-    const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+    int stages = (int)std::min<size_t>(8, (196 * 1024) / stage_bytes);
+    stages = std::max(stages, 2);
+    const size_t smem = 1024 + stages * stage_bytes + kIdxRing * kTileM * 4 +
+                        (2 * stages + 4 + kIdxRing) * 8 + 16;
+    CUtensorMap ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, 1);
+    CUtensorMap tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
     SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages);
+    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(ta, tb, a, stages);
     SK_LAUNCH_CHECK();
 }
 
 template <typename T>
-void launch_tc(const ConvArgs& a, int grid, cudaStream_t st) {
-    if (a.k_total % 64 == 0) launch_tc_kc<T, 64>(a, grid, st);
-    else if (a.k_total % 32 == 0) launch_tc_kc<T, 32>(a, grid, st);
-    else launch_tc_kc<T, 16>(a, grid, st);
+void launch_tc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
+    if (a.k_total % 64 == 0) launch_tc_kc<T, 64>(a, dt, grid, st);
+    else if (a.k_total % 32 == 0) launch_tc_kc<T, 32>(a, dt, grid, st);
+    else launch_tc_kc<T, 16>(a, dt, grid, st);
 }
 
 bool tc_ok(sk_dtype dt, int k_total, int n_total) {
     return dt != SK_F32 && k_total % 8 == 0 && n_total % 16 == 0;
 }
 
-// pick the N tile: whole C_out when <= 256, else balanced tiles of <= 256
+// N tile: whole C_out when <= 256 (or <= cta_n), else balanced tiles
 void pick_n_tiling(int n_total, int cta_n, bool tc, int& bn, int& n_nt) {
     if (!tc) {
         bn = kSimtN;
@@ -658,18 +751,14 @@ void pick_n_tiling(int n_total, int cta_n, bool tc, int& bn, int& n_nt) {
     bn = (int)ceil_div(ceil_div(n_total, n_nt), 16) * 16;
 }
 
-void launch_gconv(sk_ctx* ctx, sk_dtype dt, ConvArgs a, bool ws_mode_grid, cudaStream_t st) {
+void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a, cudaStream_t st) {
     const bool tc = tc_ok(dt, a.k_total, a.n_total);
     int grid;
-    if (a.mode == 0) {
-        grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
-    } else {
-        (void)ws_mode_grid;
-        grid = ctx->num_sms * (tc ? 1 : 8);
-    }
+    if (a.mode == 0) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
+    else grid = ctx->num_sms * (tc ? 1 : 8);
     if (tc) {
-        if (dt == SK_F16) launch_tc<__half>(a, grid, st);
-        else launch_tc<__nv_bfloat16>(a, grid, st);
+        if (dt == SK_F16) launch_tc<__half>(a, dt, grid, st);
+        else launch_tc<__nv_bfloat16>(a, dt, grid, st);
     } else {
         if (dt == SK_F32) k_gconv_simt<float><<<grid, 256, 0, st>>>(a);
         else if (dt == SK_F16) k_gconv_simt<__half><<<grid, 256, 0, st>>>(a);
@@ -699,24 +788,33 @@ ConvArgs base_args() {
     return a;
 }
 
+template <typename T>
+void gather_rows(const void* x, int c, const int* idx, const int* tiles, void* buf, int g,
+                 cudaStream_t st) {
+    k_gather_rows<T><<<g, 256, 0, st>>>(static_cast<const T*>(x), c, idx, tiles,
+                                        static_cast<T*>(buf));
+    SK_LAUNCH_CHECK();
+}
+
 }  // namespace
 
-// Forward (dgrad = false) or dgrad (dgrad = true; m is the FORWARD map).
+// Forward (dgrad = false) or dgrad (dgrad = true; m_fwd is the FORWARD map).
 void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st) {
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     validate(cfg.splits >= 0, "splits must be >= 0");
     validate(cfg.kind >= 0 && cfg.kind <= 2, "unknown dataflow kind");
     sk_kmap* m = dgrad ? kmap_transpose(m_fwd, st) : m_fwd;
-    // GEMM shape: A rows have k_total channels, output has n_total channels
+    // GEMM shape: A rows carry k_total channels, the output n_total
     const int k_total = dgrad ? c_out : c_in;
     const int n_total = dgrad ? c_in : c_out;
     const size_t es = elem_size(dt);
     const long long y_elems = (long long)m->n_out * n_total;
     if (m->n_out == 0) return;
 
-    // B operand: forward -> W^T [kd][c_out][c_in]; dgrad -> W [kd][c_in][c_out]
-    // with mirrored offsets (WeightTensor::transposed, exec.cpp:32-43)
+    // B operand [kd][n_total][k_total] (K-major): forward -> W^T per offset;
+    // dgrad -> W itself with mirrored offsets (WeightTensor::transposed,
+    // exec.cpp:32-43)
     DevBuf wt;
     const void* b = w;
     if (!dgrad) {
@@ -734,6 +832,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     a.kd = m->kd;
     a.a = x;
     a.k_total = k_total;
+    a.n_rows_a = m->n_in;
     a.b = b;
     a.n_total = n_total;
     a.mirror = dgrad ? 1 : 0;
@@ -743,15 +842,11 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
 
     if (cfg.kind == SK_IMPLICIT_GEMM) {
         Prepared* pr = kmap_prepare(m, cfg.splits, kTileM, st);
-        DevBuf d_begin;
-        d_begin.alloc((pr->num_splits + 1) * 4, st);
-        SK_CUDA(cudaMemcpyAsync(d_begin.p, pr->begin.data(), (pr->num_splits + 1) * 4,
-                                cudaMemcpyHostToDevice, st));
         a.mode = 0;
         a.entries = pr->entries.as<int>();
         a.out_row = pr->out_row.as<int>();
         a.tile_masks = pr->tile_masks.as<unsigned long long>();
-        a.split_begin = d_begin.as<int>();
+        a.split_begin = pr->d_begin.as<int>();
         a.ns = pr->num_splits;
         a.rows_pad = pr->rows_pad;
         a.n_tiles = pr->rows_pad / kTileM;
@@ -760,7 +855,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
             a.items = a.n_tiles * a.n_ntiles;
             a.y = y;
             a.out_mode = dt == SK_F32 ? 1 : 0;
-            launch_gconv(ctx, dt, a, false, st);
+            launch_gconv(ctx, dt, a, st);
         } else {
             DevBuf acc;
             float* yf = dt == SK_F32 ? static_cast<float*>(y) : nullptr;
@@ -771,25 +866,25 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
             SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
             a.y = yf;
             if (det) {
-                // splits accumulate in order: partial sums telescope
+                // splits accumulate in order so partial sums telescope
                 // (implicit_gemm_impl deterministic branch, exec.cpp:240-246)
                 a.out_mode = 3;
                 a.items = a.n_tiles * a.n_ntiles;
                 for (int s = 0; s < pr->num_splits; ++s) {
                     a.split_only = s;
-                    launch_gconv(ctx, dt, a, false, st);
+                    launch_gconv(ctx, dt, a, st);
                 }
             } else {
                 a.out_mode = 2;
                 a.items = pr->num_splits * a.n_tiles * a.n_ntiles;
-                launch_gconv(ctx, dt, a, false, st);
+                launch_gconv(ctx, dt, a, st);
             }
             if (dt != SK_F32) convert_from_f32(dt, yf, y_elems, y, st);
         }
         return;
     }
 
-    // WS-based dataflows
+    // WS-based dataflows over the per-offset, 128-padded pair lists
     kmap_ensure_ws(m, st);
     DevBuf acc;
     float* yf = dt == SK_F32 ? static_cast<float*>(y) : nullptr;
@@ -799,58 +894,51 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     }
     SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
     a.mode = 1;
-    a.ws_ptr = m->ws_ptr.as<long long>();
     a.ws_tile_ptr = m->ws_tile_ptr.as<int>();
-    a.ws_in = m->ws_in.as<int>();
-    a.ws_out = m->ws_out.as<int>();
+    a.in_pad = m->ws_in_pad.as<int>();
+    a.out_pad = m->ws_out_pad.as<int>();
+    const int* tile_ptr = m->ws_tile_ptr.as<int>();
 
     if (cfg.kind == SK_FETCH_ON_DEMAND) {
         a.y = yf;
-        a.ld_y = n_total;
         if (det) {
             a.out_mode = 3;
             for (int k = 0; k < m->kd; ++k) {
                 a.offset_only = k;
-                launch_gconv(ctx, dt, a, true, st);
+                launch_gconv(ctx, dt, a, st);
             }
         } else {
             a.out_mode = 2;
-            launch_gconv(ctx, dt, a, true, st);
+            launch_gconv(ctx, dt, a, st);
         }
     } else {
         // gather -> GEMM -> scatter-add (exec.cpp:117-158)
         const int64_t P = kmap_total_pairs(m, st);
         if (P > 0) {
+            const long long rows_pad = P + (long long)m->kd * kTileM;  // >= tiles*128
             DevBuf ga, gc;
-            ga.alloc((size_t)P * k_total * es, st);
-            gc.alloc((size_t)P * n_total * 4, st);
+            ga.alloc((size_t)rows_pad * k_total * es, st);
+            gc.alloc((size_t)rows_pad * n_total * 4, st);
             const int g = ctx->num_sms * 8;
-            if (dt == SK_F32)
-                k_gather_rows<float><<<g, 256, 0, st>>>((const float*)x, k_total, a.ws_in,
-                                                        a.ws_ptr + m->kd, ga.as<float>());
-            else if (dt == SK_F16)
-                k_gather_rows<__half><<<g, 256, 0, st>>>((const __half*)x, k_total, a.ws_in,
-                                                         a.ws_ptr + m->kd, ga.as<__half>());
-            else
-                k_gather_rows<__nv_bfloat16><<<g, 256, 0, st>>>(
-                    (const __nv_bfloat16*)x, k_total, a.ws_in, a.ws_ptr + m->kd,
-                    ga.as<__nv_bfloat16>());
-            SK_LAUNCH_CHECK();
+            if (dt == SK_F32) gather_rows<float>(x, k_total, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
+            else if (dt == SK_F16) gather_rows<__half>(x, k_total, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
+            else gather_rows<__nv_bfloat16>(x, k_total, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
             a.a = ga.p;
+            a.n_rows_a = (int)rows_pad;
             a.a_identity = 1;
             a.out_identity = 1;
             a.y = gc.p;
             a.out_mode = 1;
-            launch_gconv(ctx, dt, a, true, st);
+            launch_gconv(ctx, dt, a, st);
             if (det) {
                 for (int k = 0; k < m->kd; ++k) {
-                    k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.ws_out,
-                                                     a.ws_ptr + k, a.ws_ptr + k + 1, yf, 1);
+                    k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.out_pad,
+                                                     tile_ptr + k, tile_ptr + k + 1, yf, 1);
                     SK_LAUNCH_CHECK();
                 }
             } else {
-                k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.ws_out, a.ws_ptr,
-                                                 a.ws_ptr + m->kd, yf, 0);
+                k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.out_pad, tile_ptr,
+                                                 tile_ptr + m->kd, yf, 0);
                 SK_LAUNCH_CHECK();
             }
         }

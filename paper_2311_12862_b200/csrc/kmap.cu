@@ -279,8 +279,11 @@ __global__ void __launch_bounds__(1024) k_ws_scan(const int* __restrict__ blk_co
 __global__ void __launch_bounds__(kQB) k_ws_scatter(const int* __restrict__ os, int kd,
                                                     const long long* __restrict__ blk_off,
                                                     const long long* __restrict__ ptr,
+                                                    const int* __restrict__ tile_ptr,
                                                     int* __restrict__ ws_in,
-                                                    int* __restrict__ ws_out) {
+                                                    int* __restrict__ ws_out,
+                                                    int* __restrict__ in_pad,
+                                                    int* __restrict__ out_pad) {
     extern __shared__ int sh[];
     int* tile = sh;
     __shared__ int wcnt[kQB / 32];
@@ -297,10 +300,15 @@ __global__ void __launch_bounds__(kQB) k_ws_scatter(const int* __restrict__ os, 
         int before = 0;
         for (int w = 0; w < warp; ++w) before += wcnt[w];
         if (j >= 0) {
-            long long pos = ptr[k] + blk_off[(size_t)blockIdx.x * kd + k] + before +
+            long long rel = blk_off[(size_t)blockIdx.x * kd + k] + before +
                             __popc(hit & ((1u << lane) - 1));
+            long long pos = ptr[k] + rel;
             ws_in[pos] = j;
             ws_out[pos] = row;
+            // per-offset lists padded to 128-pair tiles (-1 pads) for FOD/GGS tiles
+            long long pp = (long long)tile_ptr[k] * kTileM + rel;
+            in_pad[pp] = j;
+            out_pad[pp] = row;
         }
         __syncthreads();
     }
@@ -349,10 +357,12 @@ __global__ void k_split_reorder(const int* __restrict__ os, int n, int kd, int n
     if (i >= (long long)rows_pad * ns) return;
     int s = (int)(i / rows_pad), p = (int)(i % rows_pad);
     int b = begin[s], w = begin[s + 1] - b, words = (w + 63) / 64;
-    int* dst = entries + (size_t)rows_pad * b + (size_t)p * w;
+    // tile-column-major: [tile][column][128 rows] so one column of one tile is a
+    // contiguous, 512B-aligned vector (one bulk copy feeds a 128-row gather)
+    int* dst = entries + (size_t)rows_pad * b + ((size_t)(p / kTileM) * w) * kTileM + (p % kTileM);
     unsigned long long* md = masks + (size_t)rows_pad * word_off[s] + (size_t)p * words;
     if (p >= n) {
-        for (int j = 0; j < w; ++j) dst[j] = -1;
+        for (int j = 0; j < w; ++j) dst[(size_t)j * kTileM] = -1;
         out_row[(size_t)s * rows_pad + p] = -1;
         for (int u = 0; u < words; ++u) md[u] = 0;
         return;
@@ -362,7 +372,7 @@ __global__ void k_split_reorder(const int* __restrict__ os, int n, int kd, int n
     unsigned long long m[2] = {0, 0};
     for (int j = 0; j < w; ++j) {
         int v = row[j];
-        dst[j] = v;
+        dst[(size_t)j * kTileM] = v;
         if (v >= 0) {
             int wi = j / 64, biw = min(64, w - wi * 64);
             m[wi] |= 1ull << (biw - 1 - (j - wi * 64));
@@ -591,6 +601,11 @@ void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
     size_t cap = (size_t)std::max<int64_t>(1, (int64_t)m->n_out * m->kd);
     m->ws_in.alloc(cap * 4, st);
     m->ws_out.alloc(cap * 4, st);
+    const size_t cap_pad = cap + (size_t)m->kd * kTileM;
+    m->ws_in_pad.alloc(cap_pad * 4, st);
+    m->ws_out_pad.alloc(cap_pad * 4, st);
+    SK_CUDA(cudaMemsetAsync(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st));
+    SK_CUDA(cudaMemsetAsync(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st));
     k_ws_scan<<<1, 1024, 0, st>>>(m->blk_counts.as<int>(), m->n_blocks, m->kd,
                                   m->blk_off.as<long long>(), m->ws_ptr.as<long long>(),
                                   m->ws_tile_ptr.as<int>());
@@ -601,17 +616,20 @@ void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
                                      (int)smem));
     k_ws_scatter<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd,
                                                  m->blk_off.as<long long>(),
-                                                 m->ws_ptr.as<long long>(), m->ws_in.as<int>(),
-                                                 m->ws_out.as<int>());
+                                                 m->ws_ptr.as<long long>(), m->ws_tile_ptr.as<int>(),
+                                                 m->ws_in.as<int>(), m->ws_out.as<int>(),
+                                                 m->ws_in_pad.as<int>(), m->ws_out_pad.as<int>());
     SK_LAUNCH_CHECK();
     m->has_ws = true;
 }
 
 int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st) {
     kmap_ensure_ws(m, st);
+    if (m->total_pairs_host >= 0) return m->total_pairs_host;
     long long v = 0;
     SK_CUDA(cudaMemcpyAsync(&v, m->ws_ptr.as<long long>() + m->kd, 8, cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));
+    m->total_pairs_host = v;
     return v;
 }
 
@@ -658,7 +676,8 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
     p->entries.alloc((size_t)p->rows_pad * kd * 4, st);
     p->out_row.alloc((size_t)p->rows_pad * ns * 4, st);
     p->masks.alloc((size_t)p->rows_pad * wacc * 8, st);
-    DevBuf d_begin, d_woff;
+    DevBuf& d_begin = p->d_begin;
+    DevBuf d_woff;
     d_begin.alloc((ns + 1) * 4, st);
     d_woff.alloc((ns + 1) * 4, st);
     SK_CUDA(cudaMemcpyAsync(d_begin.p, p->begin.data(), (ns + 1) * 4, cudaMemcpyHostToDevice, st));

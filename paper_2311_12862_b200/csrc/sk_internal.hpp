@@ -25,7 +25,8 @@ struct Prepared {
     int rows_pad = 0;     // per split
     int mask_words_max = 1;
     std::vector<int> begin;  // num_splits + 1 global offset bounds
-    DevBuf entries;          // split s at rows_pad*begin[s]: rows_pad x width_s
+    DevBuf d_begin;          // begin[] on device
+    DevBuf entries;          // split s at rows_pad*begin[s]: [tile][col][128] (tile-column-major)
     DevBuf out_row;          // num_splits x rows_pad (-1 pad rows)
     DevBuf masks;            // split s at rows_pad*word_off[s]: rows_pad x words_s
     std::vector<int> word_off;
@@ -68,7 +69,9 @@ struct sk_kmap : sk::Refcounted {
     sk::DevBuf ws_ptr;      // kd+1 int64 (exclusive scan of per-offset counts)
     sk::DevBuf blk_off;     // n_blocks x kd int64 (write cursor per block/offset)
     sk::DevBuf ws_in, ws_out;  // total_pairs (allocated at n_out*kd upper bound)
+    sk::DevBuf ws_in_pad, ws_out_pad;  // per offset padded to 128-pair tiles, -1 pads
     bool has_ws = false;
+    int64_t total_pairs_host = -1;
     // FOD/GGS tile schedule over WS lists: per offset first tile index
     sk::DevBuf ws_tile_ptr;    // kd+1 int32
     std::map<std::pair<int, int>, std::unique_ptr<sk::Prepared>> prepared;
