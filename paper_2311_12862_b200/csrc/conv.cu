@@ -21,16 +21,17 @@
 //    forward uses B = W^T (a tiny per-call transpose to [k][c_out][c_in]).
 //
 // fp16/bf16 -> k_gconv_tc: warp-specialised, persistent tcgen05 kernel
-//   warp 0     producer: per k-step one TMA tile::gather4 per lane (4 rows
-//              each = the 128-row A tile, sentinel rows -> out-of-bounds
-//              coordinate -> TMA zero fill) + one 2D TMA tile for B, both
-//              into 128B/64B/32B-swizzled K-major stages completing on an
-//              mbarrier (expect_tx). The 128 row indices of each column step
-//              arrive by a 512B cp.async.bulk into a 16-slot smem ring,
+//   warps 0-3  producers: warp w owns rows [32w, 32w+32) of the 128-row A
+//              tile and issues its 8 TMA tile::gather4 (4 rows each) from a
+//              single thread (uniform operands); sentinel rows -> out-of-
+//              bounds coordinate -> TMA zero fill. Warp 0 also loads the B
+//              tile (2D TMA). Stages are 128B/64B/32B-swizzled K-major and
+//              complete on one mbarrier (expect_tx). Row indices arrive by
+//              128B cp.async.bulk into a per-warp 16-slot smem ring,
 //              prefetched 12 column steps ahead.
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
+//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
 //              N=BN, K=16 per instruction); tcgen05.commit frees stages
-//   warps 2-5  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
+//   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
 //              buffered TMEM accumulators so tile i's epilogue overlaps tile
 //              i+1's MMAs
 // fp32 -> k_gconv_simt: the 1e-5 parity path (FFMA, fp32 accumulate).
@@ -42,8 +43,9 @@ namespace sk {
 
 namespace {
 
-constexpr int kThreadsTC = 192;  // 6 warps: TMA producer, MMA, 4 x epilogue
-constexpr int kIdxRing = 16;     // index-column ring slots (512B each)
+constexpr int kThreadsTC = 288;  // 9 warps: 4 x TMA producer, MMA, 4 x epilogue
+constexpr int kProducerWarps = 4;
+constexpr int kIdxRing = 16;     // index ring slots per producer warp (32 rows x 4B)
 constexpr int kIdxAhead = 12;    // column steps prefetched ahead (< kIdxRing)
 
 struct ConvArgs {
@@ -285,13 +287,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* stage_base = smem;
     int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(idx_ring + kIdxRing * kTileM);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(idx_ring + kProducerWarps * kIdxRing * 32);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;
     uint64_t* tempty = tfull + 2;
-    uint64_t* ifull = tempty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ifull + kIdxRing);
+    uint64_t* ifull = tempty + 2;  // [kProducerWarps][kIdxRing]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ifull + kProducerWarps * kIdxRing);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -306,12 +308,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
         }
-        for (int i = 0; i < kIdxRing; ++i) mbar_init(&ifull[i], 1);
+        for (int i = 0; i < kProducerWarps * kIdxRing; ++i) mbar_init(&ifull[i], 1);
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
     }
-    if (warp == 1) tmem_alloc(tmem_slot, ncols);
+    if (warp == kProducerWarps) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -320,59 +322,72 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int nchunks = (p.k_total + KC - 1) / KC;
     const bool use_ring = !(p.mode == 1 && p.a_identity);
 
-    if (warp == 0) {
-        // ============ producer: TMA gather4 (A) + 2D tile (B) + index prefetch ============
-        Cursor cur, pf;
-        cur.init(p, n_items);
-        pf.init(p, n_items);
-        long long cs_pf = 0;
-        auto issue_idx = [&]() {
-            if (lane == 0) {
+    if (warp < kProducerWarps) {
+        // ===== producers: warp pw owns tile rows [32 pw, 32 pw + 32): 8 TMA gather4 per
+        // k-step issued by ONE thread (uniform operands, no per-lane ELECT loop);
+        // warp 0 also arms the stage barrier and loads the B tile =====
+        if (lane == 0) {
+            const int pw = warp;
+            int* ring = idx_ring + pw * kIdxRing * 32;
+            uint64_t* myfull = ifull + pw * kIdxRing;
+            Cursor cur, pf;
+            cur.init(p, n_items);
+            pf.init(p, n_items);
+            long long cs_pf = 0;
+            auto issue_idx = [&]() {
                 const int slot = (int)(cs_pf % kIdxRing);
-                mbar_expect_tx(&ifull[slot], kTileM * 4);
-                bulk_g2s(smem_u32(idx_ring + slot * kTileM), idx_column(p, pf.it, pf.j),
-                         kTileM * 4, &ifull[slot]);
-            }
-            pf.advance(p);
-            ++cs_pf;
-        };
-        if (use_ring)
-            for (int d = 0; d < kIdxAhead && !pf.done; ++d) issue_idx();
-        long long cs = 0, step = 0;
-        while (!cur.done) {
-            int r[4];
-            if (use_ring) {
-                const int slot = (int)(cs % kIdxRing);
-                mbar_wait(&ifull[slot], (uint32_t)((cs / kIdxRing) & 1));
-                int4 v = reinterpret_cast<const int4*>(idx_ring + slot * kTileM)[lane];
-                r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
-            } else {
+                mbar_expect_tx(&myfull[slot], 128);
+                bulk_g2s(smem_u32(ring + slot * 32), idx_column(p, pf.it, pf.j) + pw * 32, 128,
+                         &myfull[slot]);
+                pf.advance(p);
+                ++cs_pf;
+            };
+            if (use_ring)
+                for (int d = 0; d < kIdxAhead && !pf.done; ++d) issue_idx();
+            long long cs = 0, step = 0;
+            while (!cur.done) {
+                int rows[32];
+                if (use_ring) {
+                    const int slot = (int)(cs % kIdxRing);
+                    mbar_wait(&myfull[slot], (uint32_t)((cs / kIdxRing) & 1));
+                    const int4* src = reinterpret_cast<const int4*>(ring + slot * 32);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) r[u] = (int)(cur.it.row0 + lane * 4 + u);
-            }
+                    for (int u = 0; u < 8; ++u) {
+                        int4 v = src[u];
+                        rows[4 * u] = v.x; rows[4 * u + 1] = v.y;
+                        rows[4 * u + 2] = v.z; rows[4 * u + 3] = v.w;
+                    }
+                } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) r[u] = r[u] < 0 ? p.n_rows_a : r[u];  // OOB -> zero fill
-            const int kg = cur.it.col_begin + cur.j;
-            const int kb = p.mirror ? p.kd - 1 - kg : kg;
-            const int brow = kb * p.n_total + cur.it.nt * BN;
-            for (int c = 0; c < nchunks; ++c, ++step) {
-                const int stage = (int)(step % stages);
-                mbar_wait(&empty[stage], (uint32_t)(((step / stages) & 1) ^ 1));
-                const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
-                if (lane == 0) {
-                    mbar_expect_tx(&full[stage], stage_bytes);
-                    tma_tile2d(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+                    for (int u = 0; u < 32; ++u) rows[u] = (int)(cur.it.row0 + pw * 32 + u);
                 }
-                __syncwarp();
-                tma_gather4(sa + (uint32_t)lane * 4 * KC * 2, &tm_a, c * KC, r[0], r[1], r[2], r[3],
-                            &full[stage]);
+#pragma unroll
+                for (int u = 0; u < 32; ++u) rows[u] = rows[u] < 0 ? p.n_rows_a : rows[u];  // OOB -> zeros
+                const int kg = cur.it.col_begin + cur.j;
+                const int kb = p.mirror ? p.kd - 1 - kg : kg;
+                const int brow = kb * p.n_total + cur.it.nt * BN;
+                for (int c = 0; c < nchunks; ++c, ++step) {
+                    const int stage = (int)(step % stages);
+                    mbar_wait(&empty[stage], (uint32_t)(((step / stages) & 1) ^ 1));
+                    const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
+                    if (pw == 0) {
+                        mbar_expect_tx(&full[stage], stage_bytes);
+                        tma_tile2d(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+                    }
+                    const uint32_t dst = sa + (uint32_t)pw * 32 * KC * 2;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        tma_gather4(dst + (uint32_t)u * 4 * KC * 2, &tm_a, c * KC, rows[4 * u],
+                                    rows[4 * u + 1], rows[4 * u + 2], rows[4 * u + 3],
+                                    &full[stage]);
+                }
+                if (use_ring && !pf.done) issue_idx();
+                cur.advance(p);
+                ++cs;
             }
-            __syncwarp();
-            if (use_ring && !pf.done) issue_idx();
-            cur.advance(p);
-            ++cs;
         }
-    } else if (warp == 1) {
+        __syncwarp();
+    } else if (warp == kProducerWarps) {
         // ================= MMA issuer (one thread) =================
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
@@ -410,7 +425,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             __syncwarp();
         }
     } else {
-        // ================= epilogue (warps 2-5 -> TMEM lane quadrants 2,3,0,1) =================
+        // ================= epilogue (warps 5-8 -> TMEM lane quadrants 1,2,3,0) =================
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         int local = 0;
@@ -475,7 +490,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem, ncols);
+    if (warp == kProducerWarps) tmem_dealloc(tmem, ncols);
 }
 
 // ---------------------------------------------------------------------------
@@ -717,8 +732,8 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
     const size_t stage_bytes = (size_t)kTileM * KC * 2 + (size_t)bn * KC * 2;
     int stages = (int)std::min<size_t>(8, (196 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
-    const size_t smem = 1024 + stages * stage_bytes + kIdxRing * kTileM * 4 +
-                        (2 * stages + 4 + kIdxRing) * 8 + 16;
+    const size_t smem = 1024 + stages * stage_bytes + kProducerWarps * kIdxRing * 32 * 4 +
+                        (2 * stages + 4 + kProducerWarps * kIdxRing) * 8 + 16;
     CUtensorMap ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, 1);
     CUtensorMap tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
     SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
