@@ -333,23 +333,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             Cursor cur, pf;
             cur.init(p, n_items);
             pf.init(p, n_items);
-            long long cs_pf = 0;
+            int pf_slot = 0;
             auto issue_idx = [&]() {
-                const int slot = (int)(cs_pf % kIdxRing);
-                mbar_expect_tx(&myfull[slot], 128);
-                bulk_g2s(smem_u32(ring + slot * 32), idx_column(p, pf.it, pf.j) + pw * 32, 128,
-                         &myfull[slot]);
+                mbar_expect_tx(&myfull[pf_slot], 128);
+                bulk_g2s(smem_u32(ring + pf_slot * 32), idx_column(p, pf.it, pf.j) + pw * 32, 128,
+                         &myfull[pf_slot]);
                 pf.advance(p);
-                ++cs_pf;
+                pf_slot = pf_slot + 1 == kIdxRing ? 0 : pf_slot + 1;
             };
             if (use_ring)
                 for (int d = 0; d < kIdxAhead && !pf.done; ++d) issue_idx();
-            long long cs = 0, step = 0;
+            int slot = 0, stage = 0;
+            uint32_t slot_ph = 0, phase = 0;
             while (!cur.done) {
                 int rows[32];
                 if (use_ring) {
-                    const int slot = (int)(cs % kIdxRing);
-                    mbar_wait(&myfull[slot], (uint32_t)((cs / kIdxRing) & 1));
+                    mbar_wait(&myfull[slot], slot_ph);
                     const int4* src = reinterpret_cast<const int4*>(ring + slot * 32);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
@@ -366,10 +365,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 const int kg = cur.it.col_begin + cur.j;
                 const int kb = p.mirror ? p.kd - 1 - kg : kg;
                 const int brow = kb * p.n_total + cur.it.nt * BN;
-                for (int c = 0; c < nchunks; ++c, ++step) {
-                    const int stage = (int)(step % stages);
-                    mbar_wait(&empty[stage], (uint32_t)(((step / stages) & 1) ^ 1));
-                    const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
+                for (int c = 0; c < nchunks; ++c) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t sa = smem_u32(stage_base) + (uint32_t)stage * stage_bytes;
                     if (pw == 0) {
                         mbar_expect_tx(&full[stage], stage_bytes);
                         tma_tile2d(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
@@ -380,10 +378,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                         tma_gather4(dst + (uint32_t)u * 4 * KC * 2, &tm_a, c * KC, rows[4 * u],
                                     rows[4 * u + 1], rows[4 * u + 2], rows[4 * u + 3],
                                     &full[stage]);
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
                 if (use_ring && !pf.done) issue_idx();
                 cur.advance(p);
-                ++cs;
+                if (++slot == kIdxRing) {
+                    slot = 0;
+                    slot_ph ^= 1;
+                }
             }
         }
         __syncwarp();
@@ -391,7 +396,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // ================= MMA issuer (one thread) =================
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
-        long long step = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t base_u = smem_u32(stage_base);
+        const uint64_t desc0 = kmajor_desc<KC>(base_u);  // stage 0, A tile, kk = 0
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             Item it = decode(p, item);
@@ -400,25 +408,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             tc_fence_after();
             const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
             unsigned long long m0 = it.m0, m1 = it.m1;
-            bool first = true;
+            uint32_t accumulate = 0;
             for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
                  j = next_col(m0, m1, it.biw0, it.bw1)) {
-                for (int c = 0; c < nchunks; ++c, ++step) {
-                    const int stage = (int)(step % stages);
-                    mbar_wait(&full[stage], (uint32_t)((step / stages) & 1));
+                for (int c = 0; c < nchunks; ++c) {
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t sa = smem_u32(stage_base + (size_t)stage * stage_bytes);
-                        const uint32_t sb = sa + a_bytes;
+                        // descriptor start address advances in 16B units
+                        const uint64_t da = desc0 + ((uint64_t)stage * stage_bytes >> 4);
+                        const uint64_t db = da + (a_bytes >> 4);
 #pragma unroll
-                        for (int kk = 0; kk < KC / 16; ++kk)
-                            tc_mma_f16(d_tmem, kmajor_desc<KC>(sa + kk * 32),
-                                       kmajor_desc<KC>(sb + kk * 32), idesc,
-                                       (first && kk == 0) ? 0u : 1u);
+                        for (int kk = 0; kk < KC / 16; ++kk) {
+                            tc_mma_f16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2),
+                                       idesc, accumulate);
+                            accumulate = 1;
+                        }
                         tc_commit(&empty[stage]);
                     }
                     __syncwarp();
-                    first = false;
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
             if (lane == 0) tc_commit(&tfull[acc]);
