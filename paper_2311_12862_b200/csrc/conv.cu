@@ -36,6 +36,8 @@
 //              i+1's MMAs
 // fp32 -> k_gconv_simt: the 1e-5 parity path (FFMA, fp32 accumulate).
 #include <cuda.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "sk_internal.hpp"
 
@@ -43,10 +45,11 @@ namespace sk {
 
 namespace {
 
-constexpr int kThreadsTC = 288;  // 9 warps: 4 x TMA producer, MMA, 4 x epilogue
-constexpr int kProducerWarps = 4;
-constexpr int kIdxRing = 16;     // index ring slots per producer warp (32 rows x 4B)
-constexpr int kIdxAhead = 12;    // column steps prefetched ahead (< kIdxRing)
+constexpr int kProducerWarps = 4;  // warps 0-3: cp.async gathers (one tile row per thread)
+constexpr int kMmaWarp = 4;        // warp 4: TMEM owner + tcgen05.mma issuer
+constexpr int kIndexWarp = 9;      // warp 9: index/descriptor streamer
+constexpr int kThreadsTC = 320;    // + warps 5-8: epilogue
+constexpr int kIdxRing = 16;       // column steps in flight in the index ring
 
 struct ConvArgs {
     int mode;  // 0 = OS rows (implicit GEMM), 1 = WS pairs (FOD / GGS GEMM)
@@ -275,10 +278,29 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | (sbo << 32) | (1ull << 46) | (layout << 61);
 }
 
+// byte offset of 16B chunk q of row r inside a K-major swizzled tile whose
+// base is aligned to the swizzle repeat (Swizzle<B,4,3>: bits[4,4+B) ^= bits[7,7+B))
+template <int KC>
+__device__ __forceinline__ uint32_t swz(int r, int q) {
+    constexpr uint32_t RB = KC * 2;
+    constexpr uint32_t B = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
+    const uint32_t off = (uint32_t)r * RB + (uint32_t)q * 16;
+    return off ^ (((off >> 7) & B) << 4);
+}
+
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// per index-ring slot: {brow (first B row of this step, -1 = end of work), unused x3}
+struct alignas(16) StepDesc {
+    int brow, pad0, pad1, pad2;
+};
+
 template <typename T, int KC>
 __global__ void __launch_bounds__(kThreadsTC, 1)
-    k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-               const ConvArgs p, int stages) {
+    k_gconv_tc(const ConvArgs p, int stages) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int BN = p.bn;
@@ -286,14 +308,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t b_bytes = (uint32_t)BN * KC * 2;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* stage_base = smem;
-    int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(idx_ring + kProducerWarps * kIdxRing * 32);
+    int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);  // [R][128]
+    StepDesc* descs = reinterpret_cast<StepDesc*>(idx_ring + kIdxRing * kTileM);  // [R]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(descs + kIdxRing);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;
     uint64_t* tempty = tfull + 2;
-    uint64_t* ifull = tempty + 2;  // [kProducerWarps][kIdxRing]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ifull + kProducerWarps * kIdxRing);
+    uint64_t* ifull = tempty + 2;       // [R]
+    uint64_t* iempty = ifull + kIdxRing;  // [R]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iempty + kIdxRing);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -301,105 +325,121 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < stages; ++i) {
-            mbar_init(&full[i], 1);
+            mbar_init(&full[i], kTileM);  // one cp.async noinc arrival per producer thread
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
         }
-        for (int i = 0; i < kProducerWarps * kIdxRing; ++i) mbar_init(&ifull[i], 1);
+        for (int i = 0; i < kIdxRing; ++i) {
+            mbar_init(&ifull[i], 1);
+            mbar_init(&iempty[i], kTileM);
+        }
         fence_mbar_init();
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
     }
-    if (warp == kProducerWarps) tmem_alloc(tmem_slot, ncols);
+    if (warp == kMmaWarp) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int n_items = num_items(p);
     const int nchunks = (p.k_total + KC - 1) / KC;
-    const bool use_ring = !(p.mode == 1 && p.a_identity);
+    const T* __restrict__ A = static_cast<const T*>(p.a);
+    const T* __restrict__ Bw = static_cast<const T*>(p.b);
 
-    if (warp < kProducerWarps) {
-        // ===== producers: warp pw owns tile rows [32 pw, 32 pw + 32): 8 TMA gather4 per
-        // k-step issued by ONE thread (uniform operands, no per-lane ELECT loop);
-        // warp 0 also arms the stage barrier and loads the B tile =====
-        if (lane == 0) {
-            const int pw = warp;
-            int* ring = idx_ring + pw * kIdxRing * 32;
-            uint64_t* myfull = ifull + pw * kIdxRing;
-            Cursor cur, pf;
-            cur.init(p, n_items);
-            pf.init(p, n_items);
-            int pf_slot = 0;
-            auto issue_idx = [&]() {
-                mbar_expect_tx(&myfull[pf_slot], 128);
-                bulk_g2s(smem_u32(ring + pf_slot * 32), idx_column(p, pf.it, pf.j) + pw * 32, 128,
-                         &myfull[pf_slot]);
-                pf.advance(p);
-                pf_slot = pf_slot + 1 == kIdxRing ? 0 : pf_slot + 1;
-            };
-            if (use_ring)
-                for (int d = 0; d < kIdxAhead && !pf.done; ++d) issue_idx();
-            int slot = 0, stage = 0;
-            uint32_t slot_ph = 0, phase = 0;
-            while (!cur.done) {
-                int rows[32];
-                if (use_ring) {
-                    mbar_wait(&myfull[slot], slot_ph);
-                    const int4* src = reinterpret_cast<const int4*>(ring + slot * 32);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        int4 v = src[u];
-                        rows[4 * u] = v.x; rows[4 * u + 1] = v.y;
-                        rows[4 * u + 2] = v.z; rows[4 * u + 3] = v.w;
-                    }
+    if (warp == kIndexWarp) {
+        // ===== index warp: walks the column steps, streams each step's 128 A-row
+        // indices (512B cp.async.bulk) + its B row base into the smem ring =====
+        Cursor cur;
+        cur.init(p, n_items);
+        const bool ident = p.mode == 1 && p.a_identity;
+        int slot = 0;
+        uint32_t ph = 0;
+        for (;;) {
+            mbar_wait(&iempty[slot], ph ^ 1);
+            if (cur.done) {
+                if (lane == 0) {
+                    descs[slot].brow = -1;
+                    mbar_arrive(&ifull[slot]);
+                }
+                break;
+            }
+            const int kg = cur.it.col_begin + cur.j;
+            const int kb = p.mirror ? p.kd - 1 - kg : kg;
+            if (ident) {
+                for (int u = lane; u < kTileM; u += 32) idx_ring[slot * kTileM + u] = (int)(cur.it.row0 + u);
+                __syncwarp();
+            }
+            if (lane == 0) {
+                descs[slot].brow = kb * p.n_total + cur.it.nt * BN;
+                if (ident) {
+                    mbar_arrive(&ifull[slot]);
                 } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) rows[u] = (int)(cur.it.row0 + pw * 32 + u);
-                }
-#pragma unroll
-                for (int u = 0; u < 32; ++u) rows[u] = rows[u] < 0 ? p.n_rows_a : rows[u];  // OOB -> zeros
-                const int kg = cur.it.col_begin + cur.j;
-                const int kb = p.mirror ? p.kd - 1 - kg : kg;
-                const int brow = kb * p.n_total + cur.it.nt * BN;
-                for (int c = 0; c < nchunks; ++c) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    const uint32_t sa = smem_u32(stage_base) + (uint32_t)stage * stage_bytes;
-                    if (pw == 0) {
-                        mbar_expect_tx(&full[stage], stage_bytes);
-                        tma_tile2d(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
-                    }
-                    const uint32_t dst = sa + (uint32_t)pw * 32 * KC * 2;
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        tma_gather4(dst + (uint32_t)u * 4 * KC * 2, &tm_a, c * KC, rows[4 * u],
-                                    rows[4 * u + 1], rows[4 * u + 2], rows[4 * u + 3],
-                                    &full[stage]);
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-                if (use_ring && !pf.done) issue_idx();
-                cur.advance(p);
-                if (++slot == kIdxRing) {
-                    slot = 0;
-                    slot_ph ^= 1;
+                    mbar_expect_tx(&ifull[slot], kTileM * 4);
+                    bulk_g2s(smem_u32(idx_ring + slot * kTileM), idx_column(p, cur.it, cur.j),
+                             kTileM * 4, &ifull[slot]);
                 }
             }
+            __syncwarp();
+            cur.advance(p);
+            if (++slot == kIdxRing) {
+                slot = 0;
+                ph ^= 1;
+            }
         }
-        __syncwarp();
-    } else if (warp == kProducerWarps) {
+    } else if (warp < kProducerWarps) {
+        // ===== producers: thread r gathers tile row r (KC/8 x 16B cp.async, zero-fill
+        // for sentinels / channel tails) and a share of the B tile; completion
+        // arrives on the stage barrier asynchronously (cp.async.mbarrier.arrive.noinc) =====
+        const int r = threadIdx.x;
+        int slot = 0, stage = 0;
+        uint32_t ph = 0, phase = 0;
+        const uint32_t base_u = smem_u32(stage_base);
+        for (;;) {
+            mbar_wait(&ifull[slot], ph);
+            const int brow = descs[slot].brow;
+            if (brow < 0) break;
+            const int ai = idx_ring[slot * kTileM + r];
+            mbar_arrive(&iempty[slot]);
+            const T* arow = A + (size_t)(ai < 0 ? 0 : ai) * p.k_total;
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t sa = base_u + (uint32_t)stage * stage_bytes;
+                const uint32_t sb = sa + a_bytes;
+#pragma unroll
+                for (int q = 0; q < KC / 8; ++q) {
+                    const int col = c * KC + q * 8;
+                    const bool ok = ai >= 0 && col < p.k_total;
+                    cp_async16(sa + swz<KC>(r, q), ok ? (const void*)(arow + col) : (const void*)A,
+                               ok ? 16u : 0u);
+                }
+                for (int i = r; i < BN * (KC / 8); i += kTileM) {
+                    const int n = i / (KC / 8), q = i % (KC / 8);
+                    const int col = c * KC + q * 8;
+                    const bool ok = (brow + n) < p.kd * p.n_total && col < p.k_total;
+                    const T* src = Bw + (size_t)(brow + n) * p.k_total + col;
+                    cp_async16(sb + swz<KC>(n, q), ok ? (const void*)src : (const void*)Bw,
+                               ok ? 16u : 0u);
+                }
+                cp_async_arrive_noinc(&full[stage]);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (++slot == kIdxRing) {
+                slot = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == kMmaWarp) {
         // ================= MMA issuer (one thread) =================
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
         int stage = 0;
         uint32_t phase = 0;
-        const uint32_t base_u = smem_u32(stage_base);
-        const uint64_t desc0 = kmajor_desc<KC>(base_u);  // stage 0, A tile, kk = 0
+        const uint64_t desc0 = kmajor_desc<KC>(smem_u32(stage_base));
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             Item it = decode(p, item);
@@ -502,7 +542,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == kProducerWarps) tmem_dealloc(tmem, ncols);
+    if (warp == kMmaWarp) tmem_dealloc(tmem, ncols);
 }
 
 // ---------------------------------------------------------------------------
@@ -739,18 +779,16 @@ CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, i
 }
 
 template <typename T, int KC>
-void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
+void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
     const int bn = a.bn;
     const size_t stage_bytes = (size_t)kTileM * KC * 2 + (size_t)bn * KC * 2;
-    int stages = (int)std::min<size_t>(8, (196 * 1024) / stage_bytes);
+    int stages = (int)std::min<size_t>(10, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
-    const size_t smem = 1024 + stages * stage_bytes + kProducerWarps * kIdxRing * 32 * 4 +
-                        (2 * stages + 4 + kProducerWarps * kIdxRing) * 8 + 16;
-    CUtensorMap ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, 1);
-    CUtensorMap tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
+    const size_t smem = 1024 + stages * stage_bytes + kIdxRing * (kTileM * 4 + 16) +
+                        (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
     SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(ta, tb, a, stages);
+    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages);
     SK_LAUNCH_CHECK();
 }
 
@@ -778,7 +816,8 @@ void pick_n_tiling(int n_total, int cta_n, bool tc, int& bn, int& n_nt) {
     bn = (int)ceil_div(ceil_div(n_total, n_nt), 16) * 16;
 }
 
-void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a, cudaStream_t st) {
+void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t st) {
+    const ConvArgs& a = a_in;
     const bool tc = tc_ok(dt, a.k_total, a.n_total);
     int grid;
     if (a.mode == 0) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
