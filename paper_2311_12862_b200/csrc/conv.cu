@@ -301,8 +301,9 @@ struct alignas(16) StepDesc {
 template <typename T, int KC>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     k_gconv_tc(const ConvArgs p, int stages) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // dynamic smem starts 1024B-aligned (no static smem); checked below since
+    // the swizzle atoms and UMMA descriptors rely on it
+    extern __shared__ __align__(1024) uint8_t smem[];
     const int BN = p.bn;
     const uint32_t a_bytes = kTileM * KC * 2;
     const uint32_t b_bytes = (uint32_t)BN * KC * 2;
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     while (ncols < (uint32_t)(2 * BN)) ncols <<= 1;
 
     if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023) __trap();
         for (int i = 0; i < stages; ++i) {
             mbar_init(&full[i], kTileM);  // one cp.async noinc arrival per producer thread
             mbar_init(&empty[i], 1);
@@ -389,38 +391,43 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
         }
     } else if (warp < kProducerWarps) {
-        // ===== producers: thread r gathers tile row r (KC/8 x 16B cp.async, zero-fill
-        // for sentinels / channel tails) and a share of the B tile; completion
-        // arrives on the stage barrier asynchronously (cp.async.mbarrier.arrive.noinc) =====
-        const int r = threadIdx.x;
+        // ===== producers: CH = KC/8 consecutive threads cover one row's KC
+        // channels (16B cp.async each, zero-fill for sentinels / channel tails),
+        // so a warp instruction touches 32/CH whole rows (coalesced lines); the
+        // same mapping loads the B tile. Completion arrives on the stage barrier
+        // asynchronously (cp.async.mbarrier.arrive.noinc). =====
+        constexpr int CH = KC / 8;           // 16B chunks per row
+        constexpr int RSTRIDE = kTileM / CH; // rows between a thread's rows
+        const int t = threadIdx.x;
+        const int q = t % CH, r0 = t / CH;
         int slot = 0, stage = 0;
         uint32_t ph = 0, phase = 0;
         const uint32_t base_u = smem_u32(stage_base);
+        const long long b_rows = (long long)p.kd * p.n_total;
         for (;;) {
             mbar_wait(&ifull[slot], ph);
             const int brow = descs[slot].brow;
             if (brow < 0) break;
-            const int ai = idx_ring[slot * kTileM + r];
+            int ai[CH];
+#pragma unroll
+            for (int i = 0; i < CH; ++i) ai[i] = idx_ring[slot * kTileM + r0 + i * RSTRIDE];
             mbar_arrive(&iempty[slot]);
-            const T* arow = A + (size_t)(ai < 0 ? 0 : ai) * p.k_total;
             for (int c = 0; c < nchunks; ++c) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 const uint32_t sa = base_u + (uint32_t)stage * stage_bytes;
                 const uint32_t sb = sa + a_bytes;
+                const int col = c * KC + q * 8;
+                const bool col_ok = col < p.k_total;
 #pragma unroll
-                for (int q = 0; q < KC / 8; ++q) {
-                    const int col = c * KC + q * 8;
-                    const bool ok = ai >= 0 && col < p.k_total;
-                    cp_async16(sa + swz<KC>(r, q), ok ? (const void*)(arow + col) : (const void*)A,
-                               ok ? 16u : 0u);
+                for (int i = 0; i < CH; ++i) {
+                    const bool ok = ai[i] >= 0 && col_ok;
+                    const T* src = A + (size_t)(ok ? ai[i] : 0) * p.k_total + (ok ? col : 0);
+                    cp_async16(sa + swz<KC>(r0 + i * RSTRIDE, q), src, ok ? 16u : 0u);
                 }
-                for (int i = r; i < BN * (KC / 8); i += kTileM) {
-                    const int n = i / (KC / 8), q = i % (KC / 8);
-                    const int col = c * KC + q * 8;
-                    const bool ok = (brow + n) < p.kd * p.n_total && col < p.k_total;
-                    const T* src = Bw + (size_t)(brow + n) * p.k_total + col;
-                    cp_async16(sb + swz<KC>(n, q), ok ? (const void*)src : (const void*)Bw,
-                               ok ? 16u : 0u);
+                for (int n = r0; n < BN; n += RSTRIDE) {
+                    const bool ok = (brow + n) < b_rows && col_ok;
+                    const T* src = Bw + (ok ? (size_t)(brow + n) * p.k_total + col : 0);
+                    cp_async16(sb + swz<KC>(n, q), src, ok ? 16u : 0u);
                 }
                 cp_async_arrive_noinc(&full[stage]);
                 if (++stage == stages) {
@@ -784,7 +791,7 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
     const size_t stage_bytes = (size_t)kTileM * KC * 2 + (size_t)bn * KC * 2;
     int stages = (int)std::min<size_t>(10, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
-    const size_t smem = 1024 + stages * stage_bytes + kIdxRing * (kTileM * 4 + 16) +
+    const size_t smem = stages * stage_bytes + kIdxRing * (kTileM * 4 + 16) +
                         (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
     SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
