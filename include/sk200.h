@@ -86,6 +86,8 @@ typedef struct {
 /* ---- errors / context ---------------------------------------------------- */
 const char* sk_last_error(void);
 const char* sk_version(void);
+/* number of device kernels this library has launched (diagnostic) */
+uint64_t sk_kernel_launches(void);
 /* One context per device; owns the stream-ordered memory pool and the
  * kernel-map cache (MapCache, kmap.hpp:159-176). */
 sk_status sk_ctx_create(int device, sk_ctx** out);
@@ -179,6 +181,57 @@ sk_status sk_conv_wgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, s
 sk_status sk_kmap_count_macs(sk_kmap* map, int splits, int pad_multiple, int warp_rows,
                              int c_in, int c_out, int64_t* effective, int64_t* redundant,
                              void* stream);
+
+/* ---- NetworkRunner (network.hpp:81-119) + autotuner (tuner.hpp) ----------
+ * Spec text: one layer per line "name kind c_in c_out kernel stride inputs
+ * transpose_of" (kind conv|conv_transposed, inputs comma list or "-",
+ * transpose_of name or "-"), the LayerSpec fields of network.hpp:20-33.
+ * Weights live on the device in `dtype`, [K^D][c_in][c_out] per layer. */
+typedef struct sk_net sk_net;
+sk_status sk_net_create(sk_ctx* ctx, int dims, const char* spec_text, sk_dtype dtype,
+                        sk_net** out);
+sk_status sk_net_destroy(sk_net* net);
+int sk_net_num_layers(const sk_net* net);
+/* partition_groups (network.cpp:141-158): map-sharing groups */
+int sk_net_num_groups(const sk_net* net);
+int sk_net_group_of_layer(const sk_net* net, int layer);
+sk_status sk_net_layer_info(const sk_net* net, int layer, int* num_offsets, int* c_in,
+                            int* c_out, int64_t* wgrad_offset);
+int64_t sk_net_num_params(const sk_net* net);
+/* device weight buffer of a layer (write it with cudaMemcpy / kernels) */
+sk_status sk_net_weight_ptr(sk_net* net, int layer, void** ptr);
+/* GroupConfig (network.hpp:54-58): phase 0 forward, 1 dgrad, 2 wgrad */
+sk_status sk_net_set_config(sk_net* net, int group, int phase, const sk_dataflow_cfg* cfg);
+sk_status sk_net_get_config(const sk_net* net, int group, int phase, sk_dataflow_cfg* cfg);
+/* NetworkRunner::forward (network.cpp:392): maps are built once per input
+ * coordinate set and group, then cached. d_out is library-owned (valid until
+ * the next forward). mapping_ms / kernel_ms: per-group CUDA-event timing
+ * (RunStats), NULL to skip (no sync). */
+sk_status sk_net_forward(sk_net* net, sk_coords* in, const void* d_feats, int channels,
+                         void* stream, const void** d_out, int* n_out, double* mapping_ms,
+                         double* kernel_ms);
+sk_status sk_net_layer_output(sk_net* net, int layer, const void** d_out, int* rows);
+/* NetworkRunner::measure_ms (network.cpp:398-438) */
+sk_status sk_net_measure(sk_net* net, sk_coords* in, const void* d_feats, int channels,
+                         int forward, int dgrad, int wgrad, void* stream, double* ms);
+int64_t sk_net_map_builds(const sk_net* net);
+/* modeled_group_traffic (network.cpp:453-471) */
+sk_status sk_net_group_traffic(sk_net* net, int group, const sk_dataflow_cfg* cfg, void* stream,
+                               double* bytes);
+/* Chained backward of the last forward over layers [layer_lo, layer_hi]
+ * (call with decreasing ranges to overlap gradient all-reduce buckets). */
+sk_status sk_net_backward(sk_net* net, const void* d_grad_out, float* d_wgrad_flat, int layer_hi,
+                          int layer_lo, void* stream);
+/* tune_inference / tune_training (tuner.cpp:134-220): training 0 =
+ * inference, 1 = workload_pattern, 2 = sparse_mapping. Log entries are
+ * {pass, group, space index, ms}. Leaves the winning configs set. */
+sk_status sk_net_tune(sk_net* net, sk_coords* in, const void* d_feats, int channels,
+                      int training, int warmup, int runs, void* stream, double* latency_ms,
+                      double* log, int log_cap, int* log_len);
+/* default_space (tuner.cpp:9-26): GGS, FOD, implicit GEMM x splits 0..4 x
+ * {small, large} */
+int sk_tune_space_size(void);
+sk_status sk_tune_space_entry(int i, sk_dataflow_cfg* cfg);
 
 #ifdef __cplusplus
 }

@@ -307,7 +307,7 @@ class Reference:
         L.ref_quantize.argtypes = [C.c_int, C.c_int, _f64p, C.c_int, C.c_void_p, _f64p, C.c_int,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
         L.ref_net_create.argtypes = [C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_uint64,
-                                     C.POINTER(C.c_void_p)]
+                                     C.c_void_p, C.POINTER(C.c_void_p)]
         L.ref_net_free.argtypes = [C.c_void_p]
         L.ref_net_free.restype = None
         L.ref_net_num_groups.argtypes = [C.c_void_p]
@@ -415,11 +415,20 @@ class Reference:
                                           C.byref(cnt)))
         return coords, of
 
-    def network(self, dims, spec_text, prec=0, threads=0, weight_seed=3):
+    def network(self, dims, spec_text, prec=0, threads=0, weight_seed=3, weights=None):
+        """NetworkRunner over `spec_text`; weights = list of [K^D, c_in, c_out]
+        arrays (layer order) or None for seeded timing weights."""
         p = C.c_void_p()
+        flat = None
+        if weights is not None:
+            flat = np.ascontiguousarray(np.concatenate([np.asarray(w, np.float64).ravel()
+                                                        for w in weights]))
         self._check(self.lib.ref_net_create(dims, spec_text.encode(), prec, threads, weight_seed,
+                                            None if flat is None else flat.ctypes.data,
                                             C.byref(p)))
-        return RefNet(self, p)
+        net = RefNet(self, p)
+        net._weights_keep = flat
+        return net
 
 
 class RefNet:

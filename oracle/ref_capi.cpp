@@ -342,7 +342,7 @@ int ref_quantize(int dims, int m, const double* raw, int channels, const double*
 // Spec text: one layer per line, "name kind c_in c_out kernel stride inputs
 // transpose_of" with inputs a comma list or "-", transpose_of a name or "-".
 int ref_net_create(int dims, const char* spec_text, int prec, int threads,
-                   uint64_t weight_seed, RefNet** out) {
+                   uint64_t weight_seed, const double* weights, RefNet** out) {
     return guard([&] {
         auto net = std::make_unique<RefNet>();
         net->spec.dims = dims;
@@ -365,14 +365,22 @@ int ref_net_create(int dims, const char* spec_text, int prec, int threads,
         }
         net->spec.validate();
         // timing weights N(0, 1/sqrt(K^D c_in)), mt19937_64(seed)
+        // weights: caller-provided (flat, layer order) or timing weights
+        // N(0, 1/sqrt(K^D c_in)) from mt19937_64(seed)
         std::mt19937_64 rng(weight_seed);
         std::vector<WeightTensor> ws;
+        size_t off = 0;
         for (const LayerSpec& l : net->spec.layers) {
             int kd = 1;
             for (int d = 0; d < dims; ++d) kd *= l.kernel;
-            std::normal_distribution<double> g(0.0, 1.0 / std::sqrt(double(kd) * l.c_in));
             std::vector<double> v(size_t(kd) * l.c_in * l.c_out);
-            for (double& x : v) x = g(rng);
+            if (weights) {
+                std::copy(weights + off, weights + off + v.size(), v.begin());
+            } else {
+                std::normal_distribution<double> g(0.0, 1.0 / std::sqrt(double(kd) * l.c_in));
+                for (double& x : v) x = g(rng);
+            }
+            off += v.size();
             ws.emplace_back(kd, l.c_in, l.c_out, std::move(v), prec_of(prec));
         }
         ExecContext ctx;

@@ -16,13 +16,18 @@ LIB_PATH = os.path.join(PKG, "libsk200.so")
 # exported symbols, in header order (include/sk200.h); tests check the .so
 # exports exactly these
 SYMBOLS = [
-    "sk_last_error", "sk_version", "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_deterministic",
+    "sk_last_error", "sk_version", "sk_kernel_launches", "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_deterministic",
     "sk_coords_create", "sk_coords_create_host", "sk_coords_retain", "sk_coords_release",
     "sk_coords_n", "sk_coords_dims", "sk_coords_id", "sk_coords_device_ptr",
     "sk_coords_stride_tag", "sk_coords_export", "sk_out_coords", "sk_kmap_build",
     "sk_kmap_transpose", "sk_kmap_prepare", "sk_kmap_retain", "sk_kmap_release",
     "sk_kmap_get_info", "sk_kmap_export_os", "sk_kmap_export_ws", "sk_kmap_export_split",
     "sk_conv_forward", "sk_conv_dgrad", "sk_conv_wgrad", "sk_kmap_count_macs",
+    "sk_net_create", "sk_net_destroy", "sk_net_num_layers", "sk_net_num_groups",
+    "sk_net_group_of_layer", "sk_net_layer_info", "sk_net_num_params", "sk_net_weight_ptr",
+    "sk_net_set_config", "sk_net_get_config", "sk_net_forward", "sk_net_layer_output",
+    "sk_net_measure", "sk_net_map_builds", "sk_net_group_traffic", "sk_net_backward",
+    "sk_net_tune", "sk_tune_space_size", "sk_tune_space_entry",
 ]
 
 SK_F32, SK_F16, SK_BF16 = 0, 1, 2
@@ -73,6 +78,7 @@ def lib():
     sig = {
         "sk_last_error": ([], C.c_char_p),
         "sk_version": ([], C.c_char_p),
+        "sk_kernel_launches": ([], C.c_uint64),
         "sk_ctx_create": ([C.c_int, pp], C.c_int),
         "sk_ctx_destroy": ([vp], C.c_int),
         "sk_ctx_set_deterministic": ([vp, C.c_int], C.c_int),
@@ -105,6 +111,29 @@ def lib():
                            vp, vp], C.c_int),
         "sk_kmap_count_macs": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64p, i64p, vp],
                                C.c_int),
+        "sk_net_create": ([vp, C.c_int, C.c_char_p, C.c_int, pp], C.c_int),
+        "sk_net_destroy": ([vp], C.c_int),
+        "sk_net_num_layers": ([vp], C.c_int),
+        "sk_net_num_groups": ([vp], C.c_int),
+        "sk_net_group_of_layer": ([vp, C.c_int], C.c_int),
+        "sk_net_layer_info": ([vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                               C.POINTER(C.c_int), i64p], C.c_int),
+        "sk_net_num_params": ([vp], C.c_int64),
+        "sk_net_weight_ptr": ([vp, C.c_int, pp], C.c_int),
+        "sk_net_set_config": ([vp, C.c_int, C.c_int, C.POINTER(DataflowCfg)], C.c_int),
+        "sk_net_get_config": ([vp, C.c_int, C.c_int, C.POINTER(DataflowCfg)], C.c_int),
+        "sk_net_forward": ([vp, vp, vp, C.c_int, vp, pp, C.POINTER(C.c_int), vp, vp], C.c_int),
+        "sk_net_layer_output": ([vp, C.c_int, pp, C.POINTER(C.c_int)], C.c_int),
+        "sk_net_measure": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                            C.POINTER(C.c_double)], C.c_int),
+        "sk_net_map_builds": ([vp], C.c_int64),
+        "sk_net_group_traffic": ([vp, C.c_int, C.POINTER(DataflowCfg), vp,
+                                  C.POINTER(C.c_double)], C.c_int),
+        "sk_net_backward": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
+        "sk_net_tune": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                         C.POINTER(C.c_double), vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
+        "sk_tune_space_size": ([], C.c_int),
+        "sk_tune_space_entry": ([C.c_int, C.POINTER(DataflowCfg)], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -26,6 +26,18 @@ sk_status guard(F&& f) {
 
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+}  // namespace
+
+namespace sk {
+void set_last_error(const std::string& m) { g_last_error = m; }
+std::atomic<unsigned long long>& launch_counter() {
+    static std::atomic<unsigned long long> c{0};
+    return c;
+}
+}  // namespace sk
+
+namespace {
+
 void release_coords(sk_coords* c);
 void release_kmap(sk_kmap* m);
 
@@ -93,6 +105,7 @@ extern "C" {
 
 const char* sk_last_error(void) { return g_last_error.c_str(); }
 const char* sk_version(void) { return "sk200 0.1 (sm_100a)"; }
+uint64_t sk_kernel_launches(void) { return sk::launch_counter().load(); }
 
 sk_status sk_ctx_create(int device, sk_ctx** out) {
     return guard([&] {

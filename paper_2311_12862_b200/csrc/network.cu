@@ -1,0 +1,791 @@
+// sk200 NetworkRunner + group autotuner,
+// native C++ over the device kmaps / dataflows.
+//
+//  * NetSpec / validate / propagate_syms / partition_groups restate
+//    network.cpp:30-158 (same validation rules, same structural symbols, same
+//    groups keyed by (in_sym, out_sym, K, stride); decoder layers join their
+//    encoder's group).
+//  * sk_net::forward restates run_forward (network.cpp:282-345): per layer,
+//    resolve producers (<= 2, summed), take the group's maps (built once per
+//    input coordinate set through the sk_coords map cache = GroupMaps cache,
+//    network.cpp:183-275), run the group's forward config. Mapping and kernel
+//    time are split per group with CUDA events (RunStats, network.hpp:62-70).
+//  * measure (network.cpp:398-438): forward, then dgrad / wgrad sweeps with
+//    all-ones dummy gradients, timed per phase (the tuner's probe).
+//  * backward: a real chained backward (dgrad output of layer i feeds its
+//    producers, skip fan-out summed), weight gradients in one flat fp32
+//    buffer — the data-parallel training step's per-GPU half.
+//  * tune: greedy_pass / tune_inference / tune_training (tuner.cpp:86-220)
+//    with a CUDA-event RunnerProbe (warmup 2, median of 5, tuner.cpp:50-60);
+//    ties break on the traffic model (cost.cpp:47-93) then space order.
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <sstream>
+#include <unordered_map>
+
+#include "sk_internal.hpp"
+
+namespace sk {
+
+struct LayerSpec {
+    std::string name;
+    int kind = 0;  // 0 conv, 1 conv_transposed (LayerKind, network.hpp:15)
+    int c_in = 1, c_out = 1, kernel = 3, stride = 1;
+    std::vector<std::string> inputs;
+    std::string transpose_of;
+};
+
+struct NetSpec {
+    int dims = 3;
+    std::vector<LayerSpec> layers;
+    int index(const std::string& n) const {
+        for (size_t i = 0; i < layers.size(); ++i)
+            if (layers[i].name == n) return (int)i;
+        return -1;
+    }
+    // NetworkSpec::validate (network.cpp:30-76)
+    void validate() const {
+        sk::validate(dims == 2 || dims == 3, "network dims must be 2 or 3");
+        sk::validate(!layers.empty(), "network has no layers");
+        std::map<std::string, int> seen;
+        for (size_t i = 0; i < layers.size(); ++i) {
+            const LayerSpec& l = layers[i];
+            sk::validate(!l.name.empty(), "layer " + std::to_string(i) + " has no name");
+            sk::validate(seen.emplace(l.name, (int)i).second, "duplicate layer name: " + l.name);
+            sk::validate(l.c_in > 0 && l.c_out > 0, l.name + ": channel counts must be positive");
+            sk::validate(l.kernel > 0 && l.kernel % 2 == 1,
+                         l.name + ": kernel size must be odd and positive");
+            sk::validate(l.stride > 0, l.name + ": stride must be positive");
+            sk::validate(l.inputs.size() <= 2, l.name + ": at most two producers supported");
+            for (const std::string& p : l.inputs) {
+                int j = index(p);
+                sk::validate(j >= 0 && j < (int)i,
+                             l.name + ": producer '" + p + "' must be an earlier layer");
+                sk::validate(layers[j].c_out == l.c_in,
+                             l.name + ": c_in does not match producer '" + p + "' c_out");
+            }
+            if (l.kind == 1) {
+                int j = index(l.transpose_of);
+                sk::validate(j >= 0 && j < (int)i,
+                             l.name + ": transpose_of must name an earlier layer");
+                sk::validate(layers[j].kind == 0, l.name + ": transpose_of must be a conv layer");
+                sk::validate(layers[j].kernel == l.kernel && layers[j].stride == l.stride,
+                             l.name + ": kernel/stride must match '" + l.transpose_of + "'");
+            } else {
+                sk::validate(l.transpose_of.empty(),
+                             l.name + ": transpose_of is only valid on conv_transposed");
+            }
+        }
+    }
+};
+
+NetSpec parse_spec(int dims, const char* text) {
+    NetSpec s;
+    s.dims = dims;
+    std::istringstream is(text ? text : "");
+    std::string line;
+    while (std::getline(is, line)) {
+        if (line.empty() || line[0] == '#') continue;
+        std::istringstream ls(line);
+        LayerSpec l;
+        std::string kind, inputs, tof;
+        if (!(ls >> l.name >> kind >> l.c_in >> l.c_out >> l.kernel >> l.stride >> inputs >> tof))
+            fail(SK_ERR_VALIDATION, "malformed layer line: " + line);
+        if (kind == "conv") l.kind = 0;
+        else if (kind == "conv_transposed") l.kind = 1;
+        else fail(SK_ERR_VALIDATION, "unknown layer kind: " + kind);
+        if (inputs != "-") {
+            std::stringstream ss(inputs);
+            std::string tok;
+            while (std::getline(ss, tok, ',')) l.inputs.push_back(tok);
+        }
+        if (tof != "-") l.transpose_of = tof;
+        s.layers.push_back(l);
+    }
+    s.validate();
+    return s;
+}
+
+struct StructKey {
+    int in_sym, out_sym, kernel, stride;
+    bool operator==(const StructKey& o) const {
+        return in_sym == o.in_sym && out_sym == o.out_sym && kernel == o.kernel &&
+               stride == o.stride;
+    }
+};
+
+// propagate_syms + partition_groups (network.cpp:98-158)
+std::vector<std::vector<int>> partition_groups(const NetSpec& net) {
+    const size_t L = net.layers.size();
+    std::vector<std::pair<int, int>> syms(L);
+    std::vector<StructKey> keys(L);
+    int next_sym = 1;
+    std::map<long long, int> derived;
+    for (size_t i = 0; i < L; ++i) {
+        const LayerSpec& l = net.layers[i];
+        int in_sym = 0;
+        if (!l.inputs.empty()) {
+            in_sym = syms[net.index(l.inputs[0])].second;
+            if (l.inputs.size() == 2)
+                validate(syms[net.index(l.inputs[1])].second == in_sym,
+                         l.name + ": skip producers live on different coordinate sets");
+        }
+        int out_sym;
+        if (l.kind == 1) {
+            int j = net.index(l.transpose_of);
+            validate(syms[j].second == in_sym, l.name +
+                                                   ": input coordinates do not match the output of '" +
+                                                   l.transpose_of + "'");
+            out_sym = syms[j].first;
+            keys[i] = keys[j];
+        } else if (l.stride == 1) {
+            out_sym = in_sym;
+            keys[i] = {in_sym, out_sym, l.kernel, 1};
+        } else {
+            long long dk = (long long)in_sym * 64 + l.stride;
+            auto it = derived.find(dk);
+            if (it == derived.end()) it = derived.emplace(dk, next_sym++).first;
+            out_sym = it->second;
+            keys[i] = {in_sym, out_sym, l.kernel, l.stride};
+        }
+        syms[i] = {in_sym, out_sym};
+    }
+    std::vector<std::vector<int>> groups;
+    std::vector<int> head;
+    for (size_t i = 0; i < L; ++i) {
+        int gid = -1;
+        for (size_t g = 0; g < groups.size(); ++g)
+            if (keys[head[g]] == keys[i]) {
+                gid = (int)g;
+                break;
+            }
+        if (gid < 0) {
+            groups.emplace_back();
+            head.push_back((int)i);
+            gid = (int)groups.size() - 1;
+        }
+        groups[gid].push_back((int)i);
+    }
+    return groups;
+}
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p, long long i);
+template <>
+__device__ __forceinline__ float ld_f<__half>(const __half* p, long long i) { return __half2float(p[i]); }
+template <>
+__device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p, long long i) { return __bfloat162float(p[i]); }
+template <>
+__device__ __forceinline__ float ld_f<float>(const float* p, long long i) { return p[i]; }
+template <typename T>
+__device__ __forceinline__ T cvt_f(float v);
+template <>
+__device__ __forceinline__ __half cvt_f<__half>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ float cvt_f<float>(float v) { return v; }
+
+// skip connection: y = a + b (network.cpp:174-181 sums producers)
+template <typename T>
+__global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, long long n,
+                      T* __restrict__ y) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = cvt_f<T>(ld_f(a, i) + ld_f(b, i));
+}
+template <typename T>
+__global__ void k_fill(T* __restrict__ y, long long n, float v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = cvt_f<T>(v);
+}
+// gradient accumulation: g (fp32) += dx
+template <typename T>
+__global__ void k_accum(float* __restrict__ g, const T* __restrict__ dx, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        g[i] += ld_f(dx, i);
+}
+template <typename T>
+__global__ void k_cast_from_f32(const float* __restrict__ g, long long n, T* __restrict__ y) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = cvt_f<T>(g[i]);
+}
+
+int grid_for(long long n) { return (int)std::min<long long>(std::max<long long>(1, ceil_div(n, 256)), 148 * 16); }
+
+template <class F>
+void by_dtype(sk_dtype dt, F&& f) {
+    if (dt == SK_F16) f(__half{});
+    else if (dt == SK_BF16) f(__nv_bfloat16{});
+    else f(float{});
+}
+
+}  // namespace
+
+}  // namespace sk
+
+using namespace sk;
+
+struct sk_net {
+    sk_ctx* ctx = nullptr;
+    NetSpec spec;
+    sk_dtype dt = SK_F16;
+    std::vector<std::vector<int>> groups;
+    std::vector<int> group_of;
+    std::vector<int> kd;
+    std::vector<DevBuf> w;
+    std::vector<sk_dataflow_cfg> cfg[3];  // per group: forward, dgrad, wgrad
+    // state of the last forward
+    uint64_t root_id = 0;
+    std::vector<sk_coords*> in_set, out_set;  // retained
+    std::vector<sk_kmap*> exec_map;           // retained, execution orientation
+    std::vector<DevBuf> out, xsum;
+    std::vector<const void*> x_ptr;
+    std::vector<size_t> wgrad_off;
+    size_t wgrad_total = 0;
+    std::vector<DevBuf> gout;  // fp32 output grads (backward)
+    int64_t map_builds = 0;
+
+    ~sk_net() { clear_state(); }
+    void clear_state() {
+        for (auto* c : in_set) if (c) sk_coords_release(c);
+        for (auto* c : out_set) if (c) sk_coords_release(c);
+        for (auto* m : exec_map) if (m) sk_kmap_release(m);
+        in_set.clear();
+        out_set.clear();
+        exec_map.clear();
+    }
+    size_t es() const { return dt == SK_F32 ? 4 : 2; }
+};
+
+namespace {
+
+sk_dataflow_cfg default_cfg() {
+    sk_dataflow_cfg c;
+    memset(&c, 0, sizeof(c));
+    c.kind = SK_GATHER_GEMM_SCATTER;  // default assignment (network.cpp:387-390)
+    c.tile = {128, 64, 0, 128, 4};
+    return c;
+}
+
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t st;
+    explicit Timer(cudaStream_t s) : st(s) {
+        SK_CUDA(cudaEventCreate(&a));
+        SK_CUDA(cudaEventCreate(&b));
+        SK_CUDA(cudaEventRecord(a, st));
+    }
+    float stop() {
+        SK_CUDA(cudaEventRecord(b, st));
+        SK_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        SK_CUDA(cudaEventElapsedTime(&ms, a, b));
+        return ms;
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+};
+
+// Per-layer maps for the network input `root`; reuses the sk_coords caches
+// (one build per (coordinate set, K, stride, orientation) = per group).
+void ensure_maps(sk_net* n, sk_coords* root, cudaStream_t st, std::vector<double>* map_ms) {
+    if (n->root_id == root->id && !n->exec_map.empty()) return;
+    n->clear_state();
+    const size_t L = n->spec.layers.size();
+    n->in_set.assign(L, nullptr);
+    n->out_set.assign(L, nullptr);
+    n->exec_map.assign(L, nullptr);
+    for (size_t i = 0; i < L; ++i) {
+        const LayerSpec& l = n->spec.layers[i];
+        std::unique_ptr<Timer> t;
+        if (map_ms) t = std::make_unique<Timer>(st);
+        sk_coords* in = l.inputs.empty() ? root : n->out_set[n->spec.index(l.inputs[0])];
+        sk_coords_retain(in);
+        n->in_set[i] = in;
+        int32_t s3[3] = {l.stride, l.stride, n->spec.dims == 3 ? l.stride : 1};
+        if (l.kind == 0) {
+            sk_coords* out = nullptr;
+            sk_status rc0 = sk_out_coords(n->ctx, in, s3, st, &out);
+            if (rc0) fail(rc0, sk_last_error());
+            n->out_set[i] = out;
+            sk_kmap* m = nullptr;
+            sk_status rc = sk_kmap_build(n->ctx, in, out, l.kernel, s3, 0, st, &m);
+            if (rc) fail(rc, sk_last_error());
+            n->exec_map[i] = m;
+        } else {
+            const int j = n->spec.index(l.transpose_of);
+            sk_coords* out = n->in_set[j];
+            sk_coords_retain(out);
+            n->out_set[i] = out;
+            sk_kmap* t2 = nullptr;
+            sk_status rc = sk_kmap_transpose(n->ctx, n->exec_map[j], st, &t2);
+            if (rc) fail(rc, sk_last_error());
+            n->exec_map[i] = t2;
+        }
+        if (map_ms) (*map_ms)[n->group_of[i]] += t->stop();
+    }
+    n->root_id = root->id;
+    ++n->map_builds;
+}
+
+void alloc_outputs(sk_net* n, cudaStream_t st) {
+    const size_t L = n->spec.layers.size();
+    n->out.resize(L);
+    n->xsum.resize(L);
+    n->x_ptr.assign(L, nullptr);
+    for (size_t i = 0; i < L; ++i) {
+        const LayerSpec& l = n->spec.layers[i];
+        size_t bytes = (size_t)std::max(n->out_set[i]->n, 1) * l.c_out * n->es();
+        if (n->out[i].bytes != bytes) n->out[i].alloc(bytes, st);
+        if (l.inputs.size() == 2) {
+            size_t xb = (size_t)std::max(n->in_set[i]->n, 1) * l.c_in * n->es();
+            if (n->xsum[i].bytes != xb) n->xsum[i].alloc(xb, st);
+        }
+    }
+}
+
+// run_forward (network.cpp:282-345)
+void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cudaStream_t st,
+                 std::vector<double>* map_ms, std::vector<double>* ker_ms) {
+    validate(channels == n->spec.layers[0].c_in || !n->spec.layers[0].inputs.empty(),
+             "network input channel count does not match the first layer");
+    ensure_maps(n, root, st, map_ms);
+    alloc_outputs(n, st);
+    const size_t L = n->spec.layers.size();
+    for (size_t i = 0; i < L; ++i) {
+        const LayerSpec& l = n->spec.layers[i];
+        std::unique_ptr<Timer> t;
+        if (ker_ms) t = std::make_unique<Timer>(st);
+        const void* x;
+        if (l.inputs.empty()) {
+            validate(channels == l.c_in, l.name + ": input channel mismatch");
+            x = feats;
+        } else if (l.inputs.size() == 1) {
+            x = n->out[n->spec.index(l.inputs[0])].p;
+        } else {
+            const long long cnt = (long long)n->in_set[i]->n * l.c_in;
+            const void* a = n->out[n->spec.index(l.inputs[0])].p;
+            const void* b = n->out[n->spec.index(l.inputs[1])].p;
+            void* y = n->xsum[i].p;
+            by_dtype(n->dt, [&](auto tag) {
+                using T = decltype(tag);
+                k_add<T><<<grid_for(cnt), 256, 0, st>>>((const T*)a, (const T*)b, cnt, (T*)y);
+            });
+            SK_LAUNCH_CHECK();
+            x = y;
+        }
+        n->x_ptr[i] = x;
+        conv_forward(n->ctx, n->exec_map[i], n->cfg[0][n->group_of[i]], n->dt, l.c_in, l.c_out, x,
+                     n->w[i].p, n->out[i].p, false, st);
+        if (ker_ms) (*ker_ms)[n->group_of[i]] += t->stop();
+    }
+}
+
+// measure_ms (network.cpp:398-438): forward always runs; dgrad / wgrad sweeps
+// with all-ones dummy gradients when requested; only masked phases count.
+double measure(sk_net* n, sk_coords* root, const void* feats, int channels, bool fwd, bool dg,
+               bool wg, cudaStream_t st) {
+    double total = 0;
+    {
+        Timer t(st);
+        run_forward(n, root, feats, channels, st, nullptr, nullptr);
+        float ms = t.stop();
+        if (fwd) total += ms;
+    }
+    if (!dg && !wg) return total;
+    const size_t L = n->spec.layers.size();
+    size_t max_out = 0, max_in = 0;
+    for (size_t i = 0; i < L; ++i) {
+        max_out = std::max(max_out, (size_t)n->out_set[i]->n * n->spec.layers[i].c_out);
+        max_in = std::max(max_in, (size_t)n->in_set[i]->n * n->spec.layers[i].c_in);
+    }
+    DevBuf ones, dx, dw;
+    ones.alloc(std::max<size_t>(max_out, 1) * n->es(), st);
+    dx.alloc(std::max<size_t>(max_in, 1) * n->es(), st);
+    size_t max_w = 0;
+    for (size_t i = 0; i < L; ++i)
+        max_w = std::max(max_w, (size_t)n->kd[i] * n->spec.layers[i].c_in * n->spec.layers[i].c_out);
+    dw.alloc(max_w * 4, st);
+    by_dtype(n->dt, [&](auto tag) {
+        using T = decltype(tag);
+        k_fill<T><<<grid_for((long long)max_out), 256, 0, st>>>((T*)ones.p, (long long)max_out, 1.f);
+    });
+    SK_LAUNCH_CHECK();
+    if (dg) {
+        Timer t(st);
+        for (size_t i = 0; i < L; ++i) {
+            const LayerSpec& l = n->spec.layers[i];
+            conv_forward(n->ctx, n->exec_map[i], n->cfg[1][n->group_of[i]], n->dt, l.c_in, l.c_out,
+                         ones.p, n->w[i].p, dx.p, true, st);
+        }
+        total += t.stop();
+    }
+    if (wg) {
+        Timer t(st);
+        for (size_t i = 0; i < L; ++i) {
+            const LayerSpec& l = n->spec.layers[i];
+            conv_wgrad(n->ctx, n->exec_map[i], n->cfg[2][n->group_of[i]], n->dt, l.c_in, l.c_out,
+                       n->x_ptr[i], ones.p, dw.as<float>(), st);
+        }
+        total += t.stop();
+    }
+    return total;
+}
+
+// Modeled DRAM bytes of a group under cfg (traffic_model, cost.cpp:47-93,
+// elem_bytes of the run dtype); the tuner's tie-break.
+double modeled_group_traffic(sk_net* n, int g, const sk_dataflow_cfg& cfg, cudaStream_t st) {
+    double total = 0;
+    for (int li : n->groups[g]) {
+        const LayerSpec& l = n->spec.layers[li];
+        sk_kmap* m = n->exec_map[li];
+        if (!m) return 0;
+        const double eb = (double)n->es();
+        const double pairs = (double)kmap_total_pairs(m, st);
+        const double n_out = m->n_out, kdv = m->kd, unit = (double)l.c_in * l.c_out;
+        double rd = 0, wr = 0;
+        if (cfg.kind == SK_GATHER_GEMM_SCATTER) {
+            wr = pairs * l.c_in + pairs * l.c_out + n_out * l.c_out;
+            rd = 2 * pairs * l.c_in + kdv * unit + pairs * l.c_out + n_out * l.c_out;
+        } else if (cfg.kind == SK_FETCH_ON_DEMAND) {
+            wr = pairs * l.c_out;
+            rd = pairs * l.c_in + kdv * unit + pairs * l.c_out;
+        } else {
+            Prepared* p = kmap_prepare(m, cfg.splits, kTileM, st);
+            const double s_eff = std::max(1, p->num_splits), red = s_eff > 1 ? 1 : 0;
+            double a_loads = 0;
+            for (int s = 0; s < p->num_splits; ++s)
+                a_loads += (double)p->rows_pad * (p->begin[s + 1] - p->begin[s]) * l.c_in;
+            wr = (s_eff * n_out + red * n_out) * l.c_out;
+            rd = a_loads + kdv * unit + red * s_eff * n_out * l.c_out;
+        }
+        total += (rd + wr) * eb;
+    }
+    return total;
+}
+
+// chained backward over layers [lo, hi] in reverse order: gout[i] (fp32) holds
+// dL/d out_i; writes dW_i into the flat buffer and pushes dL/dx into producers
+void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, cudaStream_t st) {
+    const size_t L = n->spec.layers.size();
+    size_t max_out = 0, max_in = 0;
+    for (size_t i = 0; i < L; ++i) {
+        max_out = std::max(max_out, (size_t)n->out_set[i]->n * n->spec.layers[i].c_out);
+        max_in = std::max(max_in, (size_t)n->in_set[i]->n * n->spec.layers[i].c_in);
+    }
+    DevBuf dy, dx;
+    dy.alloc(std::max<size_t>(max_out, 1) * n->es(), st);
+    dx.alloc(std::max<size_t>(max_in, 1) * n->es(), st);
+    for (int i = hi; i >= lo; --i) {
+        const LayerSpec& l = n->spec.layers[i];
+        const long long no = (long long)n->out_set[i]->n * l.c_out;
+        const long long ni = (long long)n->in_set[i]->n * l.c_in;
+        by_dtype(n->dt, [&](auto tag) {
+            using T = decltype(tag);
+            k_cast_from_f32<T><<<grid_for(no), 256, 0, st>>>(n->gout[i].as<float>(), no, (T*)dy.p);
+        });
+        SK_LAUNCH_CHECK();
+        const int g = n->group_of[i];
+        conv_wgrad(n->ctx, n->exec_map[i], n->cfg[2][g], n->dt, l.c_in, l.c_out, n->x_ptr[i],
+                   dy.p, wgrad_flat + n->wgrad_off[i], st);
+        if (l.inputs.empty()) continue;  // no gradient w.r.t. the network input
+        conv_forward(n->ctx, n->exec_map[i], n->cfg[1][g], n->dt, l.c_in, l.c_out, dy.p,
+                     n->w[i].p, dx.p, true, st);
+        for (const std::string& pn : l.inputs) {
+            const int j = n->spec.index(pn);
+            by_dtype(n->dt, [&](auto tag) {
+                using T = decltype(tag);
+                k_accum<T><<<grid_for(ni), 256, 0, st>>>(n->gout[j].as<float>(), (const T*)dx.p, ni);
+            });
+            SK_LAUNCH_CHECK();
+        }
+    }
+}
+
+// ---- tuner (tuner.cpp) ----
+std::vector<sk_dataflow_cfg> default_space() {  // tuner.cpp:9-26 (12 entries)
+    std::vector<sk_dataflow_cfg> sp;
+    sk_dataflow_cfg c = default_cfg();
+    sp.push_back(c);
+    c.kind = SK_FETCH_ON_DEMAND;
+    sp.push_back(c);
+    for (int s = 0; s <= 4; ++s)
+        for (int large = 0; large < 2; ++large) {
+            sk_dataflow_cfg ig = default_cfg();
+            ig.kind = SK_IMPLICIT_GEMM;
+            ig.splits = s;
+            ig.tile.cta_n = large ? 0 : 64;  // tile_large = whole C_out per tile
+            sp.push_back(ig);
+        }
+    return sp;
+}
+
+}  // namespace
+
+namespace {
+template <class F>
+sk_status nguard(F&& f) {
+    try {
+        f();
+        return SK_OK;
+    } catch (const sk::Error& e) {
+        sk::set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        sk::set_last_error(e.what());
+        return SK_ERR_INTERNAL;
+    }
+}
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+sk_status sk_net_create(sk_ctx* ctx, int dims, const char* spec_text, sk_dtype dtype, sk_net** out) {
+    return nguard([&] {
+        validate(ctx && out, "null argument");
+        auto n = std::make_unique<sk_net>();
+        n->ctx = ctx;
+        n->dt = dtype;
+        n->spec = parse_spec(dims, spec_text);
+        n->groups = partition_groups(n->spec);
+        const size_t L = n->spec.layers.size();
+        n->group_of.assign(L, 0);
+        for (size_t g = 0; g < n->groups.size(); ++g)
+            for (int li : n->groups[g]) n->group_of[li] = (int)g;
+        n->kd.resize(L);
+        n->w.resize(L);
+        n->wgrad_off.resize(L);
+        size_t off = 0;
+        for (size_t i = 0; i < L; ++i) {
+            const LayerSpec& l = n->spec.layers[i];
+            n->kd[i] = dims == 3 ? l.kernel * l.kernel * l.kernel : l.kernel * l.kernel;
+            n->w[i].alloc((size_t)n->kd[i] * l.c_in * l.c_out * n->es(), nullptr);
+            n->wgrad_off[i] = off;
+            off += (size_t)n->kd[i] * l.c_in * l.c_out;
+        }
+        n->wgrad_total = off;
+        for (int ph = 0; ph < 3; ++ph) n->cfg[ph].assign(n->groups.size(), default_cfg());
+        SK_CUDA(cudaStreamSynchronize(nullptr));
+        *out = n.release();
+    });
+}
+
+sk_status sk_net_destroy(sk_net* n) {
+    return nguard([&] { delete n; });
+}
+
+int sk_net_num_layers(const sk_net* n) { return n ? (int)n->spec.layers.size() : -1; }
+int sk_net_num_groups(const sk_net* n) { return n ? (int)n->groups.size() : -1; }
+int sk_net_group_of_layer(const sk_net* n, int layer) {
+    return n && layer >= 0 && layer < (int)n->group_of.size() ? n->group_of[layer] : -1;
+}
+
+sk_status sk_net_layer_info(const sk_net* n, int layer, int* num_offsets, int* c_in, int* c_out,
+                            int64_t* wgrad_offset) {
+    return nguard([&] {
+        validate(layer >= 0 && layer < (int)n->spec.layers.size(), "layer index out of range");
+        *num_offsets = n->kd[layer];
+        *c_in = n->spec.layers[layer].c_in;
+        *c_out = n->spec.layers[layer].c_out;
+        if (wgrad_offset) *wgrad_offset = (int64_t)n->wgrad_off[layer];
+    });
+}
+
+int64_t sk_net_num_params(const sk_net* n) { return n ? (int64_t)n->wgrad_total : -1; }
+
+sk_status sk_net_weight_ptr(sk_net* n, int layer, void** ptr) {
+    return nguard([&] {
+        validate(layer >= 0 && layer < (int)n->spec.layers.size(), "layer index out of range");
+        *ptr = n->w[layer].p;
+    });
+}
+
+sk_status sk_net_set_config(sk_net* n, int group, int phase, const sk_dataflow_cfg* cfg) {
+    return nguard([&] {
+        validate(group >= 0 && group < (int)n->groups.size(), "group index out of range");
+        validate(phase >= 0 && phase < 3, "phase must be 0 (forward), 1 (dgrad) or 2 (wgrad)");
+        validate(cfg->splits >= 0 && cfg->kind >= 0 && cfg->kind <= 2, "invalid dataflow config");
+        n->cfg[phase][group] = *cfg;
+    });
+}
+
+sk_status sk_net_get_config(const sk_net* n, int group, int phase, sk_dataflow_cfg* cfg) {
+    return nguard([&] {
+        validate(group >= 0 && group < (int)n->groups.size(), "group index out of range");
+        validate(phase >= 0 && phase < 3, "bad phase");
+        *cfg = n->cfg[phase][group];
+    });
+}
+
+// NetworkRunner::forward (network.cpp:392): returns the last layer's output
+// (library-owned, valid until the next forward). mapping_ms / kernel_ms (per
+// group, may be NULL) add CUDA-event timing (RunStats) and synchronise.
+sk_status sk_net_forward(sk_net* n, sk_coords* in, const void* d_feats, int channels,
+                         void* stream, const void** d_out, int* n_out, double* mapping_ms,
+                         double* kernel_ms) {
+    return nguard([&] {
+        validate(n && in, "null argument");
+        std::vector<double> mp(n->groups.size(), 0.0), kr(n->groups.size(), 0.0);
+        const bool timed = mapping_ms || kernel_ms;
+        run_forward(n, in, d_feats, channels, S(stream), timed ? &mp : nullptr,
+                    timed ? &kr : nullptr);
+        if (d_out) *d_out = n->out.back().p;
+        if (n_out) *n_out = n->out_set.back()->n;
+        for (size_t g = 0; g < n->groups.size(); ++g) {
+            if (mapping_ms) mapping_ms[g] = mp[g];
+            if (kernel_ms) kernel_ms[g] = kr[g];
+        }
+    });
+}
+
+sk_status sk_net_layer_output(sk_net* n, int layer, const void** d_out, int* rows) {
+    return nguard([&] {
+        validate(layer >= 0 && layer < (int)n->out.size(), "no forward output for layer");
+        *d_out = n->out[layer].p;
+        *rows = n->out_set[layer]->n;
+    });
+}
+
+sk_status sk_net_measure(sk_net* n, sk_coords* in, const void* d_feats, int channels, int fwd,
+                         int dgrad, int wgrad, void* stream, double* ms) {
+    return nguard([&] {
+        *ms = measure(n, in, d_feats, channels, fwd != 0, dgrad != 0, wgrad != 0, S(stream));
+    });
+}
+
+int64_t sk_net_map_builds(const sk_net* n) { return n ? n->map_builds : -1; }
+
+sk_status sk_net_group_traffic(sk_net* n, int group, const sk_dataflow_cfg* cfg, void* stream,
+                               double* bytes) {
+    return nguard([&] {
+        validate(group >= 0 && group < (int)n->groups.size(), "group index out of range");
+        *bytes = modeled_group_traffic(n, group, *cfg, S(stream));
+    });
+}
+
+// Chained backward after sk_net_forward. d_grad_out: dL/d(last output) in the
+// run dtype; layers [layer_lo, layer_hi] are processed (call with decreasing
+// ranges to interleave gradient all-reduce buckets); the first call (layer_hi
+// = last layer) seeds the gradient buffers. wgrad_flat: fp32, layout from
+// sk_net_layer_info(... wgrad_offset).
+sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, int layer_hi,
+                          int layer_lo, void* stream) {
+    return nguard([&] {
+        const int L = (int)n->spec.layers.size();
+        validate(layer_hi < L && layer_lo >= 0 && layer_lo <= layer_hi, "bad layer range");
+        validate(!n->exec_map.empty(), "backward before forward");
+        cudaStream_t st = S(stream);
+        if (layer_hi == L - 1) {
+            n->gout.resize(L);
+            for (int i = 0; i < L; ++i) {
+                size_t b = (size_t)std::max(n->out_set[i]->n, 1) * n->spec.layers[i].c_out * 4;
+                if (n->gout[i].bytes != b) n->gout[i].alloc(b, st);
+                SK_CUDA(cudaMemsetAsync(n->gout[i].p, 0, b, st));
+            }
+            const long long no = (long long)n->out_set[L - 1]->n * n->spec.layers[L - 1].c_out;
+            by_dtype(n->dt, [&](auto tag) {
+                using T = decltype(tag);
+                k_accum<T><<<grid_for(no), 256, 0, st>>>(n->gout[L - 1].as<float>(),
+                                                         (const T*)d_grad_out, no);
+            });
+            SK_LAUNCH_CHECK();
+        }
+        run_backward(n, layer_hi, layer_lo, wgrad_flat, st);
+    });
+}
+
+// tune_inference / tune_training (tuner.cpp:134-220) over the default
+// 12-entry space with a CUDA-event RunnerProbe (warmup, median of runs) on the
+// given sample. training: 0 = inference, 1 = workload_pattern, 2 = sparse_mapping.
+// log (optional, capacity log_cap entries of {pass, group, space_index, ms}).
+sk_status sk_net_tune(sk_net* n, sk_coords* in, const void* d_feats, int channels, int training,
+                      int warmup, int runs, void* stream, double* latency_ms, double* log,
+                      int log_cap, int* log_len) {
+    return nguard([&] {
+        cudaStream_t st = S(stream);
+        const std::vector<sk_dataflow_cfg> space = default_space();
+        const int G = (int)n->groups.size();
+        for (int ph = 0; ph < 3; ++ph) n->cfg[ph].assign(G, default_cfg());
+        int nlog = 0;
+        auto probe = [&](bool f, bool d, bool w) {
+            for (int i = 0; i < warmup; ++i) measure(n, in, d_feats, channels, f, d, w, st);
+            std::vector<double> t(std::max(runs, 1));
+            for (auto& v : t) v = measure(n, in, d_feats, channels, f, d, w, st);
+            std::nth_element(t.begin(), t.begin() + t.size() / 2, t.end());
+            return t[t.size() / 2];
+        };
+        // greedy_pass (tuner.cpp:86-119): groups in first-appearance order,
+        // later groups at the default, argmin with ties on (traffic, order)
+        auto greedy = [&](int pass, bool f, bool d, bool w,
+                          const std::function<void(int, const sk_dataflow_cfg&)>& bind) {
+            double last = 0;
+            for (int g = 0; g < G; ++g) {
+                double best = 1e300, best_tr = 1e300;
+                int best_i = -1;
+                for (size_t si = 0; si < space.size(); ++si) {
+                    bind(g, space[si]);
+                    const double ms = probe(f, d, w);
+                    const double tr = modeled_group_traffic(n, g, space[si], st);
+                    if (log && nlog < log_cap) {
+                        log[nlog * 4 + 0] = pass;
+                        log[nlog * 4 + 1] = g;
+                        log[nlog * 4 + 2] = (double)si;
+                        log[nlog * 4 + 3] = ms;
+                    }
+                    ++nlog;
+                    if (ms < best || (ms == best && tr < best_tr)) {
+                        best = ms;
+                        best_tr = tr;
+                        best_i = (int)si;
+                    }
+                }
+                bind(g, space[best_i]);
+                last = best;
+            }
+            return last;
+        };
+        double lat = 0;
+        if (training == 0) {
+            lat = greedy(0, true, false, false,
+                         [&](int g, const sk_dataflow_cfg& c) { n->cfg[0][g] = c; });
+        } else if (training == 1) {  // workload_pattern: (fwd, dgrad) bound, then wgrad
+            lat = greedy(0, true, true, false, [&](int g, const sk_dataflow_cfg& c) {
+                n->cfg[0][g] = c;
+                n->cfg[1][g] = c;
+            });
+            lat += greedy(1, false, false, true,
+                          [&](int g, const sk_dataflow_cfg& c) { n->cfg[2][g] = c; });
+        } else {  // sparse_mapping: forward alone, then (dgrad, wgrad) bound
+            lat = greedy(0, true, false, false,
+                         [&](int g, const sk_dataflow_cfg& c) { n->cfg[0][g] = c; });
+            lat += greedy(1, false, true, true, [&](int g, const sk_dataflow_cfg& c) {
+                n->cfg[1][g] = c;
+                n->cfg[2][g] = c;
+            });
+        }
+        if (latency_ms) *latency_ms = lat;
+        if (log_len) *log_len = nlog;
+    });
+}
+
+int sk_tune_space_size(void) { return (int)default_space().size(); }
+
+sk_status sk_tune_space_entry(int i, sk_dataflow_cfg* cfg) {
+    return nguard([&] {
+        auto sp = default_space();
+        validate(i >= 0 && i < (int)sp.size(), "space index out of range");
+        *cfg = sp[i];
+    });
+}
+
+}  // extern "C"

@@ -40,7 +40,14 @@ inline void contract(bool ok, const std::string& m) {
             ::sk::fail(SK_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) +      \
                                         " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
     } while (0)
-#define SK_LAUNCH_CHECK() SK_CUDA(cudaGetLastError())
+// every library kernel launch is followed by SK_LAUNCH_CHECK(), which also
+// counts it (sk_kernel_launches: the bench's gpu_launches evidence)
+std::atomic<unsigned long long>& launch_counter();
+#define SK_LAUNCH_CHECK()                      \
+    do {                                       \
+        ::sk::launch_counter().fetch_add(1);   \
+        SK_CUDA(cudaGetLastError());           \
+    } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

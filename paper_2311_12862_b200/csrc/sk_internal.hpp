@@ -102,5 +102,6 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
                 int c_out, const void* x, const void* dy, float* dw, cudaStream_t st);
 
 uint64_t next_coord_set_id();
+void set_last_error(const std::string& m);
 
 }  // namespace sk

@@ -1,0 +1,187 @@
+"""GPU NetworkRunner / tuner parity (network.cpp, tuner.cpp) against the
+compiled reference and a PyTorch fp64 autograd reference of the same op.
+
+* group partition == the reference's (test_net_io.cpp:85-119);
+* toy U-Net and MinkUNet-18 skeleton forward: fp32 GPU vs reference f64 with
+  identical weights (rel <= 1e-4 through the network, layers at 1e-5);
+* outputs independent of the group assignment (test_net_io.cpp:142-171),
+  cached maps reused, mapping vs kernel timing split (:173-195);
+* chained backward vs torch autograd over the exported maps;
+* tuner: |log| = G x |space|, winners are the per-group argmin (test_tuner.cpp).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2311_12862_b200 import models, network, sparse
+    return torch, sparse, network, models
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0))) if a.size else 0.0
+
+
+def scan(n_points=20000, seed=4, extent=1.0, voxel=0.05):
+    from paper_2311_12862_b200.synth import planar_patches, quantize
+    return quantize(planar_patches(n_points, seed, extent), [voxel] * 3)
+
+
+def test_groups_match_reference(env, reference):
+    torch, sk, N, M = env
+    for layers in (M.toy_unet(), M.minkunet18(), M.second_encoder()):
+        net = N.NetworkRunner(layers, dtype=torch.float32)
+        rn = reference.network(3, M.spec_text(layers))
+        assert net.num_groups == rn.num_groups
+        assert [net.group_of_layer(i) for i in range(net.num_layers)] == \
+            [rn.group_of_layer(i) for i in range(net.num_layers)]
+    net = N.NetworkRunner(M.toy_unet(), dtype=torch.float32)
+    assert net.groups() == [[0, 1, 5], [2, 4], [3]]
+    assert N.NetworkRunner(M.minkunet18(), dtype=torch.float32).num_groups == 14
+
+
+@pytest.mark.parametrize("which", ["toy", "minkunet", "second"])
+def test_forward_matches_reference(env, reference, which):
+    torch, sk, N, M = env
+    layers = {"toy": M.toy_unet, "minkunet": M.minkunet18, "second": M.second_encoder}[which]()
+    coords = scan(6000 if which != "second" else 20000, seed=5,
+                  extent=1.0 if which != "second" else 3.0,
+                  voxel=0.05 if which != "second" else 0.08)
+    net = N.NetworkRunner(layers, dtype=torch.float32, weight_seed=11)
+    ws = [net.weight(i).double().cpu().numpy() for i in range(net.num_layers)]
+    rn = reference.network(3, M.spec_text(layers), prec=1, weights=ws)
+    c_in = layers[0].c_in
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(len(coords), c_in, generator=g)
+    rn.set_input(coords, x.double().numpy(), prec=1)
+    y_ref = rn.output()
+    cs = sk.CoordSet.create(coords)
+    for cfg in (sk.DataflowConfig(sk.IMPLICIT_GEMM, 1), sk.DataflowConfig(sk.FETCH_ON_DEMAND),
+                sk.DataflowConfig(sk.GATHER_GEMM_SCATTER), sk.DataflowConfig(sk.IMPLICIT_GEMM, 3)):
+        net.set_all(cfg)
+        y, _ = net.forward(cs, x.cuda())
+        torch.cuda.synchronize()
+        assert y.shape == y_ref.shape
+        assert rel(y.double().cpu().numpy(), y_ref) <= 1e-4, cfg.name()
+
+
+def test_half_network_close_to_reference(env, reference):
+    """fp16 tensor-core path through the 77-layer MinkUNet stays close to the
+    f64 reference on the same (half-rounded) weights and inputs."""
+    torch, sk, N, M = env
+    layers = M.minkunet18()
+    coords = scan(8000, seed=6)
+    net = N.NetworkRunner(layers, dtype=torch.float16, weight_seed=12)
+    ws = [net.weight(i).double().cpu().numpy() for i in range(net.num_layers)]
+    rn = reference.network(3, M.spec_text(layers), prec=1, weights=ws)
+    x = torch.randn(len(coords), 4, generator=torch.Generator().manual_seed(2)).half()
+    rn.set_input(coords, x.double().numpy(), prec=1)
+    y_ref = rn.output()
+    net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1))
+    y, _ = net.forward(sk.CoordSet.create(coords), x.cuda())
+    torch.cuda.synchronize()
+    scale = max(1.0, float(np.abs(y_ref).max()))
+    err = float(np.abs(y.double().cpu().numpy() - y_ref).max()) / scale
+    assert err <= 2e-2, err
+
+
+def test_map_cache_and_timing_split(env):
+    torch, sk, N, M = env
+    net = N.NetworkRunner(M.toy_unet(), dtype=torch.float16)
+    cs = sk.CoordSet.create(scan(3000, seed=7))
+    x = torch.randn(cs.n, 1, device="cuda").half()
+    _, st1 = net.forward(cs, x, stats=True)
+    builds = net.map_build_count()
+    _, st2 = net.forward(cs, x, stats=True)
+    assert net.map_build_count() == builds  # cached maps reused (network.cpp:207)
+    assert st1["mapping_ms"].sum() > 0 and st1["kernel_ms"].sum() > 0
+    assert st2["mapping_ms"].sum() < st1["mapping_ms"].sum() * 0.5
+    assert net.measure_ms(cs, x, True, True, True) > 0
+    for g in range(net.num_groups):
+        assert net.modeled_group_traffic(g, sk.DataflowConfig(sk.IMPLICIT_GEMM, 1)) > 0
+
+
+def _torch_reference(torch, layers, net, cs_maps, x, ws):
+    """fp64 autograd restatement of run_forward over the GPU's exported maps."""
+    outs = {}
+    name_idx = {l.name: i for i, l in enumerate(layers)}
+    for i, l in enumerate(layers):
+        if not l.inputs:
+            xi = x
+        elif len(l.inputs) == 1:
+            xi = outs[l.inputs[0]]
+        else:
+            xi = outs[l.inputs[0]] + outs[l.inputs[1]]
+        ent = cs_maps[i]
+        y = torch.zeros(ent.shape[0], l.c_out, dtype=torch.float64)
+        for k in range(ent.shape[1]):
+            idx = ent[:, k]
+            m = idx >= 0
+            if m.any():
+                y = y.index_add(0, torch.nonzero(m).flatten(),
+                                xi[idx[m]] @ ws[i][k])
+        outs[l.name] = y
+    return outs[layers[-1].name]
+
+
+def test_backward_matches_torch_autograd(env):
+    torch, sk, N, M = env
+    layers = M.toy_unet()
+    coords = scan(2500, seed=8)
+    net = N.NetworkRunner(layers, dtype=torch.float32, weight_seed=13)
+    cs = sk.CoordSet.create(coords)
+    x = torch.randn(cs.n, 1, generator=torch.Generator().manual_seed(3))
+    net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1))
+    y, _ = net.forward(cs, x.cuda())
+    r = torch.randn(y.shape, generator=torch.Generator().manual_seed(4))
+    wgrad = torch.zeros(net.num_params, device="cuda")
+    net.backward(r.cuda(), wgrad)
+    torch.cuda.synchronize()
+    # exported execution-orientation maps of every layer
+    ins = {}
+    maps = []
+    down = sk.build_out_coords(cs, 2)
+    for l in layers:
+        if l.name == "down":
+            maps.append(sk.build_kmap(cs, down, 3, 2).os()[0])
+        elif l.name == "up":
+            maps.append(sk.build_kmap(cs, down, 3, 2).transpose().os()[0])
+        elif l.name == "mid":
+            maps.append(sk.build_kmap(down, down, 3, 1).os()[0])
+        else:
+            maps.append(sk.build_kmap(cs, cs, 3, 1).os()[0])
+    maps = [torch.from_numpy(m).long() for m in maps]
+    ws = [net.weight(i).double().cpu().requires_grad_(True) for i in range(net.num_layers)]
+    yr = _torch_reference(torch, layers, net, maps, x.double(), ws)
+    assert rel(y.double().cpu().numpy(), yr.detach().numpy()) <= 1e-4
+    (yr * r.double()).sum().backward()
+    for i in range(net.num_layers):
+        got = net.weight_grad(wgrad, i).double().cpu().numpy()
+        want = ws[i].grad.numpy()
+        scale = max(1.0, float(np.abs(want).max()))
+        assert float(np.abs(got - want).max()) / scale <= 1e-4, layers[i].name
+
+
+def test_tuner_contracts(env):
+    torch, sk, N, M = env
+    net = N.NetworkRunner(M.toy_unet(), dtype=torch.float16)
+    cs = sk.CoordSet.create(scan(3000, seed=9))
+    x = torch.randn(cs.n, 1, device="cuda").half()
+    space = N.default_space()
+    assert len(space) == 12
+    lat, log = net.tune(cs, x, training=0, warmup=1, runs=3)
+    G = net.num_groups
+    assert len(log) == G * len(space)  # tuner.cpp:86-119 call count
+    for g in range(G):
+        rows = log[log[:, 1] == g]
+        best = int(rows[np.argmin(rows[:, 3]), 2])
+        assert net.config(g) == space[best]
+    lat2, log2 = net.tune(cs, x, training=2, warmup=0, runs=1)
+    assert len(log2) == 2 * G * len(space)
