@@ -266,6 +266,14 @@ struct sk_net {
 
 namespace {
 
+// a group's config applied to one layer: implicit-GEMM splits are clamped to
+// the layer's K^D (the K=1 projection layers of a group cannot split)
+sk_dataflow_cfg layer_cfg(const sk_net* n, int phase, int layer) {
+    sk_dataflow_cfg c = n->cfg[phase][n->group_of[layer]];
+    if (c.splits > n->kd[layer]) c.splits = n->kd[layer];
+    return c;
+}
+
 sk_dataflow_cfg default_cfg() {
     sk_dataflow_cfg c;
     memset(&c, 0, sizeof(c));
@@ -384,7 +392,7 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
             x = y;
         }
         n->x_ptr[i] = x;
-        conv_forward(n->ctx, n->exec_map[i], n->cfg[0][n->group_of[i]], n->dt, l.c_in, l.c_out, x,
+        conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 0, (int)i), n->dt, l.c_in, l.c_out, x,
                      n->w[i].p, n->out[i].p, false, st);
         if (ker_ms) (*ker_ms)[n->group_of[i]] += t->stop();
     }
@@ -424,7 +432,7 @@ double measure(sk_net* n, sk_coords* root, const void* feats, int channels, bool
         Timer t(st);
         for (size_t i = 0; i < L; ++i) {
             const LayerSpec& l = n->spec.layers[i];
-            conv_forward(n->ctx, n->exec_map[i], n->cfg[1][n->group_of[i]], n->dt, l.c_in, l.c_out,
+            conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, (int)i), n->dt, l.c_in, l.c_out,
                          ones.p, n->w[i].p, dx.p, true, st);
         }
         total += t.stop();
@@ -433,7 +441,7 @@ double measure(sk_net* n, sk_coords* root, const void* feats, int channels, bool
         Timer t(st);
         for (size_t i = 0; i < L; ++i) {
             const LayerSpec& l = n->spec.layers[i];
-            conv_wgrad(n->ctx, n->exec_map[i], n->cfg[2][n->group_of[i]], n->dt, l.c_in, l.c_out,
+            conv_wgrad(n->ctx, n->exec_map[i], layer_cfg(n, 2, (int)i), n->dt, l.c_in, l.c_out,
                        n->x_ptr[i], ones.p, dw.as<float>(), st);
         }
         total += t.stop();
@@ -495,10 +503,10 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, cudaStream_t st)
         });
         SK_LAUNCH_CHECK();
         const int g = n->group_of[i];
-        conv_wgrad(n->ctx, n->exec_map[i], n->cfg[2][g], n->dt, l.c_in, l.c_out, n->x_ptr[i],
+        conv_wgrad(n->ctx, n->exec_map[i], layer_cfg(n, 2, i), n->dt, l.c_in, l.c_out, n->x_ptr[i],
                    dy.p, wgrad_flat + n->wgrad_off[i], st);
         if (l.inputs.empty()) continue;  // no gradient w.r.t. the network input
-        conv_forward(n->ctx, n->exec_map[i], n->cfg[1][g], n->dt, l.c_in, l.c_out, dy.p,
+        conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, i), n->dt, l.c_in, l.c_out, dy.p,
                      n->w[i].p, dx.p, true, st);
         for (const std::string& pn : l.inputs) {
             const int j = n->spec.index(pn);
