@@ -198,7 +198,8 @@ int sk_net_group_of_layer(const sk_net* net, int layer);
 sk_status sk_net_layer_info(const sk_net* net, int layer, int* num_offsets, int* c_in,
                             int* c_out, int64_t* wgrad_offset);
 int64_t sk_net_num_params(const sk_net* net);
-/* device weight buffer of a layer (write it with cudaMemcpy / kernels) */
+/* device weight buffer of a layer (write it with cudaMemcpy / kernels).
+ * Calling this marks the runner's cached transposed weights stale. */
 sk_status sk_net_weight_ptr(sk_net* net, int layer, void** ptr);
 /* GroupConfig (network.hpp:54-58): phase 0 forward, 1 dgrad, 2 wgrad */
 sk_status sk_net_set_config(sk_net* net, int group, int phase, const sk_dataflow_cfg* cfg);

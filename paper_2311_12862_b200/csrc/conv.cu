@@ -793,8 +793,12 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
     stages = std::max(stages, 2);
     const size_t smem = stages * stage_bytes + kIdxRing * (kTileM * 4 + 16) +
                         (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
-    SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    static size_t configured = 0;  // per template instantiation
+    if (smem > configured) {
+        SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
     k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages);
     SK_LAUNCH_CHECK();
 }
@@ -873,7 +877,8 @@ void gather_rows(const void* x, int c, const int* idx, const int* tiles, void* b
 
 // Forward (dgrad = false) or dgrad (dgrad = true; m_fwd is the FORWARD map).
 void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
-                  int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st) {
+                  int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
+                  const void* w_kmajor) {
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     validate(cfg.splits >= 0, "splits must be >= 0");
     validate(cfg.kind >= 0 && cfg.kind <= 2, "unknown dataflow kind");
@@ -890,7 +895,9 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     // exec.cpp:32-43)
     DevBuf wt;
     const void* b = w;
-    if (!dgrad) {
+    if (!dgrad && w_kmajor) {
+        b = w_kmajor;  // caller keeps W^T [kd][c_out][c_in] (inference weights)
+    } else if (!dgrad) {
         wt.alloc((size_t)m->kd * c_in * c_out * es, st);
         long long tot = (long long)m->kd * c_in * c_out;
         const int g = (int)ceil_div(tot, 256);
@@ -1017,6 +1024,17 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         }
     }
     if (dt != SK_F32) convert_from_f32(dt, yf, y_elems, y, st);
+}
+
+void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, void* wt,
+                       cudaStream_t st) {
+    const long long tot = (long long)kd * c_in * c_out;
+    if (tot == 0) return;
+    const int g = (int)ceil_div(tot, 256);
+    if (dt == SK_F32) k_transpose_w<float><<<g, 256, 0, st>>>((const float*)w, kd, c_in, c_out, (float*)wt);
+    else if (dt == SK_F16) k_transpose_w<__half><<<g, 256, 0, st>>>((const __half*)w, kd, c_in, c_out, (__half*)wt);
+    else k_transpose_w<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)w, kd, c_in, c_out, (__nv_bfloat16*)wt);
+    SK_LAUNCH_CHECK();
 }
 
 void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,

@@ -240,6 +240,8 @@ struct sk_net {
     std::vector<int> group_of;
     std::vector<int> kd;
     std::vector<DevBuf> w;
+    std::vector<DevBuf> wt;    // W^T per layer for the forward B operand (K-major)
+    bool wt_dirty = true;      // weights may have changed since the last transpose
     std::vector<sk_dataflow_cfg> cfg[3];  // per group: forward, dgrad, wgrad
     // state of the last forward
     uint64_t root_id = 0;
@@ -362,12 +364,24 @@ void alloc_outputs(sk_net* n, cudaStream_t st) {
 }
 
 // run_forward (network.cpp:282-345)
+void refresh_wt(sk_net* n, cudaStream_t st) {
+    if (!n->wt_dirty) return;
+    n->wt.resize(n->w.size());
+    for (size_t i = 0; i < n->w.size(); ++i) {
+        const LayerSpec& l = n->spec.layers[i];
+        if (n->wt[i].bytes != n->w[i].bytes) n->wt[i].alloc(n->w[i].bytes, st);
+        transpose_weights(n->dt, n->w[i].p, n->kd[i], l.c_in, l.c_out, n->wt[i].p, st);
+    }
+    n->wt_dirty = false;
+}
+
 void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cudaStream_t st,
                  std::vector<double>* map_ms, std::vector<double>* ker_ms) {
     validate(channels == n->spec.layers[0].c_in || !n->spec.layers[0].inputs.empty(),
              "network input channel count does not match the first layer");
     ensure_maps(n, root, st, map_ms);
     alloc_outputs(n, st);
+    refresh_wt(n, st);
     const size_t L = n->spec.layers.size();
     for (size_t i = 0; i < L; ++i) {
         const LayerSpec& l = n->spec.layers[i];
@@ -393,7 +407,7 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
         }
         n->x_ptr[i] = x;
         conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 0, (int)i), n->dt, l.c_in, l.c_out, x,
-                     n->w[i].p, n->out[i].p, false, st);
+                     n->w[i].p, n->out[i].p, false, st, n->wt[i].p);
         if (ker_ms) (*ker_ms)[n->group_of[i]] += t->stop();
     }
 }
@@ -615,6 +629,7 @@ sk_status sk_net_weight_ptr(sk_net* n, int layer, void** ptr) {
     return nguard([&] {
         validate(layer >= 0 && layer < (int)n->spec.layers.size(), "layer index out of range");
         *ptr = n->w[layer].p;
+        n->wt_dirty = true;  // the caller may write through the pointer
     });
 }
 

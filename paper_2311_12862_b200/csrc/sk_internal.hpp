@@ -96,8 +96,13 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st);
 int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st);
 
 // conv.cu
+// w_kmajor (optional, forward only): W already transposed to [kd][c_out][c_in]
 void conv_forward(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
-                  int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st);
+                  int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
+                  const void* w_kmajor = nullptr);
+// W [kd][c_in][c_out] -> W^T [kd][c_out][c_in]
+void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, void* wt,
+                       cudaStream_t st);
 void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                 int c_out, const void* x, const void* dy, float* dw, cudaStream_t st);
 
