@@ -482,7 +482,7 @@ double modeled_group_traffic(sk_net* n, int g, const sk_dataflow_cfg& cfg, cudaS
             wr = pairs * l.c_out;
             rd = pairs * l.c_in + kdv * unit + pairs * l.c_out;
         } else {
-            Prepared* p = kmap_prepare(m, cfg.splits, kTileM, st);
+            Prepared* p = kmap_prepare(m, std::min(cfg.splits, m->kd), kTileM, st);
             const double s_eff = std::max(1, p->num_splits), red = s_eff > 1 ? 1 : 0;
             double a_loads = 0;
             for (int s = 0; s < p->num_splits; ++s)
