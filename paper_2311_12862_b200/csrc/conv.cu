@@ -74,6 +74,7 @@ struct ConvArgs {
     int out_mode;  // 0 store T, 1 store f32, 2 red.add f32, 3 RMW f32
     int ld_y;
     int n_ntiles, bn;
+    const void* residual;  // optional [n_out][ld_y] T added in the epilogue (out_mode 0)
     int items;        // OS mode item count (WS mode: derived on device)
     int split_only;   // >= 0: only items of this split (deterministic sequencing)
     int offset_only;  // >= 0: WS mode only tiles of this offset
@@ -226,6 +227,12 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, __half*) {
 __device__ __forceinline__ uint32_t pack2(float a, float b, __nv_bfloat16*) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack2(uint32_t u, __half*) {
+    return __half22float2(*reinterpret_cast<__half2*>(&u));
+}
+__device__ __forceinline__ float2 unpack2(uint32_t u, __nv_bfloat16*) {
+    return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -509,6 +516,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 if (orow < 0 || col >= p.n_total) continue;
                 if (p.out_mode == 0) {
                     T* dst = static_cast<T*>(p.y) + (size_t)orow * p.ld_y + col;
+                    if (p.residual) {  // fused skip connection: y = conv + residual
+                        const uint4* rs = reinterpret_cast<const uint4*>(
+                            static_cast<const T*>(p.residual) + (size_t)orow * p.ld_y + col);
+                        const uint4 r0 = rs[0], r1 = rs[1];
+                        const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            float2 f = unpack2(rr[i], (T*)nullptr);
+                            v[2 * i] = __float_as_uint(__uint_as_float(v[2 * i]) + f.x);
+                            v[2 * i + 1] = __float_as_uint(__uint_as_float(v[2 * i + 1]) + f.y);
+                        }
+                    }
                     uint4 u0, u1;
                     u0.x = pack2(__uint_as_float(v[0]), __uint_as_float(v[1]), (T*)nullptr);
                     u0.y = pack2(__uint_as_float(v[2]), __uint_as_float(v[3]), (T*)nullptr);
@@ -637,8 +656,9 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
                 const int col = n0 + tc * 4 + jj;
                 if (col >= p.n_total) continue;
                 const size_t o = (size_t)orow * p.ld_y + col;
-                if (p.out_mode == 0) static_cast<T*>(p.y)[o] = from_f<T>(acc[i][jj]);
-                else if (p.out_mode == 1) static_cast<float*>(p.y)[o] = acc[i][jj];
+                const float res = p.residual ? to_f(static_cast<const T*>(p.residual)[o]) : 0.f;
+                if (p.out_mode == 0) static_cast<T*>(p.y)[o] = from_f<T>(acc[i][jj] + res);
+                else if (p.out_mode == 1) static_cast<float*>(p.y)[o] = acc[i][jj] + res;
                 else if (p.out_mode == 2) atomicAdd(static_cast<float*>(p.y) + o, acc[i][jj]);
                 else static_cast<float*>(p.y)[o] += acc[i][jj];
             }
@@ -662,9 +682,24 @@ __global__ void k_transpose_w(const T* __restrict__ w, int kd, int c_in, int c_o
 }
 
 template <typename T>
-__global__ void k_convert_out(const float* __restrict__ src, long long n, T* __restrict__ dst) {
+__global__ void k_convert_out(const float* __restrict__ src, long long n, T* __restrict__ dst,
+                              const T* __restrict__ res) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) dst[i] = from_f<T>(src[i]);
+    if (i < n) dst[i] = from_f<T>(src[i] + (res ? to_f(res[i]) : 0.f));
+}
+
+// dst[r][0:k_pad] = src[r][0:k] with zero channels k..k_pad (tensor-core
+// operands need 16 B rows: C_in % 8 != 0 inputs, e.g. the 4-channel stem)
+template <typename T>
+__global__ void k_pad_cols(const T* __restrict__ src, long long rows, int k, int k_pad,
+                           T* __restrict__ dst) {
+    const long long n = rows * k_pad;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / k_pad;
+        const int c = (int)(i % k_pad);
+        dst[i] = c < k ? src[r * k + c] : from_f<T>(0.f);
+    }
 }
 
 // GGS gather over the padded pair lists: buf[i] = x[in_pad[i]] (zeros for pads)
@@ -845,16 +880,28 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
 }
 
 template <typename T>
-void convert_out(const float* src, long long n, void* dst, cudaStream_t st) {
+void convert_out(const float* src, long long n, void* dst, const void* res, cudaStream_t st) {
     if (n <= 0) return;
-    k_convert_out<T><<<(int)ceil_div(n, 256), 256, 0, st>>>(src, n, static_cast<T*>(dst));
+    k_convert_out<T><<<(int)ceil_div(n, 256), 256, 0, st>>>(src, n, static_cast<T*>(dst),
+                                                              static_cast<const T*>(res));
     SK_LAUNCH_CHECK();
 }
 
-void convert_from_f32(sk_dtype dt, const float* src, long long n, void* dst, cudaStream_t st) {
-    if (dt == SK_F16) convert_out<__half>(src, n, dst, st);
-    else if (dt == SK_BF16) convert_out<__nv_bfloat16>(src, n, dst, st);
-    else SK_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, st));
+// fp32 accumulator -> output dtype (+ fused residual)
+void convert_from_f32(sk_dtype dt, const float* src, long long n, void* dst, const void* res,
+                      cudaStream_t st) {
+    if (dt == SK_F16) convert_out<__half>(src, n, dst, res, st);
+    else if (dt == SK_BF16) convert_out<__nv_bfloat16>(src, n, dst, res, st);
+    else if (res || src != dst) convert_out<float>(src, n, dst, res, st);
+}
+
+template <typename T>
+void pad_cols(const void* src, long long rows, int k, int k_pad, void* dst, cudaStream_t st) {
+    const long long n = rows * k_pad;
+    if (n <= 0) return;
+    k_pad_cols<T><<<(int)std::min<long long>(ceil_div(n, 256), 148 * 32), 256, 0, st>>>(
+        static_cast<const T*>(src), rows, k, k_pad, static_cast<T*>(dst));
+    SK_LAUNCH_CHECK();
 }
 
 ConvArgs base_args() {
@@ -878,7 +925,7 @@ void gather_rows(const void* x, int c, const int* idx, const int* tiles, void* b
 // Forward (dgrad = false) or dgrad (dgrad = true; m_fwd is the FORWARD map).
 void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
-                  const void* w_kmajor) {
+                  const void* w_kmajor, const void* residual) {
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     validate(cfg.splits >= 0, "splits must be >= 0");
     validate(cfg.kind >= 0 && cfg.kind <= 2, "unknown dataflow kind");
@@ -907,11 +954,29 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         SK_LAUNCH_CHECK();
         b = wt.p;
     }
-    const bool tc = tc_ok(dt, k_total, n_total);
+    // tensor cores need 16 B operand rows: zero-pad C % 8 != 0 channel dims
+    // (the 4-channel stem) instead of taking the SIMT path
+    DevBuf xpad, bpad;
+    int k_eff = k_total;
+    if (dt != SK_F32 && k_total % 8 != 0 && n_total % 16 == 0) {
+        k_eff = (k_total + 7) / 8 * 8;
+        xpad.alloc((size_t)std::max(m->n_in, 1) * k_eff * es, st);
+        bpad.alloc((size_t)m->kd * n_total * k_eff * es, st);
+        if (dt == SK_F16) {
+            pad_cols<__half>(x, m->n_in, k_total, k_eff, xpad.p, st);
+            pad_cols<__half>(b, (long long)m->kd * n_total, k_total, k_eff, bpad.p, st);
+        } else {
+            pad_cols<__nv_bfloat16>(x, m->n_in, k_total, k_eff, xpad.p, st);
+            pad_cols<__nv_bfloat16>(b, (long long)m->kd * n_total, k_total, k_eff, bpad.p, st);
+        }
+        x = xpad.p;
+        b = bpad.p;
+    }
+    const bool tc = tc_ok(dt, k_eff, n_total);
     ConvArgs a = base_args();
     a.kd = m->kd;
     a.a = x;
-    a.k_total = k_total;
+    a.k_total = k_eff;
     a.n_rows_a = m->n_in;
     a.b = b;
     a.n_total = n_total;
@@ -934,6 +999,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         if (pr->num_splits == 1) {
             a.items = a.n_tiles * a.n_ntiles;
             a.y = y;
+            a.residual = residual;
             a.out_mode = dt == SK_F32 ? 1 : 0;
             launch_gconv(ctx, dt, a, st);
         } else {
@@ -959,7 +1025,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
                 a.items = pr->num_splits * a.n_tiles * a.n_ntiles;
                 launch_gconv(ctx, dt, a, st);
             }
-            if (dt != SK_F32) convert_from_f32(dt, yf, y_elems, y, st);
+            if (dt != SK_F32 || residual) convert_from_f32(dt, yf, y_elems, y, residual, st);
         }
         return;
     }
@@ -1023,7 +1089,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
             }
         }
     }
-    if (dt != SK_F32) convert_from_f32(dt, yf, y_elems, y, st);
+    if (dt != SK_F32 || residual) convert_from_f32(dt, yf, y_elems, y, residual, st);
 }
 
 void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, void* wt,

@@ -125,86 +125,89 @@ __device__ __forceinline__ int probe(const unsigned long long* __restrict__ keys
     }
 }
 
-// One thread per output row, all KD offsets. Writes OS entries + masks for a
-// 128-row block (pad rows get -1 / 0) and the block's per-offset pair counts.
-template <int KD>
-__global__ void __launch_bounds__(kQB) k_kmap_query(
+// TPR threads per output row (offsets k = sub, sub+TPR, ...; up to
+// ceil(KD/TPR) independent probes in flight per thread), 128 rows per block.
+// Writes the OS entries + masks of the block (pad rows get -1 / 0) and the
+// block's per-offset pair counts.
+template <int KD, int TPR>
+__global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
     const int4* __restrict__ out_coords, int n_out, const unsigned long long* __restrict__ keys,
     const int* __restrict__ vals, uint64_t mask, int K, int dims, int sx, int sy, int sz,
     int transposed, int words, int* __restrict__ os, unsigned long long* __restrict__ masks,
     int* __restrict__ blk_counts) {
     extern __shared__ int q_sh[];
-    int* tile = q_sh;           // kQB x KD
+    int* tile = q_sh;            // kQB x KD
     int* cnt = q_sh + kQB * KD;  // KD
+    constexpr int PER = (KD + TPR - 1) / TPR;
     const int t = threadIdx.x;
-    const int row = blockIdx.x * kQB + t;
-    for (int k = t; k < KD; k += kQB) cnt[k] = 0;
+    const int rl = t / TPR, sub = t % TPR;
+    const int row = blockIdx.x * kQB + rl;
+    for (int k = t; k < KD; k += kQB * TPR) cnt[k] = 0;
     __syncthreads();
-    unsigned long long m0 = 0, m1 = 0;
     const bool live = row < n_out;
-    int4 q = live ? out_coords[row] : make_int4(0, 0, 0, 0);
-    constexpr int B = 8;
-    for (int k0 = 0; k0 < KD; k0 += B) {
-        unsigned long long key[B], first[B];
-        uint64_t slot[B];
-        bool ok[B];
+    const int4 q = live ? out_coords[row] : make_int4(0, 0, 0, 0);
+    unsigned long long key[PER], first[PER];
+    uint64_t slot[PER];
+    bool ok[PER];
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-            const int k = k0 + u;
-            ok[u] = live && k < KD;
-            if (!ok[u]) continue;
-            int a, b, c;
-            offset_of(k, K, dims, a, b, c);
-            int px, py, pz;
-            if (!transposed) {
-                px = q.y * sx + a;
-                py = q.z * sy + b;
-                pz = q.w * sz + c;
-            } else {
-                // q_in = (p_out + delta) / s only when every axis divides
-                // (C++ truncating %, kmap.cpp:124-129)
-                int nx = q.y + a, ny = q.z + b, nz = q.w + c;
-                if (nx % sx != 0 || ny % sy != 0 || (dims == 3 && nz % sz != 0)) {
-                    ok[u] = false;
-                    continue;
-                }
-                px = nx / sx;
-                py = ny / sy;
-                pz = dims == 3 ? nz / sz : 0;
-            }
-            if (!packable(q.x, px, py, pz)) {
+    for (int u = 0; u < PER; ++u) {
+        const int k = sub + u * TPR;
+        ok[u] = live && k < KD;
+        if (!ok[u]) continue;
+        int a, b, c;
+        offset_of(k, K, dims, a, b, c);
+        int px, py, pz;
+        if (!transposed) {
+            px = q.y * sx + a;
+            py = q.z * sy + b;
+            pz = q.w * sz + c;
+        } else {
+            // q_in = (p_out + delta) / s only when every axis divides
+            // (C++ truncating %, kmap.cpp:124-129)
+            const int nx = q.y + a, ny = q.z + b, nz = q.w + c;
+            if (nx % sx != 0 || ny % sy != 0 || (dims == 3 && nz % sz != 0)) {
                 ok[u] = false;
                 continue;
             }
-            key[u] = pack_key(q.x, px, py, pz);
-            slot[u] = hash_key(key[u]) & mask;
-            first[u] = __ldg(&keys[slot[u]]);  // B independent loads in flight
+            px = nx / sx;
+            py = ny / sy;
+            pz = dims == 3 ? nz / sz : 0;
         }
+        if (!packable(q.x, px, py, pz)) {
+            ok[u] = false;
+            continue;
+        }
+        key[u] = pack_key(q.x, px, py, pz);
+        slot[u] = hash_key(key[u]) & mask;
+        first[u] = __ldg(&keys[slot[u]]);  // PER independent loads in flight
+    }
+    unsigned long long m0 = 0, m1 = 0;
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-            const int k = k0 + u;
-            if (k >= KD) continue;
-            int j = ok[u] ? probe(keys, vals, mask, key[u], slot[u], first[u]) : -1;
-            tile[t * KD + k] = j;
-            unsigned hit = __ballot_sync(0xffffffffu, j >= 0);
-            if ((t & 31) == 0 && hit) atomicAdd(&cnt[k], __popc(hit));
-            if (j >= 0) {
-                // big-endian bit order (kmap.cpp:38-45)
-                if (k < 64) {
-                    int biw = KD < 64 ? KD : 64;
-                    m0 |= 1ull << (biw - 1 - k);
-                } else {
-                    m1 |= 1ull << (KD - 64 - 1 - (k - 64));
-                }
-            }
+    for (int u = 0; u < PER; ++u) {
+        const int k = sub + u * TPR;
+        if (k >= KD) continue;
+        const int j = ok[u] ? probe(keys, vals, mask, key[u], slot[u], first[u]) : -1;
+        tile[rl * KD + k] = j;
+        if (j >= 0) {
+            atomicAdd(&cnt[k], 1);
+            // big-endian bit order (kmap.cpp:38-45)
+            if (k < 64) m0 |= 1ull << ((KD < 64 ? KD : 64) - 1 - k);
+            else m1 |= 1ull << (KD - 64 - 1 - (k - 64));
         }
+    }
+#pragma unroll
+    for (int o = TPR / 2; o >= 1; o >>= 1) {
+        m0 |= __shfl_xor_sync(0xffffffffu, m0, o);
+        m1 |= __shfl_xor_sync(0xffffffffu, m1, o);
     }
     __syncthreads();
     int* dst = os + (size_t)blockIdx.x * kQB * KD;
-    for (int i = t; i < kQB * KD; i += kQB) dst[i] = tile[i];
-    masks[(size_t)row * words] = m0;
-    if (words == 2) masks[(size_t)row * words + 1] = m1;
-    for (int k = t; k < KD; k += kQB) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
+    for (int i = t; i < kQB * KD; i += kQB * TPR) dst[i] = tile[i];
+    if (sub == 0) {
+        masks[(size_t)row * words] = m0;
+        if (words == 2) masks[(size_t)row * words + 1] = m1;
+    }
+    for (int k = t; k < KD; k += kQB * TPR) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
 }
 
 // masks + per-block counts from an existing OS matrix (transposed maps).
@@ -425,20 +428,20 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
     const int grid = m->rows_pad / kQB;
     const uint64_t mask = (uint64_t)in->cap - 1;
     const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
-#define SK_Q(KDV)                                                                            \
+#define SK_Q(KDV, TPRV)                                                                      \
     if (smem > 48 * 1024)                                                                    \
-        SK_CUDA(cudaFuncSetAttribute(k_kmap_query<KDV>,                                      \
+        SK_CUDA(cudaFuncSetAttribute(k_kmap_query<KDV, TPRV>,                                \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_kmap_query<KDV><<<grid, kQB, smem, st>>>(                                              \
+    k_kmap_query<KDV, TPRV><<<grid, kQB * TPRV, smem, st>>>(                                 \
         out_coords, m->n_out, in->keys.as<unsigned long long>(), in->vals.as<int>(), mask,   \
         m->kernel, m->dims, m->stride[0], m->stride[1], m->stride[2], m->transposed, m->words, \
         m->os.as<int>(), m->masks.as<unsigned long long>(), m->blk_counts.as<int>())
     switch (m->kd) {
-        case 1: SK_Q(1); break;
-        case 9: SK_Q(9); break;
-        case 25: SK_Q(25); break;
-        case 27: SK_Q(27); break;
-        case 125: SK_Q(125); break;
+        case 1: SK_Q(1, 1); break;
+        case 9: SK_Q(9, 2); break;
+        case 25: SK_Q(25, 4); break;
+        case 27: SK_Q(27, 4); break;
+        case 125: SK_Q(125, 8); break;
         default: fail(SK_ERR_VALIDATION, "unsupported kernel volume " + std::to_string(m->kd));
     }
 #undef SK_Q

@@ -248,7 +248,12 @@ struct sk_net {
     std::vector<sk_coords*> in_set, out_set;  // retained
     std::vector<sk_kmap*> exec_map;           // retained, execution orientation
     std::vector<DevBuf> out, xsum;
+    std::vector<void*> out_ptr;     // layer output (may alias the consumer's xsum)
     std::vector<const void*> x_ptr;
+    // skip-add fusion: layer P (only consumer L = fuse_into[P]) writes
+    // xsum[L] = conv_P(x) + out[residual_of[P]] in its epilogue
+    std::vector<int> fuse_into, residual_of;
+    std::vector<char> fused_input;  // L's xsum is produced by a fused producer
     std::vector<size_t> wgrad_off;
     size_t wgrad_total = 0;
     std::vector<DevBuf> gout;  // fp32 output grads (backward)
@@ -352,14 +357,47 @@ void alloc_outputs(sk_net* n, cudaStream_t st) {
     n->out.resize(L);
     n->xsum.resize(L);
     n->x_ptr.assign(L, nullptr);
+    n->out_ptr.assign(L, nullptr);
     for (size_t i = 0; i < L; ++i) {
         const LayerSpec& l = n->spec.layers[i];
-        size_t bytes = (size_t)std::max(n->out_set[i]->n, 1) * l.c_out * n->es();
-        if (n->out[i].bytes != bytes) n->out[i].alloc(bytes, st);
         if (l.inputs.size() == 2) {
             size_t xb = (size_t)std::max(n->in_set[i]->n, 1) * l.c_in * n->es();
             if (n->xsum[i].bytes != xb) n->xsum[i].alloc(xb, st);
         }
+    }
+    for (size_t i = 0; i < L; ++i) {
+        const LayerSpec& l = n->spec.layers[i];
+        if (n->fuse_into[i] >= 0) {
+            n->out_ptr[i] = n->xsum[n->fuse_into[i]].p;
+            continue;
+        }
+        size_t bytes = (size_t)std::max(n->out_set[i]->n, 1) * l.c_out * n->es();
+        if (n->out[i].bytes != bytes) n->out[i].alloc(bytes, st);
+        n->out_ptr[i] = n->out[i].p;
+    }
+}
+
+// plan skip-add fusion: for L with producers {a, b}, the producer that runs
+// later and whose only consumer is L adds the other one in its epilogue
+void plan_fusion(sk_net* n) {
+    const int L = (int)n->spec.layers.size();
+    std::vector<int> consumers(L, 0);
+    for (const LayerSpec& l : n->spec.layers)
+        for (const std::string& p : l.inputs) ++consumers[n->spec.index(p)];
+    n->fuse_into.assign(L, -1);
+    n->residual_of.assign(L, -1);
+    n->fused_input.assign(L, 0);
+    for (int i = 0; i < L; ++i) {
+        const LayerSpec& l = n->spec.layers[i];
+        if (l.inputs.size() != 2) continue;
+        const int a = n->spec.index(l.inputs[0]), b = n->spec.index(l.inputs[1]);
+        int P = -1, Q = -1;
+        if (consumers[a] == 1 && b < a) P = a, Q = b;
+        else if (consumers[b] == 1 && a < b) P = b, Q = a;
+        if (P < 0 || n->fuse_into[P] >= 0) continue;
+        n->fuse_into[P] = i;
+        n->residual_of[P] = Q;
+        n->fused_input[i] = 1;
     }
 }
 
@@ -392,11 +430,13 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
             validate(channels == l.c_in, l.name + ": input channel mismatch");
             x = feats;
         } else if (l.inputs.size() == 1) {
-            x = n->out[n->spec.index(l.inputs[0])].p;
+            x = n->out_ptr[n->spec.index(l.inputs[0])];
+        } else if (n->fused_input[i]) {
+            x = n->xsum[i].p;  // written by the fused producer's epilogue
         } else {
             const long long cnt = (long long)n->in_set[i]->n * l.c_in;
-            const void* a = n->out[n->spec.index(l.inputs[0])].p;
-            const void* b = n->out[n->spec.index(l.inputs[1])].p;
+            const void* a = n->out_ptr[n->spec.index(l.inputs[0])];
+            const void* b = n->out_ptr[n->spec.index(l.inputs[1])];
             void* y = n->xsum[i].p;
             by_dtype(n->dt, [&](auto tag) {
                 using T = decltype(tag);
@@ -406,8 +446,9 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
             x = y;
         }
         n->x_ptr[i] = x;
+        const void* res = n->fuse_into[i] >= 0 ? n->out_ptr[n->residual_of[i]] : nullptr;
         conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 0, (int)i), n->dt, l.c_in, l.c_out, x,
-                     n->w[i].p, n->out[i].p, false, st, n->wt[i].p);
+                     n->w[i].p, n->out_ptr[i], false, st, n->wt[i].p, res);
         if (ker_ms) (*ker_ms)[n->group_of[i]] += t->stop();
     }
 }
@@ -597,6 +638,7 @@ sk_status sk_net_create(sk_ctx* ctx, int dims, const char* spec_text, sk_dtype d
         }
         n->wgrad_total = off;
         for (int ph = 0; ph < 3; ++ph) n->cfg[ph].assign(n->groups.size(), default_cfg());
+        plan_fusion(n.get());
         SK_CUDA(cudaStreamSynchronize(nullptr));
         *out = n.release();
     });
@@ -662,7 +704,7 @@ sk_status sk_net_forward(sk_net* n, sk_coords* in, const void* d_feats, int chan
         const bool timed = mapping_ms || kernel_ms;
         run_forward(n, in, d_feats, channels, S(stream), timed ? &mp : nullptr,
                     timed ? &kr : nullptr);
-        if (d_out) *d_out = n->out.back().p;
+        if (d_out) *d_out = n->out_ptr.back();
         if (n_out) *n_out = n->out_set.back()->n;
         for (size_t g = 0; g < n->groups.size(); ++g) {
             if (mapping_ms) mapping_ms[g] = mp[g];
@@ -673,8 +715,10 @@ sk_status sk_net_forward(sk_net* n, sk_coords* in, const void* d_feats, int chan
 
 sk_status sk_net_layer_output(sk_net* n, int layer, const void** d_out, int* rows) {
     return nguard([&] {
-        validate(layer >= 0 && layer < (int)n->out.size(), "no forward output for layer");
-        *d_out = n->out[layer].p;
+        validate(layer >= 0 && layer < (int)n->out_ptr.size(), "no forward output for layer");
+        validate(n->fuse_into[layer] < 0,
+                 "layer output is fused into its consumer's skip sum (not materialised)");
+        *d_out = n->out_ptr[layer];
         *rows = n->out_set[layer]->n;
     });
 }
