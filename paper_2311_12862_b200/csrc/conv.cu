@@ -1063,12 +1063,13 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         if (P > 0) {
             const long long rows_pad = P + (long long)m->kd * kTileM;  // >= tiles*128
             DevBuf ga, gc;
-            ga.alloc((size_t)rows_pad * k_total * es, st);
+            ga.alloc((size_t)rows_pad * a.k_total * es, st);
             gc.alloc((size_t)rows_pad * n_total * 4, st);
             const int g = ctx->num_sms * 8;
-            if (dt == SK_F32) gather_rows<float>(x, k_total, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
-            else if (dt == SK_F16) gather_rows<__half>(x, k_total, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
-            else gather_rows<__nv_bfloat16>(x, k_total, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
+            const int kk = a.k_total;  // padded width when the channels were padded
+            if (dt == SK_F32) gather_rows<float>(x, kk, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
+            else if (dt == SK_F16) gather_rows<__half>(x, kk, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
+            else gather_rows<__nv_bfloat16>(x, kk, a.in_pad, tile_ptr + m->kd, ga.p, g, st);
             a.a = ga.p;
             a.n_rows_a = (int)rows_pad;
             a.a_identity = 1;
