@@ -122,6 +122,11 @@ sk_status sk_ctx_create(int device, sk_ctx** out) {
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t thr = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // pre-grow the pool once so steady-state scans never map new memory
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, (size_t)2 << 30, nullptr) == cudaSuccess)
+                cudaFreeAsync(p, nullptr);
+            cudaStreamSynchronize(nullptr);
         }
         *out = c;
     });

@@ -45,11 +45,13 @@ namespace sk {
 
 namespace {
 
-constexpr int kProducerWarps = 4;  // warps 0-3: cp.async gathers (one tile row per thread)
-constexpr int kMmaWarp = 4;        // warp 4: TMEM owner + tcgen05.mma issuer
-constexpr int kIndexWarp = 9;      // warp 9: index/descriptor streamer
-constexpr int kThreadsTC = 320;    // + warps 5-8: epilogue
-constexpr int kIdxRing = 16;       // column steps in flight in the index ring
+constexpr int kItemM = 2 * kTileM;  // rows per work item: two 128-row MMA halves
+constexpr int kProducerWarps = 8;     // warps 0-7: cp.async row gathers
+constexpr int kMmaWarp = 8;           // warp 8: TMEM owner + tcgen05.mma issuer
+constexpr int kEpiWarp0 = 9;          // warps 9-12: epilogue (TMEM lane quadrants 1,2,3,0)
+constexpr int kIndexWarp = 13;        // warp 13: index/descriptor streamer
+constexpr int kThreadsTC = 448;
+constexpr int kIdxRing = 8;           // column steps in flight in the index ring (1 KB each)
 
 struct ConvArgs {
     int mode;  // 0 = OS rows (implicit GEMM), 1 = WS pairs (FOD / GGS GEMM)
@@ -59,7 +61,7 @@ struct ConvArgs {
     const unsigned long long* tile_masks;
     const int* split_begin;
     int ns, rows_pad, n_tiles, n_rows_valid;
-    // WS mode: per-offset pair lists padded to 128-pair tiles (-1 pads)
+    // WS mode: per-offset pair lists padded to 256-pair tiles (-1 pads)
     const int* ws_tile_ptr;
     const int* in_pad;
     const int* out_pad;
@@ -76,18 +78,24 @@ struct ConvArgs {
     int n_ntiles, bn;
     const void* residual;  // optional [n_out][ld_y] T added in the epilogue (out_mode 0)
     int items;        // OS mode item count (WS mode: derived on device)
+    long long* trace; // optional clock64 trace of CTA 0 (SK_TRACE env), 4 slots/step
     int split_only;   // >= 0: only items of this split (deterministic sequencing)
     int offset_only;  // >= 0: WS mode only tiles of this offset
 };
 
+// one work item = 256 rows (OS: 128-row tiles 2*t2 and 2*t2+1 of split s;
+// WS: one 256-pair tile of offset k) x one N-tile
 struct Item {
-    int s, t, nt, k;   // split / tile / n-tile / offset (WS)
+    int s, t2, nt, k;
     int w;             // split width (OS) or 1 (WS)
     int col_begin;     // global offset of column 0
-    long long row0;    // first row: OS tile row within the split, WS padded pair index
+    long long row0;    // first row: OS row within the split, WS padded pair index
+    int halves;        // OS: 128-row tiles present (1 or 2)
     unsigned long long m0, m1;
     int biw0, bw1;
 };
+
+__device__ __forceinline__ int pairs_of(int n_tiles) { return (n_tiles + 1) / 2; }
 
 __device__ __forceinline__ int num_items(const ConvArgs& p) {
     if (p.mode == 0) return p.items;
@@ -99,18 +107,23 @@ __device__ __forceinline__ int num_items(const ConvArgs& p) {
 __device__ Item decode(const ConvArgs& p, int item) {
     Item it;
     if (p.mode == 0) {
-        const int per = p.n_tiles * p.n_ntiles;
+        const int per = pairs_of(p.n_tiles) * p.n_ntiles;
         it.s = p.split_only >= 0 ? p.split_only : item / per;
         const int rem = p.split_only >= 0 ? item : item % per;
-        it.t = rem / p.n_ntiles;
+        it.t2 = rem / p.n_ntiles;
         it.nt = rem % p.n_ntiles;
         it.col_begin = p.split_begin[it.s];
         it.w = p.split_begin[it.s + 1] - it.col_begin;
-        it.row0 = (long long)it.t * kTileM;
+        it.row0 = (long long)it.t2 * kItemM;
         it.k = -1;
-        const unsigned long long* tm = p.tile_masks + ((size_t)it.s * p.n_tiles + it.t) * 2;
+        it.halves = (2 * it.t2 + 1 < p.n_tiles) ? 2 : 1;
+        const unsigned long long* tm = p.tile_masks + ((size_t)it.s * p.n_tiles + 2 * it.t2) * 2;
         it.m0 = tm[0];
         it.m1 = tm[1];
+        if (it.halves == 2) {
+            it.m0 |= tm[2];
+            it.m1 |= tm[3];
+        }
         it.biw0 = it.w < 64 ? it.w : 64;
         it.bw1 = it.w - 64;
     } else {
@@ -125,10 +138,11 @@ __device__ Item decode(const ConvArgs& p, int item) {
         }
         it.k = k;
         it.s = 0;
-        it.t = tile;
+        it.t2 = tile;
         it.w = 1;
         it.col_begin = k;
-        it.row0 = (long long)tile * kTileM;
+        it.row0 = (long long)tile * kItemM;
+        it.halves = 2;
         it.m0 = 1;  // one active "column"
         it.m1 = 0;
         it.biw0 = 1;
@@ -153,23 +167,28 @@ __device__ __forceinline__ int next_col(unsigned long long& m0, unsigned long lo
     return -1;
 }
 
-// 128 A-row indices of one column step (contiguous, 512B aligned)
-__device__ __forceinline__ const int* idx_column(const ConvArgs& p, const Item& it, int j) {
-    if (p.mode == 0)
-        return p.entries + (size_t)p.rows_pad * it.col_begin +
-               ((size_t)it.t * it.w + j) * kTileM;
-    return p.in_pad + it.row0;
+// the 128 A-row indices of half h of a column step (contiguous, 512B aligned);
+// nullptr when the half does not exist
+__device__ __forceinline__ const int* idx_column(const ConvArgs& p, const Item& it, int j, int h) {
+    if (p.mode == 0) {
+        if (h >= it.halves) return nullptr;
+        const long long t = 2 * (long long)it.t2 + h;
+        return p.entries + (size_t)p.rows_pad * it.col_begin + ((size_t)t * it.w + j) * kTileM;
+    }
+    return p.in_pad + it.row0 + h * kTileM;
 }
 
+// row r (0..255) of an item
 __device__ __forceinline__ int a_index(const ConvArgs& p, const Item& it, int r, int j) {
     if (p.mode == 1 && p.a_identity) return (int)(it.row0 + r);
-    return __ldg(idx_column(p, it, j) + r);
+    const int* col = idx_column(p, it, j, r / kTileM);
+    return col ? __ldg(col + (r % kTileM)) : -1;
 }
 
 __device__ __forceinline__ long long out_index(const ConvArgs& p, const Item& it, int r) {
     if (p.mode == 0) {
-        const long long row = it.row0 + r;
-        return __ldg(p.out_row + (size_t)it.s * p.rows_pad + row);
+        if (r / kTileM >= it.halves) return -1;
+        return __ldg(p.out_row + (size_t)it.s * p.rows_pad + it.row0 + r);
     }
     const long long pi = it.row0 + r;
     return p.out_identity ? pi : (long long)__ldg(p.out_pad + pi);
@@ -300,6 +319,56 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
                  : "memory");
 }
 
+// epilogue store of 16 fp32 accumulators (row orow, columns col..col+15)
+template <typename T>
+__device__ __forceinline__ void store16(const ConvArgs& p, long long orow, int col, uint32_t (&v)[16]) {
+    if (p.out_mode == 0) {
+        T* dst = static_cast<T*>(p.y) + (size_t)orow * p.ld_y + col;
+        if (p.residual) {  // fused skip connection: y = conv + residual
+            const uint4* rs = reinterpret_cast<const uint4*>(
+                static_cast<const T*>(p.residual) + (size_t)orow * p.ld_y + col);
+            const uint4 r0 = rs[0], r1 = rs[1];
+            const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float2 f = unpack2(rr[i], (T*)nullptr);
+                v[2 * i] = __float_as_uint(__uint_as_float(v[2 * i]) + f.x);
+                v[2 * i + 1] = __float_as_uint(__uint_as_float(v[2 * i + 1]) + f.y);
+            }
+        }
+        uint4 u0, u1;
+        u0.x = pack2(__uint_as_float(v[0]), __uint_as_float(v[1]), (T*)nullptr);
+        u0.y = pack2(__uint_as_float(v[2]), __uint_as_float(v[3]), (T*)nullptr);
+        u0.z = pack2(__uint_as_float(v[4]), __uint_as_float(v[5]), (T*)nullptr);
+        u0.w = pack2(__uint_as_float(v[6]), __uint_as_float(v[7]), (T*)nullptr);
+        u1.x = pack2(__uint_as_float(v[8]), __uint_as_float(v[9]), (T*)nullptr);
+        u1.y = pack2(__uint_as_float(v[10]), __uint_as_float(v[11]), (T*)nullptr);
+        u1.z = pack2(__uint_as_float(v[12]), __uint_as_float(v[13]), (T*)nullptr);
+        u1.w = pack2(__uint_as_float(v[14]), __uint_as_float(v[15]), (T*)nullptr);
+        reinterpret_cast<uint4*>(dst)[0] = u0;
+        reinterpret_cast<uint4*>(dst)[1] = u1;
+    } else {
+        float* dst = static_cast<float*>(p.y) + (size_t)orow * p.ld_y + col;
+        if (p.out_mode == 2) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                red_add_v4(dst + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                           __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+                float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                       __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+                if (p.out_mode == 3) {
+                    float4 prev = *reinterpret_cast<float4*>(dst + i);
+                    o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
+                }
+                *reinterpret_cast<float4*>(dst + i) = o;
+            }
+        }
+    }
+}
+
 // per index-ring slot: {brow (first B row of this step, -1 = end of work), unused x3}
 struct alignas(16) StepDesc {
     int brow, pad0, pad1, pad2;
@@ -307,34 +376,35 @@ struct alignas(16) StepDesc {
 
 template <typename T, int KC>
 __global__ void __launch_bounds__(kThreadsTC, 1)
-    k_gconv_tc(const ConvArgs p, int stages) {
+    k_gconv_tc(const ConvArgs p, int stages, int acc_bufs) {
     // dynamic smem starts 1024B-aligned (no static smem); checked below since
     // the swizzle atoms and UMMA descriptors rely on it
     extern __shared__ __align__(1024) uint8_t smem[];
     const int BN = p.bn;
-    const uint32_t a_bytes = kTileM * KC * 2;
+    const uint32_t a_half = kTileM * KC * 2;   // one 128-row half
+    const uint32_t a_bytes = 2 * a_half;       // 256-row A tile
     const uint32_t b_bytes = (uint32_t)BN * KC * 2;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* stage_base = smem;
-    int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);  // [R][128]
-    StepDesc* descs = reinterpret_cast<StepDesc*>(idx_ring + kIdxRing * kTileM);  // [R]
+    int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);  // [R][256]
+    StepDesc* descs = reinterpret_cast<StepDesc*>(idx_ring + kIdxRing * kItemM);   // [R]
     uint64_t* bars = reinterpret_cast<uint64_t*>(descs + kIdxRing);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;
     uint64_t* tempty = tfull + 2;
-    uint64_t* ifull = tempty + 2;       // [R]
+    uint64_t* ifull = tempty + 2;         // [R]
     uint64_t* iempty = ifull + kIdxRing;  // [R]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iempty + kIdxRing);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
-    while (ncols < (uint32_t)(2 * BN)) ncols <<= 1;
+    while (ncols < (uint32_t)(acc_bufs * 2 * BN)) ncols <<= 1;
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023) __trap();
         for (int i = 0; i < stages; ++i) {
-            mbar_init(&full[i], kTileM);  // one cp.async noinc arrival per producer thread
+            mbar_init(&full[i], kProducerWarps * 32);  // cp.async noinc arrivals
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -343,7 +413,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         for (int i = 0; i < kIdxRing; ++i) {
             mbar_init(&ifull[i], 1);
-            mbar_init(&iempty[i], kTileM);
+            mbar_init(&iempty[i], kProducerWarps * 32);
         }
         fence_mbar_init();
     }
@@ -358,8 +428,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const T* __restrict__ Bw = static_cast<const T*>(p.b);
 
     if (warp == kIndexWarp) {
-        // ===== index warp: walks the column steps, streams each step's 128 A-row
-        // indices (512B cp.async.bulk) + its B row base into the smem ring =====
+        // ===== index warp: walks the column steps and streams each step's 256
+        // A-row indices (cp.async.bulk, 512B per half) + its B row base =====
         Cursor cur;
         cur.init(p, n_items);
         const bool ident = p.mode == 1 && p.a_identity;
@@ -367,6 +437,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint32_t ph = 0;
         for (;;) {
             mbar_wait(&iempty[slot], ph ^ 1);
+            int* ring = idx_ring + slot * kItemM;
             if (cur.done) {
                 if (lane == 0) {
                     descs[slot].brow = -1;
@@ -376,18 +447,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
             const int kg = cur.it.col_begin + cur.j;
             const int kb = p.mirror ? p.kd - 1 - kg : kg;
+            const int* c0 = ident ? nullptr : idx_column(p, cur.it, cur.j, 0);
+            const int* c1 = ident ? nullptr : idx_column(p, cur.it, cur.j, 1);
             if (ident) {
-                for (int u = lane; u < kTileM; u += 32) idx_ring[slot * kTileM + u] = (int)(cur.it.row0 + u);
-                __syncwarp();
+                for (int u = lane; u < kItemM; u += 32) ring[u] = (int)(cur.it.row0 + u);
+            } else if (!c1) {
+                for (int u = kTileM + lane; u < kItemM; u += 32) ring[u] = -1;  // missing half
             }
+            __syncwarp();
             if (lane == 0) {
                 descs[slot].brow = kb * p.n_total + cur.it.nt * BN;
                 if (ident) {
                     mbar_arrive(&ifull[slot]);
                 } else {
-                    mbar_expect_tx(&ifull[slot], kTileM * 4);
-                    bulk_g2s(smem_u32(idx_ring + slot * kTileM), idx_column(p, cur.it, cur.j),
-                             kTileM * 4, &ifull[slot]);
+                    const uint32_t bytes = (c1 ? 2 : 1) * kTileM * 4;
+                    mbar_expect_tx(&ifull[slot], bytes);
+                    bulk_g2s(smem_u32(ring), c0, kTileM * 4, &ifull[slot]);
+                    if (c1) bulk_g2s(smem_u32(ring + kTileM), c1, kTileM * 4, &ifull[slot]);
                 }
             }
             __syncwarp();
@@ -400,14 +476,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     } else if (warp < kProducerWarps) {
         // ===== producers: CH = KC/8 consecutive threads cover one row's KC
         // channels (16B cp.async each, zero-fill for sentinels / channel tails),
-        // so a warp instruction touches 32/CH whole rows (coalesced lines); the
-        // same mapping loads the B tile. Completion arrives on the stage barrier
-        // asynchronously (cp.async.mbarrier.arrive.noinc). =====
-        constexpr int CH = KC / 8;           // 16B chunks per row
-        constexpr int RSTRIDE = kTileM / CH; // rows between a thread's rows
+        // so a warp instruction touches 32/CH whole rows; the same mapping loads
+        // the B tile. Completion arrives on the stage barrier asynchronously
+        // (cp.async.mbarrier.arrive.noinc). =====
+        constexpr int CH = KC / 8;                            // 16B chunks per row
+        constexpr int PT = kProducerWarps * 32;               // producer threads
+        constexpr int RSTRIDE = PT / CH;                      // rows between a thread's rows
+        constexpr int RPT = kItemM / RSTRIDE;                 // rows per thread
         const int t = threadIdx.x;
         const int q = t % CH, r0 = t / CH;
-        int slot = 0, stage = 0;
+        int slot = 0, stage = 0, tstep = 0;
         uint32_t ph = 0, phase = 0;
         const uint32_t base_u = smem_u32(stage_base);
         const long long b_rows = (long long)p.kd * p.n_total;
@@ -415,21 +493,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             mbar_wait(&ifull[slot], ph);
             const int brow = descs[slot].brow;
             if (brow < 0) break;
-            int ai[CH];
+            int ai[RPT];
 #pragma unroll
-            for (int i = 0; i < CH; ++i) ai[i] = idx_ring[slot * kTileM + r0 + i * RSTRIDE];
+            for (int i = 0; i < RPT; ++i) ai[i] = idx_ring[slot * kItemM + r0 + i * RSTRIDE];
             mbar_arrive(&iempty[slot]);
             for (int c = 0; c < nchunks; ++c) {
+                const long long t_a = p.trace ? clock64() : 0;
                 mbar_wait(&empty[stage], phase ^ 1);
+                if (p.trace && blockIdx.x == 0 && t == 0 && tstep < 2048) {
+                    p.trace[tstep * 4 + 0] = t_a;
+                    p.trace[tstep * 4 + 1] = clock64();
+                }
+                ++tstep;
                 const uint32_t sa = base_u + (uint32_t)stage * stage_bytes;
                 const uint32_t sb = sa + a_bytes;
                 const int col = c * KC + q * 8;
                 const bool col_ok = col < p.k_total;
 #pragma unroll
-                for (int i = 0; i < CH; ++i) {
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = r0 + i * RSTRIDE;
                     const bool ok = ai[i] >= 0 && col_ok;
                     const T* src = A + (size_t)(ok ? ai[i] : 0) * p.k_total + (ok ? col : 0);
-                    cp_async16(sa + swz<KC>(r0 + i * RSTRIDE, q), src, ok ? 16u : 0u);
+                    cp_async16(sa + (uint32_t)(r / kTileM) * a_half + swz<KC>(r % kTileM, q), src,
+                               ok ? 16u : 0u);
                 }
                 for (int n = r0; n < BN; n += RSTRIDE) {
                     const bool ok = (brow + n) < b_rows && col_ok;
@@ -451,16 +537,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // ================= MMA issuer (one thread) =================
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
-        int stage = 0;
+        int stage = 0, tstep = 0;
         uint32_t phase = 0;
         const uint64_t desc0 = kmajor_desc<KC>(smem_u32(stage_base));
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             Item it = decode(p, item);
-            const int acc = local & 1;
-            mbar_wait(&tempty[acc], (uint32_t)(((local >> 1) & 1) ^ 1));
+            const int acc = acc_bufs == 2 ? (local & 1) : 0;
+            const uint32_t aph = acc_bufs == 2 ? (uint32_t)((local >> 1) & 1) : (uint32_t)(local & 1);
+            mbar_wait(&tempty[acc], aph ^ 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
+            const uint32_t d0 = tmem + (uint32_t)(acc * 2 * BN);  // half 0; half 1 at +BN
             unsigned long long m0 = it.m0, m1 = it.m1;
             uint32_t accumulate = 0;
             for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
@@ -468,14 +555,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int c = 0; c < nchunks; ++c) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (p.trace && blockIdx.x == 0 && lane == 0 && tstep < 2048)
+                        p.trace[tstep * 4 + 2] = clock64();
+                    ++tstep;
                     if (lane == 0) {
-                        // descriptor start address advances in 16B units
+                        // descriptor start addresses advance in 16B units
                         const uint64_t da = desc0 + ((uint64_t)stage * stage_bytes >> 4);
+                        const uint64_t da1 = da + (a_half >> 4);
                         const uint64_t db = da + (a_bytes >> 4);
 #pragma unroll
                         for (int kk = 0; kk < KC / 16; ++kk) {
-                            tc_mma_f16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2),
-                                       idesc, accumulate);
+                            tc_mma_f16(d0, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                                       accumulate);
+                            tc_mma_f16(d0 + (uint32_t)BN, da1 + (uint64_t)(kk * 2),
+                                       db + (uint64_t)(kk * 2), idesc, accumulate);
                             accumulate = 1;
                         }
                         tc_commit(&empty[stage]);
@@ -490,75 +583,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (lane == 0) tc_commit(&tfull[acc]);
             __syncwarp();
         }
-    } else {
-        // ================= epilogue (warps 5-8 -> TMEM lane quadrants 1,2,3,0) =================
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+        // ====== epilogue: thread owns TMEM lane (quad*32+lane) = rows r, 128+r ======
         const int quad = warp & 3;
-        const int r = quad * 32 + lane;
+        const int lr = quad * 32 + lane;
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             Item it = decode(p, item);
-            const long long orow = out_index(p, it, r);  // issued before the wait
-            const int acc = local & 1;
-            mbar_wait(&tfull[acc], (uint32_t)((local >> 1) & 1));
+            long long orow[2];
+            orow[0] = out_index(p, it, lr);  // issued before the wait
+            orow[1] = out_index(p, it, kTileM + lr);
+            const int acc = acc_bufs == 2 ? (local & 1) : 0;
+            const uint32_t aph = acc_bufs == 2 ? (uint32_t)((local >> 1) & 1) : (uint32_t)(local & 1);
+            mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             const bool empty_tile = (it.m0 | it.m1) == 0;
             const int n0 = it.nt * BN;
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-                uint32_t v[16];
-                if (!empty_tile) {
-                    tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
-                    tmem_ld_wait();
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] = 0;
-                }
-                const int col = n0 + c0;
-                if (orow < 0 || col >= p.n_total) continue;
-                if (p.out_mode == 0) {
-                    T* dst = static_cast<T*>(p.y) + (size_t)orow * p.ld_y + col;
-                    if (p.residual) {  // fused skip connection: y = conv + residual
-                        const uint4* rs = reinterpret_cast<const uint4*>(
-                            static_cast<const T*>(p.residual) + (size_t)orow * p.ld_y + col);
-                        const uint4 r0 = rs[0], r1 = rs[1];
-                        const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            float2 f = unpack2(rr[i], (T*)nullptr);
-                            v[2 * i] = __float_as_uint(__uint_as_float(v[2 * i]) + f.x);
-                            v[2 * i + 1] = __float_as_uint(__uint_as_float(v[2 * i + 1]) + f.y);
-                        }
-                    }
-                    uint4 u0, u1;
-                    u0.x = pack2(__uint_as_float(v[0]), __uint_as_float(v[1]), (T*)nullptr);
-                    u0.y = pack2(__uint_as_float(v[2]), __uint_as_float(v[3]), (T*)nullptr);
-                    u0.z = pack2(__uint_as_float(v[4]), __uint_as_float(v[5]), (T*)nullptr);
-                    u0.w = pack2(__uint_as_float(v[6]), __uint_as_float(v[7]), (T*)nullptr);
-                    u1.x = pack2(__uint_as_float(v[8]), __uint_as_float(v[9]), (T*)nullptr);
-                    u1.y = pack2(__uint_as_float(v[10]), __uint_as_float(v[11]), (T*)nullptr);
-                    u1.z = pack2(__uint_as_float(v[12]), __uint_as_float(v[13]), (T*)nullptr);
-                    u1.w = pack2(__uint_as_float(v[14]), __uint_as_float(v[15]), (T*)nullptr);
-                    reinterpret_cast<uint4*>(dst)[0] = u0;
-                    reinterpret_cast<uint4*>(dst)[1] = u1;
-                } else {
-                    float* dst = static_cast<float*>(p.y) + (size_t)orow * p.ld_y + col;
-                    if (p.out_mode == 2) {
-#pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            red_add_v4(dst + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                       __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                for (int c0 = 0; c0 < BN; c0 += 16) {
+                    uint32_t v[16];
+                    if (!empty_tile) {
+                        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) +
+                                      (uint32_t)(acc * 2 * BN + h * BN + c0),
+                                  v);
+                        tmem_ld_wait();
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 16; i += 4) {
-                            float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                   __uint_as_float(v[i + 2]),
-                                                   __uint_as_float(v[i + 3]));
-                            if (p.out_mode == 3) {
-                                float4 prev = *reinterpret_cast<float4*>(dst + i);
-                                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
-                            }
-                            *reinterpret_cast<float4*>(dst + i) = o;
-                        }
+                        for (int i = 0; i < 16; ++i) v[i] = 0;
                     }
+                    const int col = n0 + c0;
+                    if (orow[h] < 0 || col >= p.n_total) continue;
+                    store16<T>(p, orow[h], col, v);
                 }
             }
             tc_fence_before();
@@ -602,7 +658,8 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
     const T* __restrict__ A = static_cast<const T*>(p.a);
     const T* __restrict__ Bw = static_cast<const T*>(p.b);
     const int n_items = num_items(p);
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int iter = blockIdx.x; iter < 2 * n_items; iter += gridDim.x) {
+        const int item = iter >> 1, h = iter & 1;  // 128-row half h of a 256-row item
         Item it = decode(p, item);
         const int n0 = it.nt * kSimtN;
         float acc[8][4];
@@ -616,7 +673,7 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
             const int kg = it.col_begin + j;
             const int kb = p.mirror ? p.kd - 1 - kg : kg;
             __syncthreads();
-            if (tid < kTileM) aidx[tid] = a_index(p, it, tid, j);
+            if (tid < kTileM) aidx[tid] = a_index(p, it, h * kTileM + tid, j);
             __syncthreads();
             for (int c0 = 0; c0 < p.k_total; c0 += kSimtK) {
                 for (int i = tid; i < kTileM * kSimtK; i += 256) {
@@ -649,7 +706,7 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const long long orow = out_index(p, it, tr * 8 + i);
+            const long long orow = out_index(p, it, h * kTileM + tr * 8 + i);
             if (orow < 0) continue;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
@@ -706,7 +763,7 @@ __global__ void k_pad_cols(const T* __restrict__ src, long long rows, int k, int
 template <typename T>
 __global__ void k_gather_rows(const T* __restrict__ x, int c, const int* __restrict__ idx,
                               const int* __restrict__ tile_total, T* __restrict__ buf) {
-    const long long nelem = (long long)(*tile_total) * kTileM * c;
+    const long long nelem = (long long)(*tile_total) * kItemM * c;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
          i += (long long)gridDim.x * blockDim.x) {
         long long pr = i / c;
@@ -722,7 +779,7 @@ __global__ void k_gather_rows(const T* __restrict__ x, int c, const int* __restr
 __global__ void k_scatter_add(const float* __restrict__ buf, int c, const int* __restrict__ idx,
                               const int* __restrict__ tile_lo, const int* __restrict__ tile_hi,
                               float* __restrict__ y, int deterministic) {
-    const long long a = (long long)(*tile_lo) * kTileM, b = (long long)(*tile_hi) * kTileM;
+    const long long a = (long long)(*tile_lo) * kItemM, b = (long long)(*tile_hi) * kItemM;
     const long long nelem = (b - a) * c;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
          i += (long long)gridDim.x * blockDim.x) {
@@ -823,10 +880,11 @@ CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, i
 template <typename T, int KC>
 void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
     const int bn = a.bn;
-    const size_t stage_bytes = (size_t)kTileM * KC * 2 + (size_t)bn * KC * 2;
+    const size_t stage_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
     int stages = (int)std::min<size_t>(10, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
-    const size_t smem = stages * stage_bytes + kIdxRing * (kTileM * 4 + 16) +
+    const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
+    const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
                         (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
     static size_t configured = 0;  // per template instantiation
     if (smem > configured) {
@@ -834,7 +892,7 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages);
+    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages, acc_bufs);
     SK_LAUNCH_CHECK();
 }
 
@@ -863,7 +921,14 @@ void pick_n_tiling(int n_total, int cta_n, bool tc, int& bn, int& n_nt) {
 }
 
 void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t st) {
-    const ConvArgs& a = a_in;
+    ConvArgs a = a_in;
+    static const bool trace = getenv("SK_TRACE") != nullptr;
+    DevBuf tbuf;
+    if (trace) {
+        tbuf.alloc(2048 * 4 * 8, st);
+        SK_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, st));
+        a.trace = tbuf.as<long long>();
+    }
     const bool tc = tc_ok(dt, a.k_total, a.n_total);
     int grid;
     if (a.mode == 0) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
@@ -876,6 +941,26 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
         else if (dt == SK_F16) k_gconv_simt<__half><<<grid, 256, 0, st>>>(a);
         else k_gconv_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(a);
         SK_LAUNCH_CHECK();
+    }
+    if (trace && tc) {
+        std::vector<long long> h(2048 * 4);
+        SK_CUDA(cudaMemcpyAsync(h.data(), tbuf.p, tbuf.bytes, cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        const long long t0 = h[0];
+        int n = 0;
+        while (n < 2048 && h[n * 4 + 1]) ++n;
+        double issue_gap = 0, land = 0, wait_empty = 0, wait_idx = 0;
+        for (int i = 0; i < n; ++i) wait_idx += h[i * 4 + 3];
+        fprintf(stderr, "idx-ring wait %.0f cyc/step\n", n ? wait_idx / n : 0);
+        for (int i = 1; i < n; ++i) issue_gap += h[i * 4 + 1] - h[(i - 1) * 4 + 1];
+        for (int i = 0; i < n; ++i) {
+            land += h[i * 4 + 2] - h[i * 4 + 1];
+            wait_empty += h[i * 4 + 1] - h[i * 4 + 0];
+        }
+        fprintf(stderr, "trace k=%d n=%d bn=%d grid=%d steps(cta0)=%d: issue_gap %.0f cyc, "
+                "issue->mma %.0f cyc, empty_wait %.0f cyc, total %lld cyc\n", a.k_total,
+                a.n_total, a.bn, grid, n, n > 1 ? issue_gap / (n - 1) : 0, n ? land / n : 0,
+                n ? wait_empty / n : 0, n ? h[(n - 1) * 4 + 2] - t0 : 0);
     }
 }
 
@@ -996,8 +1081,9 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         a.rows_pad = pr->rows_pad;
         a.n_tiles = pr->rows_pad / kTileM;
         a.n_rows_valid = m->n_out;
+        const int pairs = (a.n_tiles + 1) / 2;  // 256-row items
         if (pr->num_splits == 1) {
-            a.items = a.n_tiles * a.n_ntiles;
+            a.items = pairs * a.n_ntiles;
             a.y = y;
             a.residual = residual;
             a.out_mode = dt == SK_F32 ? 1 : 0;
@@ -1015,14 +1101,14 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
                 // splits accumulate in order so partial sums telescope
                 // (implicit_gemm_impl deterministic branch, exec.cpp:240-246)
                 a.out_mode = 3;
-                a.items = a.n_tiles * a.n_ntiles;
+                a.items = pairs * a.n_ntiles;
                 for (int s = 0; s < pr->num_splits; ++s) {
                     a.split_only = s;
                     launch_gconv(ctx, dt, a, st);
                 }
             } else {
                 a.out_mode = 2;
-                a.items = pr->num_splits * a.n_tiles * a.n_ntiles;
+                a.items = pr->num_splits * pairs * a.n_ntiles;
                 launch_gconv(ctx, dt, a, st);
             }
             if (dt != SK_F32 || residual) convert_from_f32(dt, yf, y_elems, y, residual, st);
@@ -1061,7 +1147,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         // gather -> GEMM -> scatter-add (exec.cpp:117-158)
         const int64_t P = kmap_total_pairs(m, st);
         if (P > 0) {
-            const long long rows_pad = P + (long long)m->kd * kTileM;  // >= tiles*128
+            const long long rows_pad = P + (long long)m->kd * kItemM;  // >= tiles*256
             DevBuf ga, gc;
             ga.alloc((size_t)rows_pad * a.k_total * es, st);
             gc.alloc((size_t)rows_pad * n_total * 4, st);

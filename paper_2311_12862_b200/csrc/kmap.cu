@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(1024) k_ws_scan(const int* __restrict__ blk_co
             ptr[k] = acc;
             tile_ptr[k] = tacc;
             acc += tot[k];
-            tacc += (int)((tot[k] + kTileM - 1) / kTileM);
+            tacc += (int)((tot[k] + kTileWS - 1) / kTileWS);
         }
         ptr[kd] = acc;
         tile_ptr[kd] = tacc;
@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(kQB) k_ws_scatter(const int* __restrict__ os, 
             long long pos = ptr[k] + rel;
             ws_in[pos] = j;
             ws_out[pos] = row;
-            // per-offset lists padded to 128-pair tiles (-1 pads) for FOD/GGS tiles
-            long long pp = (long long)tile_ptr[k] * kTileM + rel;
+            // per-offset lists padded to 256-pair tiles (-1 pads) for FOD/GGS tiles
+            long long pp = (long long)tile_ptr[k] * kTileWS + rel;
             in_pad[pp] = j;
             out_pad[pp] = row;
         }
@@ -604,7 +604,7 @@ void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
     size_t cap = (size_t)std::max<int64_t>(1, (int64_t)m->n_out * m->kd);
     m->ws_in.alloc(cap * 4, st);
     m->ws_out.alloc(cap * 4, st);
-    const size_t cap_pad = cap + (size_t)m->kd * kTileM;
+    const size_t cap_pad = cap + (size_t)m->kd * kTileWS;
     m->ws_in_pad.alloc(cap_pad * 4, st);
     m->ws_out_pad.alloc(cap_pad * 4, st);
     SK_CUDA(cudaMemsetAsync(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st));

@@ -83,6 +83,7 @@ struct sk_kmap : sk::Refcounted {
 namespace sk {
 
 constexpr int kTileM = 128;  // MMA M rows per tile = pad multiple
+constexpr int kTileWS = 256; // pairs per FOD/GGS tile (padded per offset)
 
 // kmap.cu
 void coords_build_table(sk_coords* c, cudaStream_t st);
