@@ -47,6 +47,7 @@ namespace {
 
 constexpr int kItemM = 2 * kTileM;  // rows per work item: two 128-row MMA halves
 constexpr int kProducerWarps = 8;     // warps 0-7: cp.async row gathers
+constexpr int kTmaWarps = 4;          // warps 0-3: TMA gather4 producers (TMA variant)
 constexpr int kMmaWarp = 8;           // warp 8: TMEM owner + tcgen05.mma issuer
 constexpr int kEpiWarp0 = 9;          // warps 9-12: epilogue (TMEM lane quadrants 1,2,3,0)
 constexpr int kIndexWarp = 13;        // warp 13: index/descriptor streamer
@@ -286,6 +287,26 @@ __device__ __forceinline__ void tma_tile2d(uint32_t dst, const CUtensorMap* tm, 
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// whole-warp (uniform) callers: one elected lane issues
+__device__ __forceinline__ void tma_gather4_elect(uint32_t dst, const CUtensorMap* tm, int col,
+                                                  int r0, int r1, int r2, int r3, uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n"
+        "@P cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_tile2d_elect(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                                 uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n"
+        "@P cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
     asm volatile(
@@ -374,9 +395,15 @@ struct alignas(16) StepDesc {
     int brow, pad0, pad1, pad2;
 };
 
-template <typename T, int KC>
+// USE_TMA = true: producer warps 0-3 issue TMA tile::gather4 (4 rows each,
+// sentinel rows -> out-of-bounds coordinate -> zero fill without L2 traffic)
+// from uniform warp code (shuffled operands, elect.sync inside the asm), and
+// warp 0 loads B with one 2D TMA tile. USE_TMA = false: warps 0-7 gather with
+// 16 B cp.async (reference path, kept for A/B measurement).
+template <typename T, int KC, bool USE_TMA>
 __global__ void __launch_bounds__(kThreadsTC, 1)
-    k_gconv_tc(const ConvArgs p, int stages, int acc_bufs) {
+    k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+               const ConvArgs p, int stages, int acc_bufs) {
     // dynamic smem starts 1024B-aligned (no static smem); checked below since
     // the swizzle atoms and UMMA descriptors rely on it
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -404,7 +431,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023) __trap();
         for (int i = 0; i < stages; ++i) {
-            mbar_init(&full[i], kProducerWarps * 32);  // cp.async noinc arrivals
+            // cp.async: one noinc arrival per producer thread; TMA: one
+            // expect_tx arrival per gathering warp
+            mbar_init(&full[i], USE_TMA ? kTmaWarps : kProducerWarps * 32);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -413,9 +442,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         for (int i = 0; i < kIdxRing; ++i) {
             mbar_init(&ifull[i], 1);
-            mbar_init(&iempty[i], kProducerWarps * 32);
+            mbar_init(&iempty[i], USE_TMA ? kTmaWarps : kProducerWarps * 32);
         }
         fence_mbar_init();
+        if (USE_TMA) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
+        }
     }
     if (warp == kMmaWarp) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
@@ -473,7 +506,54 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 ph ^= 1;
             }
         }
-    } else if (warp < kProducerWarps) {
+    } else if (USE_TMA && warp < kTmaWarps) {
+        // ===== TMA producers: warp w owns rows [64w, 64w+64) = 16 gather4 per
+        // step; lanes 0-15 hold the 4-row index groups, shuffled to the whole
+        // warp so the TMA operands are warp-uniform =====
+        constexpr int GPW = kItemM / 4 / kTmaWarps;  // gathers per warp per step (16)
+        int slot = 0, stage = 0;
+        uint32_t ph = 0, phase = 0;
+        const uint32_t base_u = smem_u32(stage_base);
+        const uint32_t my_bytes = GPW * 4 * KC * 2 + (warp == 0 ? b_bytes : 0);
+        for (;;) {
+            mbar_wait(&ifull[slot], ph);
+            const int brow = descs[slot].brow;
+            if (brow < 0) break;
+            int4 g4 = make_int4(-1, -1, -1, -1);
+            if (lane < GPW) g4 = reinterpret_cast<const int4*>(idx_ring + slot * kItemM)[warp * GPW + lane];
+            g4.x = g4.x < 0 ? p.n_rows_a : g4.x;  // sentinel -> out of bounds -> zeros
+            g4.y = g4.y < 0 ? p.n_rows_a : g4.y;
+            g4.z = g4.z < 0 ? p.n_rows_a : g4.z;
+            g4.w = g4.w < 0 ? p.n_rows_a : g4.w;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&iempty[slot]);
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t sa = base_u + (uint32_t)stage * stage_bytes;
+                if (lane == 0) mbar_expect_tx(&full[stage], my_bytes);
+                __syncwarp();
+                if (warp == 0) tma_tile2d_elect(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+#pragma unroll
+                for (int g = 0; g < GPW; ++g) {
+                    const int r = (warp * GPW + g) * 4;  // first of the 4 rows
+                    const uint32_t dst = sa + (uint32_t)(r / kTileM) * a_half +
+                                         (uint32_t)(r % kTileM) * KC * 2;
+                    tma_gather4_elect(dst, &tm_a, c * KC, __shfl_sync(0xffffffffu, g4.x, g),
+                                      __shfl_sync(0xffffffffu, g4.y, g),
+                                      __shfl_sync(0xffffffffu, g4.z, g),
+                                      __shfl_sync(0xffffffffu, g4.w, g), &full[stage]);
+                }
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (++slot == kIdxRing) {
+                slot = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (!USE_TMA && warp < kProducerWarps) {
         // ===== producers: CH = KC/8 consecutive threads cover one row's KC
         // channels (16B cp.async each, zero-fill for sentinels / channel tails),
         // so a warp instruction touches 32/CH whole rows; the same mapping loads
@@ -878,7 +958,11 @@ CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, i
 }
 
 template <typename T, int KC>
-void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
+void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
+    static const bool use_tma = [] {
+        const char* e = getenv("SK_GATHER");
+        return !(e && std::string(e) == "cpasync");
+    }();
     const int bn = a.bn;
     const size_t stage_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
     int stages = (int)std::min<size_t>(10, (200 * 1024) / stage_bytes);
@@ -886,13 +970,22 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype, int grid, cudaStream_t st) {
     const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
                         (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
-    static size_t configured = 0;  // per template instantiation
-    if (smem > configured) {
-        SK_CUDA(cudaFuncSetAttribute(k_gconv_tc<T, KC>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
+    CUtensorMap ta, tb;
+    if (use_tma) {
+        ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, 1);
+        tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
+    } else {
+        memset(&ta, 0, sizeof(ta));
+        memset(&tb, 0, sizeof(tb));
     }
-    k_gconv_tc<T, KC><<<grid, kThreadsTC, smem, st>>>(a, stages, acc_bufs);
+    auto kern = use_tma ? k_gconv_tc<T, KC, true> : k_gconv_tc<T, KC, false>;
+    static size_t configured[2] = {0, 0};  // per template instantiation
+    if (smem > configured[use_tma]) {
+        SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        configured[use_tma] = smem;
+    }
+    kern<<<grid, kThreadsTC, smem, st>>>(ta, tb, a, stages, acc_bufs);
     SK_LAUNCH_CHECK();
 }
 
