@@ -959,9 +959,11 @@ CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, i
 
 template <typename T, int KC>
 void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
+    // cp.async measured faster than TMA gather4 for C <= 128 on B200
+    // (tools/layer_bench.py, profiles/r01_gather_paths.md); SK_GATHER=tma selects TMA
     static const bool use_tma = [] {
         const char* e = getenv("SK_GATHER");
-        return !(e && std::string(e) == "cpasync");
+        return e && std::string(e) == "tma";
     }();
     const int bn = a.bn;
     const size_t stage_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
