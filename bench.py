@@ -147,6 +147,9 @@ def main():
     ap.add_argument("--impl", default="sk200", choices=["sk200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--splits", type=int, default=1)
+    ap.add_argument("--workload", default="infer", choices=["infer", "train"],
+                    help="infer: configs[1] MinkUNet inference (default); train: configs[3] "
+                         "mixed-precision DP training step, global batch 8 scans")
     ap.add_argument("--no-tune", action="store_true",
                     help="skip the per-group autotuner; use implicit GEMM --splits everywhere")
     args = ap.parse_args()
@@ -156,6 +159,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.workload == "train":
+        return run_train(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -306,6 +311,78 @@ def main():
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_train(args, rank, world, local):
+    """configs[3]: MinkUNet mixed-precision training step (fwd + dgrad + wgrad),
+    global batch 8 scans dealt scene-by-scene to the ranks, bucketed NCCL
+    all-reduce of fp32 weight gradients overlapping the backward (strong
+    scaling: the global batch is fixed)."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2311_12862_b200 import _lib, sparse as sk
+    from paper_2311_12862_b200.dist import DataParallelTrainer, shard_scenes
+    from paper_2311_12862_b200.models import minkunet18
+    from paper_2311_12862_b200.network import NetworkRunner
+    B = 8
+    batches = [make_scans(B, 100 * s + 1) for s in range(args.warmup + args.steps)]
+    net = NetworkRunner(minkunet18(), dtype=torch.float16, weight_seed=3)
+    net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large()))
+    tr = DataParallelTrainer(net, lr=1e-3, momentum=0.9)
+    rng = np.random.default_rng(rank)
+    prepared = []
+    for scans in batches:
+        mine = shard_scenes([len(c) for c in scans], rank, world)
+        prepared.append([(torch.from_numpy(scans[i]).cuda(),
+                          torch.from_numpy(rng.standard_normal((len(scans[i]), 4))
+                                           .astype(np.float16)).cuda(),
+                          torch.from_numpy(rng.standard_normal((len(scans[i]), 96))
+                                           .astype(np.float16)).cuda()) for i in mine])
+
+    def step(i):
+        scenes = [(sk.CoordSet.create(c), x, t) for c, x, t in prepared[i]]
+        return tr.train_step(scenes, B)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.lib().sk_kernel_launches()
+    clocks = ClockSampler(local)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(args.warmup, args.warmup + args.steps):
+        step(i)
+    b.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t_ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    value = B * args.steps / (t_ms / 1e3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "scans/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic",
+            "config": {"workload": "MinkUNet-18 mixed-precision training step (fwd + dgrad + "
+                                   "wgrad, SGD), global batch 8 synthetic ~128k-voxel scans, "
+                                   "scene-sharded DP with bucketed NCCL all-reduce",
+                       "global_batch": B, "parallelism": f"dp{world}",
+                       "params": int(net.num_params)},
+            "gpu_launches": int(_lib.lib().sk_kernel_launches() - launches0),
+            "clocks": clk}), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

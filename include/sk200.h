@@ -220,9 +220,10 @@ int64_t sk_net_map_builds(const sk_net* net);
 sk_status sk_net_group_traffic(sk_net* net, int group, const sk_dataflow_cfg* cfg, void* stream,
                                double* bytes);
 /* Chained backward of the last forward over layers [layer_lo, layer_hi]
- * (call with decreasing ranges to overlap gradient all-reduce buckets). */
+ * (call with decreasing ranges to overlap gradient all-reduce buckets).
+ * accumulate != 0 adds into d_wgrad_flat (several scans per rank). */
 sk_status sk_net_backward(sk_net* net, const void* d_grad_out, float* d_wgrad_flat, int layer_hi,
-                          int layer_lo, void* stream);
+                          int layer_lo, int accumulate, void* stream);
 /* tune_inference / tune_training (tuner.cpp:134-220): training 0 =
  * inference, 1 = workload_pattern, 2 = sparse_mapping. Log entries are
  * {pass, group, space index, ms}. Leaves the winning configs set. */

@@ -129,7 +129,7 @@ def lib():
         "sk_net_map_builds": ([vp], C.c_int64),
         "sk_net_group_traffic": ([vp, C.c_int, C.POINTER(DataflowCfg), vp,
                                   C.POINTER(C.c_double)], C.c_int),
-        "sk_net_backward": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
+        "sk_net_backward": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, vp], C.c_int),
         "sk_net_tune": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp,
                          C.POINTER(C.c_double), vp, C.c_int, C.POINTER(C.c_int)], C.c_int),
         "sk_tune_space_size": ([], C.c_int),

@@ -1286,11 +1286,12 @@ void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, 
 }
 
 void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
-                int c_out, const void* x, const void* dy, float* dw, cudaStream_t st) {
+                int c_out, const void* x, const void* dy, float* dw, cudaStream_t st,
+                bool accumulate) {
     (void)cfg;  // conv_wgrad ignores cfg.kind in the reference (exec.cpp:398-414)
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     kmap_ensure_ws(m, st);
-    SK_CUDA(cudaMemsetAsync(dw, 0, (size_t)m->kd * c_in * c_out * 4, st));
+    if (!accumulate) SK_CUDA(cudaMemsetAsync(dw, 0, (size_t)m->kd * c_in * c_out * 4, st));
     if (m->n_out == 0 || m->n_in == 0) return;
     // pair chunking: enough blocks to fill the machine; deterministic mode
     // uses one chunk per offset (no cross-block float atomics on one cell)

@@ -538,7 +538,7 @@ double modeled_group_traffic(sk_net* n, int g, const sk_dataflow_cfg& cfg, cudaS
 
 // chained backward over layers [lo, hi] in reverse order: gout[i] (fp32) holds
 // dL/d out_i; writes dW_i into the flat buffer and pushes dL/dx into producers
-void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, cudaStream_t st) {
+void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate, cudaStream_t st) {
     const size_t L = n->spec.layers.size();
     size_t max_out = 0, max_in = 0;
     for (size_t i = 0; i < L; ++i) {
@@ -559,7 +559,7 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, cudaStream_t st)
         SK_LAUNCH_CHECK();
         const int g = n->group_of[i];
         conv_wgrad(n->ctx, n->exec_map[i], layer_cfg(n, 2, i), n->dt, l.c_in, l.c_out, n->x_ptr[i],
-                   dy.p, wgrad_flat + n->wgrad_off[i], st);
+                   dy.p, wgrad_flat + n->wgrad_off[i], st, accumulate);
         if (l.inputs.empty()) continue;  // no gradient w.r.t. the network input
         conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, i), n->dt, l.c_in, l.c_out, dy.p,
                      n->w[i].p, dx.p, true, st);
@@ -746,7 +746,7 @@ sk_status sk_net_group_traffic(sk_net* n, int group, const sk_dataflow_cfg* cfg,
 // = last layer) seeds the gradient buffers. wgrad_flat: fp32, layout from
 // sk_net_layer_info(... wgrad_offset).
 sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, int layer_hi,
-                          int layer_lo, void* stream) {
+                          int layer_lo, int accumulate, void* stream) {
     return nguard([&] {
         const int L = (int)n->spec.layers.size();
         validate(layer_hi < L && layer_lo >= 0 && layer_lo <= layer_hi, "bad layer range");
@@ -767,7 +767,7 @@ sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, 
             });
             SK_LAUNCH_CHECK();
         }
-        run_backward(n, layer_hi, layer_lo, wgrad_flat, st);
+        run_backward(n, layer_hi, layer_lo, wgrad_flat, accumulate != 0, st);
     });
 }
 

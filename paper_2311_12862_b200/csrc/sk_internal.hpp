@@ -105,8 +105,10 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype 
 // W [kd][c_in][c_out] -> W^T [kd][c_out][c_in]
 void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, void* wt,
                        cudaStream_t st);
+// accumulate: dw += (instead of dw =) the weight gradient
 void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
-                int c_out, const void* x, const void* dy, float* dw, cudaStream_t st);
+                int c_out, const void* x, const void* dy, float* dw, cudaStream_t st,
+                bool accumulate = false);
 
 uint64_t next_coord_set_id();
 void set_last_error(const std::string& m);

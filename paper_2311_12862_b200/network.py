@@ -171,13 +171,20 @@ class NetworkRunner:
         return b.value
 
     def backward(self, grad_out: torch.Tensor, wgrad: torch.Tensor, layer_hi: int | None = None,
-                 layer_lo: int = 0) -> None:
-        """Chained backward of the last forward into the flat fp32 `wgrad`."""
+                 layer_lo: int = 0, accumulate: bool = False) -> None:
+        """Chained backward of the last forward into the flat fp32 `wgrad`
+        (layers [layer_lo, layer_hi]; the first call must start at the last layer)."""
         hi = self.num_layers - 1 if layer_hi is None else layer_hi
         g = grad_out.to(device="cuda", dtype=self.dtype).contiguous()
         assert wgrad.dtype == torch.float32 and wgrad.numel() == self.num_params
-        check(lib().sk_net_backward(self.ptr, _ptr(g), _ptr(wgrad), hi, layer_lo, _stream()))
+        check(lib().sk_net_backward(self.ptr, _ptr(g), _ptr(wgrad), hi, layer_lo, int(accumulate),
+                                    _stream()))
         self._grad_keep = g
+
+    def weights_updated(self) -> None:
+        """Mark the device weights as changed (e.g. written through weight(i))."""
+        p = C.c_void_p()
+        check(lib().sk_net_weight_ptr(self.ptr, 0, C.byref(p)))
 
     def weight_grad(self, wgrad: torch.Tensor, i: int) -> torch.Tensor:
         kd, ci, co, off = self.layer_shapes[i]
