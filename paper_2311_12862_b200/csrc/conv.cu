@@ -918,6 +918,218 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
     }
 }
 
+// ---------------------------------------------------------------------------
+// tcgen05 wgrad: dW_k[ci][co] = sum_p x[in_p][ci] * dy[out_p][co] (exec.cpp:259-279)
+// GEMM with M = C_in (128-channel tiles), N = C_out tile, K = the pairs of one
+// offset. Both operands are gathered rows, i.e. MN-major: each pair's row is
+// 128 B of channels, 8 pairs form a 1024 B SW128 atom (SBO), 64-channel
+// blocks are LBO = 8 KB apart. CTA b owns a contiguous range of virtual tiles
+// (mn-tile, 256-pair tile); consecutive tiles of the same (mn, offset)
+// accumulate in TMEM and are flushed with fp32 red.add when the run ends.
+constexpr int kWgK = 64;            // pairs per k-step
+constexpr int kWgThreads = 288;     // warps 0-3 producers, 4 MMA, 5-8 epilogue
+constexpr int kWgStepsPerTile = kTileWS / kWgK;
+
+struct WgArgs {
+    const void* x;
+    const void* dy;
+    int c_in, c_out, kd;
+    const int* tile_ptr;  // [kd+1], 256-pair tiles per offset
+    const int* in_pad;
+    const int* out_pad;
+    float* dw;
+    int m_tiles, n_tiles, bn, nblk_b;
+};
+
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t saddr) {
+    constexpr uint64_t lbo = 8192 >> 4, sbo = 1024 >> 4;
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | (lbo << 16) | (sbo << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+__device__ __forceinline__ int wg_offset_of(const int* tp, int kd, int t) {
+    int k = 0;
+    while (k + 1 <= kd && tp[k + 1] <= t) ++k;
+    return k;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int stages) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t a_bytes = 2 * 8192;                   // 128 channels x 64 pairs
+    const uint32_t b_bytes = (uint32_t)p.nblk_b * 8192;  // bn channels (64-blocks) x 64 pairs
+    const uint32_t stage_bytes = a_bytes + b_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + stages;
+    uint64_t* tfull = bars + 2 * stages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int BN = p.bn;
+    uint32_t ncols = 32;
+    while (ncols < (uint32_t)(2 * BN)) ncols <<= 1;
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023) __trap();
+        for (int i = 0; i < stages; ++i) {
+            mbar_init(&full[i], 128);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 4) tmem_alloc(tmem_slot, ncols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const long long NT = p.tile_ptr[p.kd];  // 256-pair tiles
+    const long long V = NT * p.m_tiles * p.n_tiles;
+    const long long v0 = V * blockIdx.x / gridDim.x, v1 = V * (blockIdx.x + 1) / gridDim.x;
+
+    if (warp < 4) {
+        // producers: threads 0-63 gather x rows, 64-127 dy rows (pair t % 64),
+        // 16 B cp.async per 8 channels; indices prefetched 8 steps ahead
+        const int t = threadIdx.x;
+        const bool is_x = t < 64;
+        const int kk = t & 63;
+        const int C = is_x ? p.c_in : p.c_out;
+        const T* src = static_cast<const T*>(is_x ? p.x : p.dy);
+        const int* idx = is_x ? p.in_pad : p.out_pad;
+        const long long nsteps = (v1 - v0) * kWgStepsPerTile;
+        auto pair_of = [&](long long g) -> long long {
+            const long long v = v0 + g / kWgStepsPerTile;
+            return (v % NT) * kTileWS + (g % kWgStepsPerTile) * kWgK + kk;
+        };
+        int pre[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pre[i] = i < nsteps ? __ldg(idx + pair_of(i)) : -1;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (long long g = 0; g < nsteps; ++g) {
+            const int row = pre[0];
+#pragma unroll
+            for (int i = 0; i < 7; ++i) pre[i] = pre[i + 1];
+            pre[7] = g + 8 < nsteps ? __ldg(idx + pair_of(g + 8)) : -1;
+            const long long v = v0 + g / kWgStepsPerTile;
+            const long long mn = v / NT;
+            const int c_lo = is_x ? (int)(mn / p.n_tiles) * 128 : (int)(mn % p.n_tiles) * BN;
+            const int c_n = min(is_x ? 128 : BN, C - c_lo);
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t sbase = smem_u32(smem) + (uint32_t)stage * stage_bytes + (is_x ? 0 : a_bytes);
+            const T* rp = src + (size_t)(row < 0 ? 0 : row) * C + c_lo;
+            for (int c = 0; c < c_n; c += 8) {
+                const uint32_t off = (uint32_t)(c / 64) * 8192 + (uint32_t)(kk / 8) * 1024 +
+                                     (uint32_t)(kk % 8) * 128 + (uint32_t)((c % 64) / 8) * 16;
+                const uint32_t sw = off ^ (((off >> 7) & 7) << 4);
+                cp_async16(sbase + sw, row < 0 ? (const void*)src : (const void*)(rp + c),
+                           row < 0 ? 0u : 16u);
+            }
+            cp_async_arrive_noinc(&full[stage]);
+            if (++stage == stages) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    } else if (warp == 4) {
+        // MMA issuer: runs of tiles with the same (mn tile, offset) accumulate
+        const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) | (1u << 15) |
+                               (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(kTileM >> 4) << 24);
+        int stage = 0;
+        uint32_t phase = 0;
+        int run = -1;
+        long long cur_key = -1;
+        uint32_t acc = 0, accumulate = 0;
+        for (long long v = v0; v < v1; ++v) {
+            const long long mn = v / NT;
+            const long long key = mn * (p.kd + 1) + wg_offset_of(p.tile_ptr, p.kd, (int)(v % NT));
+            if (key != cur_key) {
+                if (run >= 0 && lane == 0) tc_commit(&tfull[acc]);
+                ++run;
+                acc = run & 1;
+                mbar_wait(&tempty[acc], (uint32_t)(((run >> 1) & 1) ^ 1));
+                tc_fence_after();
+                cur_key = key;
+                accumulate = 0;
+            }
+            for (int sidx = 0; sidx < kWgStepsPerTile; ++sidx) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = smem_u32(smem) + (uint32_t)stage * stage_bytes;
+#pragma unroll
+                    for (int k16 = 0; k16 < kWgK / 16; ++k16) {
+                        tc_mma_f16(tmem + acc * (uint32_t)BN, mnmajor_desc(sa + k16 * 2048),
+                                   mnmajor_desc(sa + a_bytes + k16 * 2048), idesc, accumulate);
+                        accumulate = 1;
+                    }
+                    tc_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        if (run >= 0 && lane == 0) tc_commit(&tfull[acc]);
+        __syncwarp();
+    } else {
+        // epilogue: TMEM lane = channel ci of the M tile; flush a run with red.add
+        const int quad = warp & 3;
+        const int lr = quad * 32 + lane;
+        int run = -1;
+        long long cur_key = -1, cur_mn = 0;
+        int cur_k = 0;
+        auto flush = [&](int r, long long mn, int k) {
+            const uint32_t a = r & 1;
+            mbar_wait(&tfull[a], (uint32_t)((r >> 1) & 1));
+            tc_fence_after();
+            const int ci = (int)(mn / p.n_tiles) * 128 + lr;
+            const int co0 = (int)(mn % p.n_tiles) * BN;
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + a * (uint32_t)BN + (uint32_t)c0, v);
+                tmem_ld_wait();
+                if (ci >= p.c_in) continue;
+                float* dst = p.dw + ((size_t)k * p.c_in + ci) * p.c_out + co0 + c0;
+                const int lim = min(16, p.c_out - co0 - c0);
+                if (lim == 16 && (p.c_out % 4) == 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        red_add_v4(dst + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                   __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+                } else {
+                    for (int i = 0; i < lim; ++i) atomicAdd(dst + i, __uint_as_float(v[i]));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[a]);
+        };
+        for (long long v = v0; v < v1; ++v) {
+            const long long mn = v / NT;
+            const int k = wg_offset_of(p.tile_ptr, p.kd, (int)(v % NT));
+            const long long key = mn * (p.kd + 1) + k;
+            if (key != cur_key) {
+                if (run >= 0) flush(run, cur_mn, cur_k);
+                ++run;
+                cur_key = key;
+                cur_mn = mn;
+                cur_k = k;
+            }
+        }
+        if (run >= 0) flush(run, cur_mn, cur_k);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 4) tmem_dealloc(tmem, ncols);
+}
+
 size_t elem_size(sk_dtype dt) { return dt == SK_F32 ? 4 : 2; }
 
 // ---- tensor maps (driver entry point resolved once through cudart) ----
@@ -1293,6 +1505,36 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
     kmap_ensure_ws(m, st);
     if (!accumulate) SK_CUDA(cudaMemsetAsync(dw, 0, (size_t)m->kd * c_in * c_out * 4, st));
     if (m->n_out == 0 || m->n_in == 0) return;
+    if (dt != SK_F32 && !ctx->deterministic && c_in % 8 == 0 && c_out % 8 == 0) {
+        // tcgen05 path (fp32 accumulate in TMEM, fp32 red.add flush)
+        WgArgs a;
+        a.x = x;
+        a.dy = dy;
+        a.c_in = c_in;
+        a.c_out = c_out;
+        a.kd = m->kd;
+        a.tile_ptr = m->ws_tile_ptr.as<int>();
+        a.in_pad = m->ws_in_pad.as<int>();
+        a.out_pad = m->ws_out_pad.as<int>();
+        a.dw = dw;
+        a.m_tiles = (int)ceil_div(c_in, 128);
+        a.n_tiles = (int)ceil_div(c_out, 256);
+        a.bn = (int)ceil_div(ceil_div(c_out, a.n_tiles), 16) * 16;
+        a.nblk_b = (int)ceil_div(a.bn, 64);
+        const size_t stage_bytes = 16384 + (size_t)a.nblk_b * 8192;
+        const int stages = (int)std::max<size_t>(2, std::min<size_t>(8, (200 * 1024) / stage_bytes));
+        const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+        auto kern = dt == SK_F16 ? k_wgrad_tc<__half> : k_wgrad_tc<__nv_bfloat16>;
+        static size_t configured = 0;
+        if (smem > configured) {
+            SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            configured = smem;
+        }
+        kern<<<ctx->num_sms, kWgThreads, smem, st>>>(a, stages);
+        SK_LAUNCH_CHECK();
+        return;
+    }
     // pair chunking: enough blocks to fill the machine; deterministic mode
     // uses one chunk per offset (no cross-block float atomics on one cell)
     const int chunk = ctx->deterministic ? (int)std::max<int64_t>(1, (int64_t)m->n_out) : 2048;
