@@ -99,7 +99,7 @@ struct Item {
 __device__ __forceinline__ int pairs_of(int n_tiles) { return (n_tiles + 1) / 2; }
 
 __device__ __forceinline__ int num_items(const ConvArgs& p) {
-    if (p.mode == 0) return p.items;
+    if (p.mode != 1) return p.items;
     if (p.offset_only >= 0)
         return (p.ws_tile_ptr[p.offset_only + 1] - p.ws_tile_ptr[p.offset_only]) * p.n_ntiles;
     return p.ws_tile_ptr[p.kd] * p.n_ntiles;
@@ -107,6 +107,21 @@ __device__ __forceinline__ int num_items(const ConvArgs& p) {
 
 __device__ Item decode(const ConvArgs& p, int item) {
     Item it;
+    if (p.mode == 2) {  // dense identity map (K=1, stride 1): a plain GEMM
+        it.s = 0;
+        it.k = 0;
+        it.t2 = item / p.n_ntiles;
+        it.nt = item % p.n_ntiles;
+        it.w = 1;
+        it.col_begin = 0;
+        it.row0 = (long long)it.t2 * kItemM;
+        it.halves = 2;
+        it.m0 = 1;
+        it.m1 = 0;
+        it.biw0 = 1;
+        it.bw1 = 0;
+        return it;
+    }
     if (p.mode == 0) {
         const int per = pairs_of(p.n_tiles) * p.n_ntiles;
         it.s = p.split_only >= 0 ? p.split_only : item / per;
@@ -181,12 +196,14 @@ __device__ __forceinline__ const int* idx_column(const ConvArgs& p, const Item& 
 
 // row r (0..255) of an item
 __device__ __forceinline__ int a_index(const ConvArgs& p, const Item& it, int r, int j) {
+    if (p.mode == 2) return it.row0 + r < p.n_rows_valid ? (int)(it.row0 + r) : -1;
     if (p.mode == 1 && p.a_identity) return (int)(it.row0 + r);
     const int* col = idx_column(p, it, j, r / kTileM);
     return col ? __ldg(col + (r % kTileM)) : -1;
 }
 
 __device__ __forceinline__ long long out_index(const ConvArgs& p, const Item& it, int r) {
+    if (p.mode == 2) return it.row0 + r < p.n_rows_valid ? it.row0 + r : -1;
     if (p.mode == 0) {
         if (r / kTileM >= it.halves) return -1;
         return __ldg(p.out_row + (size_t)it.s * p.rows_pad + it.row0 + r);
@@ -465,7 +482,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // A-row indices (cp.async.bulk, 512B per half) + its B row base =====
         Cursor cur;
         cur.init(p, n_items);
-        const bool ident = p.mode == 1 && p.a_identity;
+        const bool ident = (p.mode == 1 && p.a_identity) || p.mode == 2;
         int slot = 0;
         uint32_t ph = 0;
         for (;;) {
@@ -483,7 +500,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             const int* c0 = ident ? nullptr : idx_column(p, cur.it, cur.j, 0);
             const int* c1 = ident ? nullptr : idx_column(p, cur.it, cur.j, 1);
             if (ident) {
-                for (int u = lane; u < kItemM; u += 32) ring[u] = (int)(cur.it.row0 + u);
+                for (int u = lane; u < kItemM; u += 32) {
+                    const long long rr = cur.it.row0 + u;
+                    ring[u] = (p.mode == 2 && rr >= p.n_rows_valid) ? -1 : (int)rr;
+                }
             } else if (!c1) {
                 for (int u = kTileM + lane; u < kItemM; u += 32) ring[u] = -1;  // missing half
             }
@@ -514,14 +534,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         int slot = 0, stage = 0;
         uint32_t ph = 0, phase = 0;
         const uint32_t base_u = smem_u32(stage_base);
-        const uint32_t my_bytes = GPW * 4 * KC * 2 + (warp == 0 ? b_bytes : 0);
+        const bool dense = p.mode == 2;  // A rows contiguous: two 128-row 2D tiles
+        const uint32_t my_bytes = dense ? (warp == 0 ? a_bytes + b_bytes : 0)
+                                        : GPW * 4 * KC * 2 + (warp == 0 ? b_bytes : 0);
         for (;;) {
             mbar_wait(&ifull[slot], ph);
             const int brow = descs[slot].brow;
             if (brow < 0) break;
             int4 g4 = make_int4(-1, -1, -1, -1);
-            if (lane < GPW) g4 = reinterpret_cast<const int4*>(idx_ring + slot * kItemM)[warp * GPW + lane];
+            if (dense) g4.x = __shfl_sync(0xffffffffu, idx_ring[slot * kItemM], 0);
+            else if (lane < GPW) g4 = reinterpret_cast<const int4*>(idx_ring + slot * kItemM)[warp * GPW + lane];
             g4.x = g4.x < 0 ? p.n_rows_a : g4.x;  // sentinel -> out of bounds -> zeros
+            // (dense: g4.x is the item's first row, always valid)
             g4.y = g4.y < 0 ? p.n_rows_a : g4.y;
             g4.z = g4.z < 0 ? p.n_rows_a : g4.z;
             g4.w = g4.w < 0 ? p.n_rows_a : g4.w;
@@ -533,6 +557,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 if (lane == 0) mbar_expect_tx(&full[stage], my_bytes);
                 __syncwarp();
                 if (warp == 0) tma_tile2d_elect(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+                if (dense) {
+                    if (warp == 0) {
+                        const int r0 = g4.x;  // first row of the item (identity ring)
+                        tma_tile2d_elect(sa, &tm_a, c * KC, r0, &full[stage]);
+                        tma_tile2d_elect(sa + a_half, &tm_a, c * KC, r0 + kTileM, &full[stage]);
+                    }
+                } else
 #pragma unroll
                 for (int g = 0; g < GPW; ++g) {
                     const int r = (warp * GPW + g) * 4;  // first of the 4 rows
@@ -1184,20 +1215,21 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
     const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
                         (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
+    const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
     CUtensorMap ta, tb;
-    if (use_tma) {
-        ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, 1);
+    if (tma) {
+        ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
         tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
     } else {
         memset(&ta, 0, sizeof(ta));
         memset(&tb, 0, sizeof(tb));
     }
-    auto kern = use_tma ? k_gconv_tc<T, KC, true> : k_gconv_tc<T, KC, false>;
+    auto kern = tma ? k_gconv_tc<T, KC, true> : k_gconv_tc<T, KC, false>;
     static size_t configured[2] = {0, 0};  // per template instantiation
-    if (smem > configured[use_tma]) {
+    if (smem > configured[tma]) {
         SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-        configured[use_tma] = smem;
+        configured[tma] = smem;
     }
     kern<<<grid, kThreadsTC, smem, st>>>(ta, tb, a, stages, acc_bufs);
     SK_LAUNCH_CHECK();
@@ -1238,7 +1270,7 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
     }
     const bool tc = tc_ok(dt, a.k_total, a.n_total);
     int grid;
-    if (a.mode == 0) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
+    if (a.mode != 1) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
     else grid = ctx->num_sms * (tc ? 1 : 8);
     if (tc) {
         if (dt == SK_F16) launch_tc<__half>(a, dt, grid, st);
@@ -1377,6 +1409,18 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     pick_n_tiling(n_total, cfg.tile.cta_n, tc, a.bn, a.n_ntiles);
     const bool det = ctx->deterministic;
 
+    if (m->identity && tc && !det) {
+        // K=1 stride-1 layer on one coordinate set: y = x W_0 for every
+        // dataflow (the map is the identity), so run it as a dense GEMM
+        a.mode = 2;
+        a.n_rows_valid = m->n_out;
+        a.items = (int)ceil_div(m->n_out, kItemM) * a.n_ntiles;
+        a.y = y;
+        a.residual = residual;
+        a.out_mode = 0;
+        launch_gconv(ctx, dt, a, st);
+        return;
+    }
     if (cfg.kind == SK_IMPLICIT_GEMM) {
         Prepared* pr = kmap_prepare(m, cfg.splits, kTileM, st);
         a.mode = 0;

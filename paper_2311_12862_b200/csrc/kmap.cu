@@ -558,6 +558,8 @@ sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t str
     m->transposed = transposed;
     m->n_in = in->n;
     m->n_out = out->n;
+    m->identity = kernel == 1 && in == out && m->stride[0] == 1 && m->stride[1] == 1 &&
+                  m->stride[2] == 1;
     alloc_map(m, st);
     launch_query(m, out->coords.as<int4>(), in, st);
     return m;
@@ -575,6 +577,7 @@ sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
     m->transposed = !src->transposed;
     m->n_in = src->n_out;
     m->n_out = src->n_in;
+    m->identity = src->identity;
     alloc_map(m, st);
     SK_CUDA(cudaMemsetAsync(m->os.p, 0xFF, m->os.bytes, st));
     long long total = (long long)src->n_out * src->kd;

@@ -61,6 +61,7 @@ struct sk_kmap : sk::Refcounted {
     int transposed = 0;
     int n_in = 0, n_out = 0;
     int rows_pad = 0;       // n_out rounded up to 128 (the raw OS is stored padded)
+    bool identity = false;  // K=1, stride 1, in set == out set: entries[q][0] == q
     int words = 1;          // mask words of the full-width map
     int n_blocks = 0;       // query blocks (for per-block pair counts)
     sk::DevBuf os;          // rows_pad x kd int32

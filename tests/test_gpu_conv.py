@@ -162,3 +162,27 @@ def test_contract_errors(env):
         sk.conv_forward(m, x, w.float())
     with pytest.raises(sk.ValidationError):
         sk.conv_forward(m, x, w, sk.DataflowConfig(sk.IMPLICIT_GEMM, 99))
+
+
+@pytest.mark.parametrize("cin,cout", [(32, 96), (96, 96), (128, 256), (256, 256), (4, 32)])
+def test_identity_k1_dense_path(env, restatement, cin, cout):
+    """K=1 stride-1 layers on one coordinate set run as a dense GEMM (the map
+    is the identity); every dataflow config must agree with the oracle."""
+    torch, sk = env
+    from paper_2311_12862_b200.synth import random_instance_coords
+    c_np = random_instance_coords(5, 9000, -20, 20)
+    c = sk.CoordSet.create(c_np)
+    m = sk.build_kmap(c, c, 1, 1)
+    ent, _ = m.os()
+    assert (ent[:, 0] == np.arange(len(c_np))).all()
+    x = torch.randn(m.n_in, cin).half()
+    w = (torch.randn(1, cin, cout) / np.sqrt(cin)).half()
+    y_ref = restatement.conv(ent, x.double().numpy(), w.double().numpy())
+    dy = torch.randn(m.n_out, cout).half()
+    dx_ref = restatement.dgrad(restatement.transpose_os(ent, m.n_in), dy.double().numpy(),
+                               w.double().numpy())
+    for cfg in configs(sk)[:4]:
+        y = sk.conv_forward(m, x.cuda(), w.cuda(), cfg)
+        assert max_rel_err(y.double().cpu().numpy(), y_ref) <= TOL_HALF, cfg.name()
+        dx = sk.conv_dgrad(m, dy.cuda(), w.cuda(), cfg)
+        assert max_rel_err(dx.double().cpu().numpy(), dx_ref) <= TOL_HALF, cfg.name()
