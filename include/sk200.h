@@ -212,6 +212,10 @@ sk_status sk_net_forward(sk_net* net, sk_coords* in, const void* d_feats, int ch
                          void* stream, const void** d_out, int* n_out, double* mapping_ms,
                          double* kernel_ms);
 sk_status sk_net_layer_output(sk_net* net, int layer, const void** d_out, int* rows);
+/* forward with per-layer GPU milliseconds (CUDA events, one sync at the end)
+ * and the total map-building time */
+sk_status sk_net_forward_profiled(sk_net* net, sk_coords* in, const void* d_feats, int channels,
+                                  void* stream, double* layer_ms, double* mapping_ms_total);
 /* NetworkRunner::measure_ms (network.cpp:398-438) */
 sk_status sk_net_measure(sk_net* net, sk_coords* in, const void* d_feats, int channels,
                          int forward, int dgrad, int wgrad, void* stream, double* ms);

@@ -413,18 +413,36 @@ void refresh_wt(sk_net* n, cudaStream_t st) {
     n->wt_dirty = false;
 }
 
+// per-layer CUDA events, read once at the end (no per-layer sync)
+struct LayerEvents {
+    std::vector<cudaEvent_t> ev;
+    explicit LayerEvents(size_t n) : ev(2 * n) {
+        for (auto& e : ev) SK_CUDA(cudaEventCreate(&e));
+    }
+    ~LayerEvents() {
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    float ms(size_t i) {
+        float v = 0;
+        SK_CUDA(cudaEventElapsedTime(&v, ev[2 * i], ev[2 * i + 1]));
+        return v;
+    }
+};
+
 void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cudaStream_t st,
-                 std::vector<double>* map_ms, std::vector<double>* ker_ms) {
+                 std::vector<double>* map_ms, std::vector<double>* ker_ms,
+                 std::vector<double>* layer_ms = nullptr) {
     validate(channels == n->spec.layers[0].c_in || !n->spec.layers[0].inputs.empty(),
              "network input channel count does not match the first layer");
     ensure_maps(n, root, st, map_ms);
     alloc_outputs(n, st);
     refresh_wt(n, st);
     const size_t L = n->spec.layers.size();
+    std::unique_ptr<LayerEvents> evs;
+    if (ker_ms || layer_ms) evs = std::make_unique<LayerEvents>(L);
     for (size_t i = 0; i < L; ++i) {
         const LayerSpec& l = n->spec.layers[i];
-        std::unique_ptr<Timer> t;
-        if (ker_ms) t = std::make_unique<Timer>(st);
+        if (evs) SK_CUDA(cudaEventRecord(evs->ev[2 * i], st));
         const void* x;
         if (l.inputs.empty()) {
             validate(channels == l.c_in, l.name + ": input channel mismatch");
@@ -449,7 +467,16 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
         const void* res = n->fuse_into[i] >= 0 ? n->out_ptr[n->residual_of[i]] : nullptr;
         conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 0, (int)i), n->dt, l.c_in, l.c_out, x,
                      n->w[i].p, n->out_ptr[i], false, st, n->wt[i].p, res);
-        if (ker_ms) (*ker_ms)[n->group_of[i]] += t->stop();
+        if (evs) SK_CUDA(cudaEventRecord(evs->ev[2 * i + 1], st));
+    }
+    if (evs) {
+        SK_CUDA(cudaEventSynchronize(evs->ev[2 * L - 1]));
+        if (layer_ms) layer_ms->assign(L, 0.0);
+        for (size_t i = 0; i < L; ++i) {
+            const double v = evs->ms(i);
+            if (ker_ms) (*ker_ms)[n->group_of[i]] += v;
+            if (layer_ms) (*layer_ms)[i] = v;
+        }
     }
 }
 
@@ -710,6 +737,19 @@ sk_status sk_net_forward(sk_net* n, sk_coords* in, const void* d_feats, int chan
             if (mapping_ms) mapping_ms[g] = mp[g];
             if (kernel_ms) kernel_ms[g] = kr[g];
         }
+    });
+}
+
+// forward with per-layer GPU times (CUDA events, one sync at the end)
+sk_status sk_net_forward_profiled(sk_net* n, sk_coords* in, const void* d_feats, int channels,
+                                  void* stream, double* layer_ms, double* mapping_ms_total) {
+    return nguard([&] {
+        std::vector<double> mp(n->groups.size(), 0.0), lm;
+        run_forward(n, in, d_feats, channels, S(stream), &mp, nullptr, &lm);
+        for (size_t i = 0; i < lm.size(); ++i) layer_ms[i] = lm[i];
+        double t = 0;
+        for (double v : mp) t += v;
+        if (mapping_ms_total) *mapping_ms_total = t;
     });
 }
 

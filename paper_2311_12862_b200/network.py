@@ -148,6 +148,16 @@ class NetworkRunner:
         # copy out of the library-owned buffer (valid until the next forward)
         return device_view(ptr, (rows, cols), self.dtype).clone()
 
+    def forward_profiled(self, coords: CoordSet, feats: torch.Tensor):
+        """Per-layer GPU ms (CUDA events, no per-layer sync) and map-build ms."""
+        feats = feats.to(device="cuda", dtype=self.dtype).contiguous()
+        lm = np.zeros(self.num_layers)
+        mp = C.c_double()
+        check(lib().sk_net_forward_profiled(self.ptr, coords.ptr, _ptr(feats), feats.shape[1],
+                                            _stream(), lm.ctypes.data_as(C.c_void_p),
+                                            C.byref(mp)))
+        return lm, mp.value
+
     def layer_output(self, i: int) -> torch.Tensor:
         p, rows = C.c_void_p(), C.c_int()
         check(lib().sk_net_layer_output(self.ptr, i, C.byref(p), C.byref(rows)))
