@@ -270,6 +270,8 @@ def main():
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("dominant_dram_bytes_per_launch")
 
+    kmap_roof = kmap_roofline(sk, pk) if rank == 0 else None
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -304,6 +306,7 @@ def main():
                                    f"({', '.join(net.layers[i].name for i in net.groups()[g_dom][:3])}...)",
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"
                                         if "fallback" not in pk else "fallback"},
+            "roofline_kmap": kmap_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "scans/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -386,6 +389,49 @@ def run_train(args, rank, world, local):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def kmap_roofline(sk, pk):
+    """Kernel-map build (hash insert + K=3 submanifold query: OS matrix, masks,
+    per-offset counts) on the C5 1M-voxel sweep point (10 disjoint tiles of the
+    planar n=160k / 2.5 cm recipe); algorithmic bytes per the
+    survey's contract with the actual table size (cap x 12 B, charged once for
+    the insert and once for the query)."""
+    import torch
+    from paper_2311_12862_b200.synth import planar_patches, quantize
+    tiles = []
+    for t in range(10):
+        c = quantize(planar_patches(160_000, 1 + t, 2.0), [0.025] * 3)
+        c[:, 1] += 200 * t
+        tiles.append(c)
+    coords = torch.from_numpy(np.concatenate(tiles)).cuda()
+    n = coords.shape[0]
+    cap = 64
+    while cap < 2 * n:
+        cap *= 2
+    ins, qry = [], []
+    for _ in range(4):
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record()
+        cs = sk.CoordSet.create(coords)  # copy + hash insert (+ range check read)
+        b.record()
+        m = sk.build_kmap(cs, cs, 3, 1)  # query kernel: OS, masks, counts
+        c.record()
+        torch.cuda.synchronize()
+        ins.append(a.elapsed_time(b))
+        qry.append(b.elapsed_time(c))
+        del m, cs
+    t_ins, t_q = statistics.median(ins[1:]), statistics.median(qry[1:])
+    kd = 27
+    b_ins = 16 * n + 16 * cap + 16 * n       # coords copy (r+w) + table write (16 B slots)
+    b_q = 16 * n + 16 * cap + 4 * kd * n + 8 * n  # out coords, table read, OS, masks
+    achieved = (b_ins + b_q) / ((t_ins + t_q) * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs", 6650.0),
+            "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs", 6650.0), "traffic": None,
+            "voxels": int(n), "insert_ms": t_ins, "query_ms": t_q,
+            "query_gbs": b_q / (t_q * 1e-3) / 1e9,
+            "algorithmic_bytes": int(b_ins + b_q),
+            "kernel": "k_hash_insert + k_kmap_query<27,4> (1M-voxel C5 sweep point)"}
 
 
 def layer_pairs(sk, net, cs):

@@ -2,7 +2,8 @@
 //
 // Data layout in HBM
 //   coords      int4 [n]                         (Coord, tensor.hpp:15-20)
-//   hash table  u64 keys [cap] + i32 vals [cap]  cap = pow2 >= 2n, linear probing
+//   hash table  16 B slots {u64 key, u32 row, pad} [cap], cap = pow2 >= 2n,
+//               linear probing; one 16 B load resolves a probe (key + row)
 //   OS map      i32 [rows_pad][KD], -1 sentinel   (KernelMapOS, kmap.hpp:65-93)
 //   masks       u64 [rows_pad][words]             (compute_masks, kmap.cpp:34-47)
 //   WS lists    CSR over offsets: ptr[KD+1], in[P], out[P], ascending out row
@@ -48,9 +49,16 @@ __device__ __forceinline__ void offset_of(int k, int K, int dims, int& a, int& b
     }
 }
 
+__device__ __forceinline__ unsigned long long* slot_key(ulonglong2* t, uint64_t s) {
+    return &t[s].x;
+}
+__device__ __forceinline__ unsigned* slot_val(ulonglong2* t, uint64_t s) {
+    return reinterpret_cast<unsigned*>(&t[s].y);  // low 32 bits (little endian)
+}
+
 __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
-                              unsigned long long* __restrict__ keys, int* __restrict__ vals,
-                              uint64_t mask, int* __restrict__ err) {
+                              ulonglong2* __restrict__ table, uint64_t mask,
+                              int* __restrict__ err) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int4 c = coords[i];
@@ -61,9 +69,9 @@ __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
     unsigned long long key = pack_key(c.x, c.y, c.z, c.w);
     uint64_t s = hash_key(key) & mask;
     for (;;) {
-        unsigned long long prev = atomicCAS(&keys[s], (unsigned long long)kEmpty, key);
+        unsigned long long prev = atomicCAS(slot_key(table, s), (unsigned long long)kEmpty, key);
         if (prev == (unsigned long long)kEmpty || prev == key) {
-            atomicMin(&vals[s], i);
+            atomicMin(slot_val(table, s), (unsigned)i);
             return;
         }
         s = (s + 1) & mask;
@@ -71,8 +79,8 @@ __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
 }
 
 __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, int sy, int sz,
-                              int dims, unsigned long long* __restrict__ keys,
-                              int* __restrict__ vals, uint64_t mask, int* __restrict__ slot_out,
+                              int dims, ulonglong2* __restrict__ table, uint64_t mask,
+                              int* __restrict__ slot_out,
                               int4* __restrict__ q_out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -85,9 +93,9 @@ __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, in
     unsigned long long key = pack_key(q.x, q.y, q.z, q.w);
     uint64_t s = hash_key(key) & mask;
     for (;;) {
-        unsigned long long prev = atomicCAS(&keys[s], (unsigned long long)kEmpty, key);
+        unsigned long long prev = atomicCAS(slot_key(table, s), (unsigned long long)kEmpty, key);
         if (prev == (unsigned long long)kEmpty || prev == key) {
-            atomicMin(&vals[s], i);
+            atomicMin(slot_val(table, s), (unsigned)i);
             slot_out[i] = (int)s;
             return;
         }
@@ -95,33 +103,32 @@ __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, in
     }
 }
 
-__global__ void k_down_flag(const int* __restrict__ slot, const int* __restrict__ vals, int n,
+__global__ void k_down_flag(const int* __restrict__ slot, ulonglong2* __restrict__ table, int n,
                             int* __restrict__ flag) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    flag[i] = vals[slot[i]] == i ? 1 : 0;
+    flag[i] = *slot_val(table, slot[i]) == (unsigned)i ? 1 : 0;
 }
 
 __global__ void k_down_compact(const int* __restrict__ flag, const int* __restrict__ pos,
                                const int* __restrict__ slot, const int4* __restrict__ q, int n,
-                               int* __restrict__ vals, int4* __restrict__ out) {
+                               ulonglong2* __restrict__ table, int4* __restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !flag[i]) return;
     int p = pos[i];
     out[p] = q[i];
-    vals[slot[i]] = p;  // the table now maps out-coordinate -> out row
+    *slot_val(table, slot[i]) = (unsigned)p;  // the table now maps out-coordinate -> out row
 }
 
-__device__ __forceinline__ int probe(const unsigned long long* __restrict__ keys,
-                                     const int* __restrict__ vals, uint64_t mask,
-                                     unsigned long long key, uint64_t s,
-                                     unsigned long long first) {
-    unsigned long long kk = first;
+// resolve a probe whose first slot (key + row) is already loaded
+__device__ __forceinline__ int probe(const ulonglong2* __restrict__ table, uint64_t mask,
+                                     unsigned long long key, uint64_t s, ulonglong2 first) {
+    ulonglong2 e = first;
     for (;;) {
-        if (kk == key) return __ldg(&vals[s]);
-        if (kk == (unsigned long long)kEmpty) return -1;
+        if (e.x == key) return (int)(unsigned)e.y;
+        if (e.x == (unsigned long long)kEmpty) return -1;
         s = (s + 1) & mask;
-        kk = __ldg(&keys[s]);
+        e = __ldg(&table[s]);
     }
 }
 
@@ -131,8 +138,8 @@ __device__ __forceinline__ int probe(const unsigned long long* __restrict__ keys
 // block's per-offset pair counts.
 template <int KD, int TPR>
 __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
-    const int4* __restrict__ out_coords, int n_out, const unsigned long long* __restrict__ keys,
-    const int* __restrict__ vals, uint64_t mask, int K, int dims, int sx, int sy, int sz,
+    const int4* __restrict__ out_coords, int n_out, const ulonglong2* __restrict__ table,
+    uint64_t mask, int K, int dims, int sx, int sy, int sz,
     int transposed, int words, int* __restrict__ os, unsigned long long* __restrict__ masks,
     int* __restrict__ blk_counts) {
     extern __shared__ int q_sh[];
@@ -146,7 +153,8 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
     __syncthreads();
     const bool live = row < n_out;
     const int4 q = live ? out_coords[row] : make_int4(0, 0, 0, 0);
-    unsigned long long key[PER], first[PER];
+    unsigned long long key[PER];
+    ulonglong2 first[PER];
     uint64_t slot[PER];
     bool ok[PER];
 #pragma unroll
@@ -179,14 +187,14 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
         }
         key[u] = pack_key(q.x, px, py, pz);
         slot[u] = hash_key(key[u]) & mask;
-        first[u] = __ldg(&keys[slot[u]]);  // PER independent loads in flight
+        first[u] = __ldg(&table[slot[u]]);  // PER independent 16 B loads in flight
     }
     unsigned long long m0 = 0, m1 = 0;
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
         const int k = sub + u * TPR;
         if (k >= KD) continue;
-        const int j = ok[u] ? probe(keys, vals, mask, key[u], slot[u], first[u]) : -1;
+        const int j = ok[u] ? probe(table, mask, key[u], slot[u], first[u]) : -1;
         tile[rl * KD + k] = j;
         if (j >= 0) {
             atomicAdd(&cnt[k], 1);
@@ -451,7 +459,7 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
         SK_CUDA(cudaFuncSetAttribute(k_kmap_query<KDV, TPRV>,                                \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     k_kmap_query<KDV, TPRV><<<grid, kQB * TPRV, smem, st>>>(                                 \
-        out_coords, m->n_out, in->keys.as<unsigned long long>(), in->vals.as<int>(), mask,   \
+        out_coords, m->n_out, in->table.as<ulonglong2>(), mask,                              \
         m->kernel, m->dims, m->stride[0], m->stride[1], m->stride[2], m->transposed, m->words, \
         m->os.as<int>(), m->masks.as<unsigned long long>(), m->blk_counts.as<int>())
     switch (m->kd) {
@@ -488,17 +496,15 @@ void coords_build_table(sk_coords* c, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(c->mu);
     if (c->has_table) return;
     c->cap = pow2_cap(c->n);
-    c->keys.alloc((size_t)c->cap * 8, st);
-    c->vals.alloc((size_t)c->cap * 4, st);
-    SK_CUDA(cudaMemsetAsync(c->keys.p, 0xFF, c->keys.bytes, st));
-    SK_CUDA(cudaMemsetAsync(c->vals.p, 0x7F, c->vals.bytes, st));
+    c->table.alloc((size_t)c->cap * 16, st);
+    SK_CUDA(cudaMemsetAsync(c->table.p, 0xFF, c->table.bytes, st));  // empty key, row = UINT_MAX
     DevBuf err;
     err.alloc(4, st);
     SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
     if (c->n > 0) {
         k_hash_insert<<<(int)ceil_div(c->n, 256), 256, 0, st>>>(
-            c->coords.as<int4>(), c->n, c->keys.as<unsigned long long>(), c->vals.as<int>(),
-            (uint64_t)c->cap - 1, err.as<int>());
+            c->coords.as<int4>(), c->n, c->table.as<ulonglong2>(), (uint64_t)c->cap - 1,
+            err.as<int>());
         SK_LAUNCH_CHECK();
     }
     int h_err = 0;
@@ -517,10 +523,8 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     out->id = next_coord_set_id();
     for (int d = 0; d < 3; ++d) out->stride_tag[d] = in->stride_tag[d] * (d < in->dims ? stride[d] : 1);
     out->cap = pow2_cap(n);
-    out->keys.alloc((size_t)out->cap * 8, st);
-    out->vals.alloc((size_t)out->cap * 4, st);
-    SK_CUDA(cudaMemsetAsync(out->keys.p, 0xFF, out->keys.bytes, st));
-    SK_CUDA(cudaMemsetAsync(out->vals.p, 0x7F, out->vals.bytes, st));
+    out->table.alloc((size_t)out->cap * 16, st);
+    SK_CUDA(cudaMemsetAsync(out->table.p, 0xFF, out->table.bytes, st));
     if (n == 0) {
         out->n = 0;
         out->has_table = true;
@@ -534,10 +538,10 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     const int g = (int)ceil_div(n, 256);
     k_down_insert<<<g, 256, 0, st>>>(in->coords.as<int4>(), n, stride[0], stride[1],
                                      in->dims == 3 ? stride[2] : 1, in->dims,
-                                     out->keys.as<unsigned long long>(), out->vals.as<int>(),
-                                     (uint64_t)out->cap - 1, slot.as<int>(), q.as<int4>());
+                                     out->table.as<ulonglong2>(), (uint64_t)out->cap - 1,
+                                     slot.as<int>(), q.as<int4>());
     SK_LAUNCH_CHECK();
-    k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->vals.as<int>(), n, flag.as<int>());
+    k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), n, flag.as<int>());
     SK_LAUNCH_CHECK();
     size_t tbytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tbytes, flag.as<int>(), pos.as<int>(), n + 1, st);
@@ -553,7 +557,7 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     out->n = h_last_pos + h_last_flag;
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
     k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(),
-                                      q.as<int4>(), n, out->vals.as<int>(),
+                                      q.as<int4>(), n, out->table.as<ulonglong2>(),
                                       out->coords.as<int4>());
     SK_LAUNCH_CHECK();
     out->has_table = true;

@@ -43,8 +43,8 @@ struct sk_coords : sk::Refcounted {
     int32_t stride_tag[3] = {1, 1, 1};
     uint64_t id = 0;
     sk::DevBuf coords;  // int4 [n]
-    // open-addressing hash: keys u64 [cap], vals i32 [cap] (row index)
-    sk::DevBuf keys, vals;
+    // open-addressing hash: 16 B slots {u64 key, u32 row, pad} [cap]
+    sk::DevBuf table;
     int64_t cap = 0;
     bool has_table = false;
     std::mutex mu;
