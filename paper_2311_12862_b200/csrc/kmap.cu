@@ -67,7 +67,7 @@ __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
         return;
     }
     unsigned long long key = pack_key(c.x, c.y, c.z, c.w);
-    uint64_t s = hash_key(key) & mask;
+    uint64_t s = hash_slot(key, mask);
     for (;;) {
         unsigned long long prev = atomicCAS(slot_key(table, s), (unsigned long long)kEmpty, key);
         if (prev == (unsigned long long)kEmpty || prev == key) {
@@ -91,7 +91,7 @@ __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, in
     if (dims == 3) q.w = (int)floor_div(c.w, sz);
     q_out[i] = q;
     unsigned long long key = pack_key(q.x, q.y, q.z, q.w);
-    uint64_t s = hash_key(key) & mask;
+    uint64_t s = hash_slot(key, mask);
     for (;;) {
         unsigned long long prev = atomicCAS(slot_key(table, s), (unsigned long long)kEmpty, key);
         if (prev == (unsigned long long)kEmpty || prev == key) {
@@ -136,6 +136,12 @@ __device__ __forceinline__ int probe(const ulonglong2* __restrict__ table, uint6
 // ceil(KD/TPR) independent probes in flight per thread), 128 rows per block.
 // Writes the OS entries + masks of the block (pad rows get -1 / 0) and the
 // block's per-offset pair counts.
+template <int KD>
+struct KShape {  // K and D implied by K^D (1, 9, 25, 27, 125)
+    static constexpr int dims = (KD == 27 || KD == 125) ? 3 : 2;
+    static constexpr int K = KD == 1 ? 1 : (KD == 9 || KD == 27) ? 3 : 5;
+};
+
 template <int KD, int TPR>
 __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
     const int4* __restrict__ out_coords, int n_out, const ulonglong2* __restrict__ table,
@@ -162,8 +168,18 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
         const int k = sub + u * TPR;
         ok[u] = live && k < KD;
         if (!ok[u]) continue;
+        // lexicographic offset (kmap.cpp:58-71) with compile-time K (no divides)
+        constexpr int KK = KShape<KD>::K, H = KK / 2;
         int a, b, c;
-        offset_of(k, K, dims, a, b, c);
+        if (KShape<KD>::dims == 3) {
+            a = k / (KK * KK) - H;
+            b = (k / KK) % KK - H;
+            c = k % KK - H;
+        } else {
+            a = k / KK - H;
+            b = k % KK - H;
+            c = 0;
+        }
         int px, py, pz;
         if (!transposed) {
             px = q.y * sx + a;
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
             continue;
         }
         key[u] = pack_key(q.x, px, py, pz);
-        slot[u] = hash_key(key[u]) & mask;
+        slot[u] = hash_slot(key[u], mask);
         first[u] = __ldg(&table[slot[u]]);  // PER independent 16 B loads in flight
     }
     unsigned long long m0 = 0, m1 = 0;

@@ -98,13 +98,16 @@ __host__ __device__ inline uint64_t pack_key(int32_t b, int32_t x, int32_t y, in
     return (uint64_t(uint32_t(b)) << 51) | (uint64_t(uint32_t(x + kBias)) << 34) |
            (uint64_t(uint32_t(y + kBias)) << 17) | uint64_t(uint32_t(z + kBias));
 }
-__host__ __device__ inline uint64_t hash_key(uint64_t k) {  // murmur3 fmix64
-    k ^= k >> 33;
-    k *= 0xff51afd7ed558ccdull;
-    k ^= k >> 33;
-    k *= 0xc4ceb9fe1a85ec53ull;
-    k ^= k >> 33;
-    return k;
+// Fibonacci (multiplicative) hashing: the TOP log2(cap) bits of k * 2^64/phi
+// -- one 64-bit multiply per probe; every key bit reaches the slot bits.
+// mask = cap - 1 (cap a power of two).
+__host__ __device__ inline uint64_t hash_slot(uint64_t k, uint64_t mask) {
+#if defined(__CUDA_ARCH__)
+    const int bits = __popcll(mask);
+#else
+    const int bits = __builtin_popcountll(mask);
+#endif
+    return (k * 0x9E3779B97F4A7C15ull) >> (64 - bits);
 }
 __host__ __device__ inline int64_t floor_div(int64_t a, int64_t b) {
     int64_t q = a / b;
