@@ -407,7 +407,7 @@ def kmap_roofline(sk, pk):
     coords = torch.from_numpy(np.concatenate(tiles)).cuda()
     n = coords.shape[0]
     cap = 64
-    while cap < 2 * n:
+    while cap < 4 * n:  # load factor <= 1/4 (kmap.cu pow2_cap)
         cap *= 2
     ins, qry = [], []
     for _ in range(4):

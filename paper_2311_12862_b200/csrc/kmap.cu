@@ -127,8 +127,14 @@ __device__ __forceinline__ int probe(const ulonglong2* __restrict__ table, uint6
     for (;;) {
         if (e.x == key) return (int)(unsigned)e.y;
         if (e.x == (unsigned long long)kEmpty) return -1;
-        s = (s + 1) & mask;
-        e = __ldg(&table[s]);
+        // two slots per iteration (usually the same 32 B sector)
+        const uint64_t s1 = (s + 1) & mask, s2 = (s + 2) & mask;
+        const ulonglong2 e1 = __ldg(&table[s1]);
+        const ulonglong2 e2 = __ldg(&table[s2]);
+        if (e1.x == key) return (int)(unsigned)e1.y;
+        if (e1.x == (unsigned long long)kEmpty) return -1;
+        s = s2;
+        e = e2;
     }
 }
 
@@ -460,9 +466,11 @@ __global__ void k_iota(int* __restrict__ v, int n) {
     if (i < n) v[i] = i;
 }
 
+// load factor <= 1/4: short linear-probing chains keep warps convergent (a
+// warp waits for its longest chain); 16 B slots -> 64 n..128 n bytes, L2-resident
 int64_t pow2_cap(int64_t n) {
     int64_t c = 64;
-    while (c < 2 * n) c <<= 1;
+    while (c < 4 * n) c <<= 1;
     return c;
 }
 
