@@ -25,6 +25,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", "-I" + INCLUDE, "-I" + CSRC]
+# developer builds only (e.g. SK_NVCC_EXTRA=-DSK_CONV_TRACE for the conv timeline)
+FLAGS += os.environ.get("SK_NVCC_EXTRA", "").split()
 
 
 def _deps():

@@ -46,12 +46,16 @@ namespace sk {
 namespace {
 
 constexpr int kItemM = 2 * kTileM;  // rows per work item: two 128-row MMA halves
-constexpr int kProducerWarps = 8;     // warps 0-7: cp.async row gathers
+constexpr int kProducerWarps = 16;    // warps 0-15: cp.async gathers of the real rows
+constexpr int kGroupRows = kItemM / kProducerWarps;  // rows per producer warp (16)
 constexpr int kTmaWarps = 4;          // warps 0-3: TMA gather4 producers (TMA variant)
-constexpr int kMmaWarp = 8;           // warp 8: TMEM owner + tcgen05.mma issuer
-constexpr int kEpiWarp0 = 9;          // warps 9-12: epilogue (TMEM lane quadrants 1,2,3,0)
-constexpr int kIndexWarp = 13;        // warp 13: index/descriptor streamer
-constexpr int kThreadsTC = 448;
+constexpr int kMmaWarp = 16;          // warp 16: TMEM owner + tcgen05.mma issuer
+constexpr int kIndexWarp = 17;        // warp 17: index/descriptor streamer
+constexpr int kZeroWarp0 = 18;        // warps 18-19: st.shared zeros for stale sentinel rows
+constexpr int kZeroWarps = 2;
+constexpr int kEpiWarp0 = 20;         // warps 20-23: epilogue (TMEM lane quadrants 0-3)
+constexpr int kThreadsTC = 768;
+constexpr int kMaxStages = 10;       // launch_tc_kc caps the stage count
 constexpr int kIdxRing = 8;           // column steps in flight in the index ring (1 KB each)
 
 struct ConvArgs {
@@ -79,13 +83,33 @@ struct ConvArgs {
     int n_ntiles, bn;
     const void* residual;  // optional [n_out][ld_y] T added in the epilogue (out_mode 0)
     int items;        // OS mode item count (WS mode: derived on device)
-    long long* trace; // optional clock64 trace of CTA 0 (SK_TRACE env), 4 slots/step
     int split_only;   // >= 0: only items of this split (deterministic sequencing)
+    long long* trace; // SK_CONV_TRACE builds: per-step clock64 timeline of CTA 0
+    int exp;          // SK_CONV_TRACE builds: SK_EXP bits 1 no A gathers, 2 no zeroing, 4 no MMA, 8 no B TMA
     int offset_only;  // >= 0: WS mode only tiles of this offset
 };
 
 // one work item = 256 rows (OS: 128-row tiles 2*t2 and 2*t2+1 of split s;
 // WS: one 256-pair tile of offset k) x one N-tile
+#ifdef SK_CONV_TRACE
+#define SK_TR(slot, cond)                                                              \
+    do {                                                                               \
+        if (p.trace && blockIdx.x == 0 && (cond) && tr_n < 4096)                       \
+            p.trace[(size_t)tr_n * 8 + (slot)] = clock64();                            \
+    } while (0)
+#else
+#define SK_TR(slot, cond) do {} while (0)
+#endif
+#ifdef SK_CONV_TRACE
+#define SK_TZ(k)                                                                       \
+    do {                                                                               \
+        if (p.trace && blockIdx.x == 0 && lane == 0 && zw == 0 && tr_n < 4096)         \
+            p.trace[4096 * 8 + (size_t)tr_n * 4 + (k)] = clock64();                    \
+    } while (0)
+#else
+#define SK_TZ(k) do {} while (0)
+#endif
+
 struct Item {
     int s, t2, nt, k;
     int w;             // split width (OS) or 1 (WS)
@@ -212,14 +236,30 @@ __device__ __forceinline__ long long out_index(const ConvArgs& p, const Item& it
     return p.out_identity ? pi : (long long)__ldg(p.out_pad + pi);
 }
 
+// position of the k-th (0-based) set bit of r
+__device__ __forceinline__ int kth_bit64(uint64_t r, int k) {
+    const uint32_t lo = (uint32_t)r, hi = (uint32_t)(r >> 32);
+    const int c = __popc(lo);
+    return k < c ? (int)__fns(lo, 0, k + 1) : 32 + (int)__fns(hi, 0, k - c + 1);
+}
+
+// i-th work item of this CTA. Items come out of the mask sort in roughly
+// descending cost, so rounds alternate direction (boustrophedon) to even out
+// the per-CTA sums of a static persistent schedule; -1 = no more items.
+__device__ __forceinline__ int item_of(int i, int n_items) {
+    const int g = gridDim.x;
+    const long long it = (long long)i * g + ((i & 1) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
+    return it < n_items ? (int)it : -1;
+}
+
 // iterator over the column steps (item, active column) of this CTA
 struct Cursor {
-    int item, n_items, j;
+    int local, n_items, j;
     Item it;
     unsigned long long m0, m1;
     bool done;
     __device__ void load(const ConvArgs& p) {
-        while (item < n_items) {
+        for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
             it = decode(p, item);
             m0 = it.m0;
             m1 = it.m1;
@@ -228,19 +268,18 @@ struct Cursor {
                 done = false;
                 return;
             }
-            item += gridDim.x;
         }
         done = true;
     }
     __device__ void init(const ConvArgs& p, int n) {
         n_items = n;
-        item = blockIdx.x;
+        local = 0;
         load(p);
     }
     __device__ void advance(const ConvArgs& p) {
         j = next_col(m0, m1, it.biw0, it.bw1);
         if (j < 0) {
-            item += gridDim.x;
+            ++local;
             load(p);
         }
     }
@@ -333,6 +372,16 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_elect(uint32_t dst, const void* src, uint32_t bytes,
+                                               uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n"
+        "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // K-major smem descriptor; row = KC*2 bytes, 8-row swizzle atoms (SBO).
 template <int KC>
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr) {
@@ -407,6 +456,41 @@ __device__ __forceinline__ void store16(const ConvArgs& p, long long orow, int c
     }
 }
 
+// One K step of both 128-row halves (KC/16 MMAs each, interleaved so they
+// share the B stage), then commit -> bar. Called by the whole warp with
+// uniform operands; elect.sync picks the issuing lane.
+template <int KC>
+__device__ __forceinline__ void tc_mma_step_f16(uint32_t d0, uint32_t d1, uint64_t a0, uint64_t a1,
+                                                uint64_t b, uint32_t idesc, uint32_t accumulate,
+                                                uint64_t* bar) {
+#pragma unroll
+    for (int kk = 0; kk < KC / 16; ++kk) {
+        const uint32_t acc = (kk > 0 || accumulate) ? 1u : 0u;
+        asm volatile(
+            "{\n.reg .pred E, p;\n"
+            "elect.sync _|E, 0xffffffff;\n"
+            "setp.ne.b32 p, %6, 0;\n"
+            "@E tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, p;\n"
+            "@E tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %5, p;\n"
+            "}\n" ::"r"(d0),
+            "r"(d1), "l"(a0 + (uint64_t)(kk * 2)), "l"(a1 + (uint64_t)(kk * 2)),
+            "l"(b + (uint64_t)(kk * 2)), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+    asm volatile(
+        "{\n.reg .pred E;\nelect.sync _|E, 0xffffffff;\n"
+        "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred E;\nelect.sync _|E, 0xffffffff;\n"
+        "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
 // per index-ring slot: {brow (first B row of this step, -1 = end of work), unused x3}
 struct alignas(16) StepDesc {
     int brow, pad0, pad1, pad2;
@@ -440,6 +524,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     uint64_t* ifull = tempty + 2;         // [R]
     uint64_t* iempty = ifull + kIdxRing;  // [R]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iempty + kIdxRing);
+    uint32_t* scratch = tmem_slot + 4;  // [producer warps][kGroupRows] compacted row lists
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -450,7 +535,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int i = 0; i < stages; ++i) {
             // cp.async: one noinc arrival per producer thread; TMA: one
             // expect_tx arrival per gathering warp
-            mbar_init(&full[i], USE_TMA ? kTmaWarps : kProducerWarps * 32);
+#ifdef SK_CONV_TRACE
+            const int zw_n = (p.exp & 32) ? 0 : kZeroWarps;
+#else
+            const int zw_n = kZeroWarps;
+#endif
+            mbar_init(&full[i], USE_TMA ? kTmaWarps : kProducerWarps * 32 + zw_n + 1);  // + B TMA
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -459,13 +549,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         for (int i = 0; i < kIdxRing; ++i) {
             mbar_init(&ifull[i], 1);
-            mbar_init(&iempty[i], USE_TMA ? kTmaWarps : kProducerWarps * 32);
+#ifdef SK_CONV_TRACE
+            const int zw_n = (p.exp & 32) ? 0 : kZeroWarps;
+#else
+            const int zw_n = kZeroWarps;
+#endif
+            mbar_init(&iempty[i], USE_TMA ? kTmaWarps : kProducerWarps + zw_n);
         }
         fence_mbar_init();
-        if (USE_TMA) {
+        if (USE_TMA)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
-        }
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
     }
     if (warp == kMmaWarp) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
@@ -477,16 +571,81 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const T* __restrict__ A = static_cast<const T*>(p.a);
     const T* __restrict__ Bw = static_cast<const T*>(p.b);
 
-    if (warp == kIndexWarp) {
-        // ===== index warp: walks the column steps and streams each step's 256
+    if (warp == kIndexWarp && p.mode == 0 && !USE_TMA) {
+        // ===== index warp, implicit GEMM: per item, the lanes work out the
+        // item's active columns in parallel (lane k: k-th set bit of the
+        // tile OR-mask, ascending) with their index-column pointers and B
+        // rows; the serial part per step is then one ring publish (wait slot,
+        // descriptor, expect_tx, one or two 512 B cp.async.bulk). A single
+        // warp's dependent address math per step was the pipeline's pace. =====
+        int slot = 0;
+        uint32_t ph = 0;
+        for (int local = 0, item; (item = item_of(local, n_items)) >= 0; ++local) {
+            const Item it = decode(p, item);
+            const uint64_t r0 = it.biw0 > 0 ? (__brevll(it.m0) >> (64 - it.biw0)) : 0ull;
+            const uint64_t r1 = it.bw1 > 0 ? (__brevll(it.m1) >> (64 - it.bw1)) : 0ull;
+            const int n0 = __popcll(r0), n = n0 + __popcll(r1);
+            const int* tile0 = p.entries + (size_t)p.rows_pad * it.col_begin +
+                               (size_t)(2 * it.t2) * it.w * kTileM;
+            const int half1 = it.halves == 2 ? it.w * kTileM : -1;  // offset of half 1's column
+            for (int base = 0; base < n; base += 32) {
+                const int k = base + lane;
+                int j = 0;
+                if (k < n) j = k < n0 ? kth_bit64(r0, k) : 64 + kth_bit64(r1, k - n0);
+                const int kg = it.col_begin + j;
+                const int brow_l = (p.mirror ? p.kd - 1 - kg : kg) * p.n_total + it.nt * BN;
+                const int cnt = min(32, n - base);
+                for (int u = 0; u < cnt; ++u) {
+                    const int ju = __shfl_sync(0xffffffffu, j, u);
+                    const int brow = __shfl_sync(0xffffffffu, brow_l, u);
+                    const int* c0 = tile0 + (size_t)ju * kTileM;
+                    mbar_wait_sleep(&iempty[slot], ph ^ 1);
+                    int* ring = idx_ring + slot * kItemM;
+                    if (half1 < 0) {
+                        for (int v = kTileM + lane; v < kItemM; v += 32) ring[v] = -1;  // missing half
+                        __syncwarp();
+                    }
+                    if (lane == 0) {
+                        descs[slot].brow = brow;
+                        mbar_expect_tx(&ifull[slot], (half1 >= 0 ? 2 : 1) * kTileM * 4);
+                    }
+                    __syncwarp();
+                    bulk_g2s_elect(smem_u32(ring), c0, kTileM * 4, &ifull[slot]);
+                    if (half1 >= 0)
+                        bulk_g2s_elect(smem_u32(ring + kTileM), c0 + half1, kTileM * 4, &ifull[slot]);
+                    if (++slot == kIdxRing) {
+                        slot = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+        mbar_wait_sleep(&iempty[slot], ph ^ 1);
+        if (lane == 0) {
+            descs[slot].brow = -1;
+            mbar_arrive(&ifull[slot]);
+        }
+    } else if (warp == kIndexWarp) {
+        // ===== index warp (FOD/GGS pair tiles, dense, TMA variant): walks the column steps and streams each step's 256
         // A-row indices (cp.async.bulk, 512B per half) + its B row base =====
         Cursor cur;
+#ifdef SK_CONV_TRACE
+        int tr_n = 0;
+#endif
         cur.init(p, n_items);
         const bool ident = (p.mode == 1 && p.a_identity) || p.mode == 2;
         int slot = 0;
         uint32_t ph = 0;
         for (;;) {
-            mbar_wait(&iempty[slot], ph ^ 1);
+#ifdef SK_CONV_TRACE
+            if (p.trace && blockIdx.x == 0 && lane == 0 && tr_n < 4096)
+                p.trace[4096 * 12 + (size_t)tr_n * 2] = clock64();
+#endif
+            mbar_wait_sleep(&iempty[slot], ph ^ 1);
+#ifdef SK_CONV_TRACE
+            if (p.trace && blockIdx.x == 0 && lane == 0 && tr_n < 4096)
+                p.trace[4096 * 12 + (size_t)tr_n * 2 + 1] = clock64();
+#endif
             int* ring = idx_ring + slot * kItemM;
             if (cur.done) {
                 if (lane == 0) {
@@ -508,18 +667,28 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int u = kTileM + lane; u < kItemM; u += 32) ring[u] = -1;  // missing half
             }
             __syncwarp();
+#ifdef SK_CONV_TRACE
+            if (p.trace && blockIdx.x == 0 && lane == 0 && tr_n < 4096)
+                p.trace[4096 * 14 + (size_t)tr_n * 2] = clock64();
+#endif
             if (lane == 0) {
                 descs[slot].brow = kb * p.n_total + cur.it.nt * BN;
-                if (ident) {
-                    mbar_arrive(&ifull[slot]);
-                } else {
-                    const uint32_t bytes = (c1 ? 2 : 1) * kTileM * 4;
-                    mbar_expect_tx(&ifull[slot], bytes);
-                    bulk_g2s(smem_u32(ring), c0, kTileM * 4, &ifull[slot]);
-                    if (c1) bulk_g2s(smem_u32(ring + kTileM), c1, kTileM * 4, &ifull[slot]);
-                }
+                if (ident) mbar_arrive(&ifull[slot]);
+                else mbar_expect_tx(&ifull[slot], (c1 ? 2 : 1) * kTileM * 4);
             }
             __syncwarp();
+#ifdef SK_CONV_TRACE
+            if (p.trace && blockIdx.x == 0 && lane == 0 && tr_n < 4096)
+                p.trace[4096 * 14 + (size_t)tr_n * 2 + 1] = clock64();
+#endif
+            if (!ident) {  // uniform issue, elected lane (no per-lane R2UR loops)
+                bulk_g2s_elect(smem_u32(ring), c0, kTileM * 4, &ifull[slot]);
+                if (c1) bulk_g2s_elect(smem_u32(ring + kTileM), c1, kTileM * 4, &ifull[slot]);
+            }
+            SK_TR(7, lane == 0);
+#ifdef SK_CONV_TRACE
+            ++tr_n;
+#endif
             cur.advance(p);
             if (++slot == kIdxRing) {
                 slot = 0;
@@ -585,58 +754,177 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
         }
     } else if (!USE_TMA && warp < kProducerWarps) {
-        // ===== producers: CH = KC/8 consecutive threads cover one row's KC
-        // channels (16B cp.async each, zero-fill for sentinels / channel tails),
-        // so a warp instruction touches 32/CH whole rows; the same mapping loads
-        // the B tile. Completion arrives on the stage barrier asynchronously
+        // ===== producers: warp w owns rows [16w, 16w+16) of every step and
+        // gathers only its REAL rows, compacted (ballot + prefix, a 16-entry
+        // per-warp list) so every cp.async instruction is fully populated:
+        // CH = KC/8 lanes per row, 32/CH rows per instruction. LDGSTS drain
+        // cost follows the instruction count, not the active lanes, so
+        // predicated-off sentinel lanes would waste it. Stale sentinel rows are
+        // the zero warps' job; warp 0 also loads the B tile with one 2D TMA
+        // (elected lane, expect_tx). Completion is signalled asynchronously
         // (cp.async.mbarrier.arrive.noinc). =====
-        constexpr int CH = KC / 8;                            // 16B chunks per row
-        constexpr int PT = kProducerWarps * 32;               // producer threads
-        constexpr int RSTRIDE = PT / CH;                      // rows between a thread's rows
-        constexpr int RPT = kItemM / RSTRIDE;                 // rows per thread
+        constexpr int CH = KC / 8;        // 16B chunks per row
+        constexpr int RPI = 32 / CH;      // rows per cp.async instruction
+        constexpr int IT = (kGroupRows + RPI - 1) / RPI;
+        constexpr uint32_t RB = KC * 2;   // bytes per stage row
+        constexpr uint32_t SWB = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
+        const int q = lane % CH, sub = lane / CH;
+        uint32_t* list = scratch + warp * kGroupRows;  // (idx << 5) | row
+        const size_t row_bytes = (size_t)p.k_total * sizeof(T);
+        const char* __restrict__ Ab = reinterpret_cast<const char*>(A) + q * 16;
+        const uint32_t half_off = (uint32_t)(warp * kGroupRows / kTileM) * a_half;
+        const uint32_t row0 = (uint32_t)(warp * kGroupRows % kTileM);
+#ifdef SK_CONV_TRACE
         const int t = threadIdx.x;
-        const int q = t % CH, r0 = t / CH;
-        int slot = 0, stage = 0, tstep = 0;
+        int tr_n = 0;
+#endif
+        int slot = 0, stage = 0;
         uint32_t ph = 0, phase = 0;
         const uint32_t base_u = smem_u32(stage_base);
-        const long long b_rows = (long long)p.kd * p.n_total;
         for (;;) {
-            mbar_wait(&ifull[slot], ph);
+            mbar_wait_sleep(&ifull[slot], ph);
             const int brow = descs[slot].brow;
             if (brow < 0) break;
-            int ai[RPT];
+            const int my = lane < kGroupRows ? idx_ring[slot * kItemM + warp * kGroupRows + lane] : -1;
+            const uint32_t real = __ballot_sync(0xffffffffu, my >= 0);
+            if (my >= 0) list[__popc(real & ((1u << lane) - 1))] = ((uint32_t)my << 5) | (uint32_t)lane;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&iempty[slot]);
+#ifdef SK_CONV_TRACE
+            const int n_do = (p.exp & 1) ? 0 : __popc(real);
+#else
+            const int n_do = __popc(real);
+#endif
+            uint32_t e[IT];
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) ai[i] = idx_ring[slot * kItemM + r0 + i * RSTRIDE];
-            mbar_arrive(&iempty[slot]);
+            for (int i = 0; i < IT; ++i) e[i] = (sub + i * RPI < n_do) ? list[sub + i * RPI] : 0u;
+            __syncwarp();  // list reused next step
             for (int c = 0; c < nchunks; ++c) {
-                const long long t_a = p.trace ? clock64() : 0;
-                mbar_wait(&empty[stage], phase ^ 1);
-                if (p.trace && blockIdx.x == 0 && t == 0 && tstep < 2048) {
-                    p.trace[tstep * 4 + 0] = t_a;
-                    p.trace[tstep * 4 + 1] = clock64();
-                }
-                ++tstep;
+                SK_TR(0, t == 0);
+                mbar_wait_sleep(&empty[stage], phase ^ 1);
+                SK_TR(1, t == 0);
                 const uint32_t sa = base_u + (uint32_t)stage * stage_bytes;
-                const uint32_t sb = sa + a_bytes;
-                const int col = c * KC + q * 8;
-                const bool col_ok = col < p.k_total;
-                // zero-fill cp.async (src-size 0) for sentinel rows / channel
-                // tails: measured faster than st.shared + fence.proxy.async
-                // (the proxy fence waits for the thread's in-flight copies)
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                    const int r = r0 + i * RSTRIDE;
-                    const bool ok = ai[i] >= 0 && col_ok;
-                    const T* src = A + (size_t)(ok ? ai[i] : 0) * p.k_total + (ok ? col : 0);
-                    cp_async16(sa + (uint32_t)(r / kTileM) * a_half + swz<KC>(r % kTileM, q), src,
-                               ok ? 16u : 0u);
+                if (warp == 0) {
+#ifdef SK_CONV_TRACE
+                    if (p.exp & 8) { if (lane == 0) mbar_arrive(&full[stage]); } else
+#endif
+                    {
+                    if (lane == 0) mbar_expect_tx(&full[stage], b_bytes);
+                    __syncwarp();
+                    tma_tile2d_elect(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+                    }
                 }
-                for (int n = r0; n < BN; n += RSTRIDE) {
-                    const bool ok = (brow + n) < b_rows && col_ok;
-                    const T* src = Bw + (ok ? (size_t)(brow + n) * p.k_total + col : 0);
-                    cp_async16(sb + swz<KC>(n, q), src, ok ? 16u : 0u);
+                const uint32_t sa_w = sa + half_off;
+                const int col = c * KC + q * 8;
+                const uint32_t nbytes = col < p.k_total ? 16u : 0u;  // channel tail -> zeros
+                const char* src_c = Ab + (size_t)c * KC * sizeof(T);
+#pragma unroll
+                for (int i = 0; i < IT; ++i) {
+                    if (sub + i * RPI >= n_do) break;
+                    const uint32_t r = row0 + (e[i] & 31u);            // row within the half
+                    const uint32_t off = r * RB + (uint32_t)q * 16;
+                    cp_async16(sa_w + (off ^ (((off >> 7) & SWB) << 4)),
+                               src_c + (size_t)(e[i] >> 5) * row_bytes, nbytes);
                 }
                 cp_async_arrive_noinc(&full[stage]);
+                SK_TR(2, t == 0);
+#ifdef SK_CONV_TRACE
+                ++tr_n;
+#endif
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (++slot == kIdxRing) {
+                slot = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (!USE_TMA && warp >= kZeroWarp0 && warp < kZeroWarp0 + kZeroWarps
+#ifdef SK_CONV_TRACE
+               && !(p.exp & 32)
+#endif
+               ) {
+        // ===== zero warps: st.shared zeros into sentinel rows, but only rows
+        // that still hold real data from the previous use of the stage (a
+        // per-stage dirty mask per 32-row group): about half of the sentinel
+        // rows are already zero. Lane l owns row l of each of its groups
+        // (KC/8 16-byte stores, swizzled so 8 consecutive rows hit distinct
+        // banks). Then fence.proxy.async so the tensor core (async proxy) sees
+        // the zeros; these warps issue no cp.async, so the fence never waits
+        // on in-flight gathers. =====
+        constexpr int CH = KC / 8;
+        constexpr uint32_t RB = KC * 2;
+        constexpr uint32_t SWB = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
+        constexpr int GROUPS = kItemM / 32 / kZeroWarps;  // 32-row groups per zero warp
+        const int zw = warp - kZeroWarp0;
+        uint32_t dreg[kMaxStages];  // stage contents unknown at start: all dirty
+#pragma unroll
+        for (int k = 0; k < kMaxStages; ++k) dreg[k] = ~0u;
+#ifdef SK_CONV_TRACE
+        int tr_n = 0;
+#endif
+        int slot = 0, stage = 0;
+        uint32_t ph = 0, phase = 0;
+        const uint32_t base_u = smem_u32(stage_base);
+        for (;;) {
+            SK_TZ(0);
+            mbar_wait_sleep(&ifull[slot], ph);
+            SK_TZ(1);
+            if (descs[slot].brow < 0) break;
+            uint32_t real[GROUPS];
+#pragma unroll
+            for (int g = 0; g < GROUPS; ++g)
+                real[g] = __ballot_sync(0xffffffffu,
+                                        idx_ring[slot * kItemM + (zw * GROUPS + g) * 32 + lane] >= 0);
+            if (lane == 0) mbar_arrive(&iempty[slot]);
+            for (int c = 0; c < nchunks; ++c) {
+                SK_TZ(2);
+                mbar_wait_sleep(&empty[stage], phase ^ 1);
+                SK_TZ(3);
+                const uint32_t sa = base_u + (uint32_t)stage * stage_bytes;
+                // lane g < GROUPS keeps group g's per-stage dirty masks in registers
+                uint32_t mine = 0, my_real = 0;
+#pragma unroll
+                for (int g = 0; g < GROUPS; ++g)
+                    if (lane == g) my_real = real[g];
+#pragma unroll
+                for (int k = 0; k < kMaxStages; ++k)
+                    if (k == stage) {
+                        mine = ~my_real & dreg[k];
+                        dreg[k] = my_real;
+                    }
+                uint32_t need[GROUPS];
+#pragma unroll
+                for (int g = 0; g < GROUPS; ++g) need[g] = __shfl_sync(0xffffffffu, mine, g);
+#pragma unroll
+                for (int g = 0; g < GROUPS; ++g) {
+                    if (!(need[g] >> lane & 1u)) continue;
+#ifdef SK_CONV_TRACE
+                    if (p.exp & 2) continue;
+#endif
+                    const int grp = zw * GROUPS + g;
+                    const uint32_t r = (uint32_t)(grp * 32 % kTileM + lane);
+                    const uint32_t rb = sa + (uint32_t)(grp * 32 / kTileM) * a_half + r * RB;
+                    const uint32_t x = ((r * RB >> 7) & SWB) << 4;  // Swizzle<B,4,3> of this row
+#pragma unroll
+                    for (int qq = 0; qq < CH; ++qq)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
+                                         rb + (((uint32_t)qq * 16) ^ x)),
+                                     "r"(0)
+                                     : "memory");
+                }
+#ifdef SK_CONV_TRACE
+                if (!(p.exp & 16))
+#endif
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[stage]);
+                SK_TR(6, lane == 0 && zw == 0);
+#ifdef SK_CONV_TRACE
+                ++tr_n;
+#endif
                 if (++stage == stages) {
                     stage = 0;
                     phase ^= 1;
@@ -648,18 +936,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
         }
     } else if (warp == kMmaWarp) {
-        // ================= MMA issuer (one thread) =================
+        // ===== MMA issuer: the whole warp runs the loop with uniform values
+        // and elect.sync picks the issuing lane inside the asm, so descriptors
+        // stay in uniform registers (no per-MMA R2UR/elect loops) =====
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
-        int stage = 0, tstep = 0;
+        int stage = 0;
         uint32_t phase = 0;
         const uint64_t desc0 = kmajor_desc<KC>(smem_u32(stage_base));
+#ifdef SK_CONV_TRACE
+        int tr_n = 0;
+        long long tt0 = 0, tt1 = 0;
+#endif
         int local = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+        for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
             Item it = decode(p, item);
             const int acc = acc_bufs == 2 ? (local & 1) : 0;
             const uint32_t aph = acc_bufs == 2 ? (uint32_t)((local >> 1) & 1) : (uint32_t)(local & 1);
+#ifdef SK_CONV_TRACE
+            tt0 = clock64();
+#endif
             mbar_wait(&tempty[acc], aph ^ 1);
+#ifdef SK_CONV_TRACE
+            tt1 = clock64();
+#endif
             tc_fence_after();
             const uint32_t d0 = tmem + (uint32_t)(acc * 2 * BN);  // half 0; half 1 at +BN
             unsigned long long m0 = it.m0, m1 = it.m1;
@@ -667,34 +967,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
                  j = next_col(m0, m1, it.biw0, it.bw1)) {
                 for (int c = 0; c < nchunks; ++c) {
+                    SK_TR(3, lane == 0);
                     mbar_wait(&full[stage], phase);
+                    SK_TR(4, lane == 0);
                     tc_fence_after();
-                    if (p.trace && blockIdx.x == 0 && lane == 0 && tstep < 2048)
-                        p.trace[tstep * 4 + 2] = clock64();
-                    ++tstep;
-                    if (lane == 0) {
-                        // descriptor start addresses advance in 16B units
-                        const uint64_t da = desc0 + ((uint64_t)stage * stage_bytes >> 4);
-                        const uint64_t da1 = da + (a_half >> 4);
-                        const uint64_t db = da + (a_bytes >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < KC / 16; ++kk) {
-                            tc_mma_f16(d0, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
-                                       accumulate);
-                            tc_mma_f16(d0 + (uint32_t)BN, da1 + (uint64_t)(kk * 2),
-                                       db + (uint64_t)(kk * 2), idesc, accumulate);
-                            accumulate = 1;
-                        }
-                        tc_commit(&empty[stage]);
-                    }
-                    __syncwarp();
+                    // descriptor start addresses advance in 16B units
+                    const uint64_t da = desc0 + ((uint64_t)stage * stage_bytes >> 4);
+#ifdef SK_CONV_TRACE
+                    if (p.exp & 4) tc_commit_elect(&empty[stage]); else
+#endif
+                    tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, da, da + (a_half >> 4),
+                                        da + (a_bytes >> 4), idesc, accumulate, &empty[stage]);
+                    SK_TR(5, lane == 0);
+#ifdef SK_CONV_TRACE
+                    tt0 = tt1 = 0;
+                    ++tr_n;
+#endif
+                    accumulate = 1;
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             }
-            if (lane == 0) tc_commit(&tfull[acc]);
+            tc_commit_elect(&tfull[acc]);
             __syncwarp();
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
@@ -702,14 +998,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const int quad = warp & 3;
         const int lr = quad * 32 + lane;
         int local = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+        for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
             Item it = decode(p, item);
             long long orow[2];
             orow[0] = out_index(p, it, lr);  // issued before the wait
             orow[1] = out_index(p, it, kTileM + lr);
             const int acc = acc_bufs == 2 ? (local & 1) : 0;
             const uint32_t aph = acc_bufs == 2 ? (uint32_t)((local >> 1) & 1) : (uint32_t)(local & 1);
-            mbar_wait(&tfull[acc], aph);
+            mbar_wait_sleep<256>(&tfull[acc], aph);
             tc_fence_after();
             const bool empty_tile = (it.m0 | it.m1) == 0;
             const int n0 = it.nt * BN;
@@ -1213,20 +1509,16 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
     }();
     const int bn = a.bn;
     const size_t stage_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
-    int stages = (int)std::min<size_t>(10, (200 * 1024) / stage_bytes);
+    int stages = (int)std::min<size_t>(kMaxStages, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
     const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
-                        (2 * stages + 4 + 2 * kIdxRing) * 8 + 16;
+                        (2 * stages + 4 + 2 * kIdxRing) * 8 + 16 + kProducerWarps * kGroupRows * 4;
     const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
     CUtensorMap ta, tb;
-    if (tma) {
-        ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
-        tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
-    } else {
-        memset(&ta, 0, sizeof(ta));
-        memset(&tb, 0, sizeof(tb));
-    }
+    if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
+    else memset(&ta, 0, sizeof(ta));
+    tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
     auto kern = tma ? k_gconv_tc<T, KC, true> : k_gconv_tc<T, KC, false>;
     static size_t configured[2] = {0, 0};  // per template instantiation
     if (smem > configured[tma]) {
@@ -1264,13 +1556,36 @@ void pick_n_tiling(int n_total, int cta_n, bool tc, int& bn, int& n_nt) {
 
 void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t st) {
     ConvArgs a = a_in;
-    static const bool trace = getenv("SK_TRACE") != nullptr;
+#ifdef SK_CONV_TRACE
     DevBuf tbuf;
-    if (trace) {
-        tbuf.alloc(2048 * 4 * 8, st);
+    const char* tpath = getenv("SK_TRACE");
+    if (tpath) {
+        tbuf.alloc(4096 * 16 * 8, st);
         SK_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, st));
         a.trace = tbuf.as<long long>();
     }
+    a.exp = getenv("SK_EXP") ? atoi(getenv("SK_EXP")) : 0;
+    struct Dump {
+        DevBuf& b; const char* path; cudaStream_t st; const ConvArgs& a;
+        ~Dump() {
+            if (!path) return;
+            std::vector<long long> h(4096 * 16);
+            cudaMemcpyAsync(h.data(), b.p, b.bytes, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            if (FILE* f = fopen(path, "a")) {
+                fprintf(f, "# k=%d n=%d bn=%d\n", a.k_total, a.n_total, a.bn);
+                for (int i = 0; i < 4096 && h[i * 8 + 4]; ++i) {
+                    for (int j = 0; j < 8; ++j) fprintf(f, "%lld ", h[i * 8 + j]);
+                    for (int j = 0; j < 4; ++j) fprintf(f, "%lld ", h[4096 * 8 + i * 4 + j]);
+                    for (int j = 0; j < 2; ++j) fprintf(f, "%lld ", h[4096 * 12 + i * 2 + j]);
+                    for (int j = 0; j < 2; ++j) fprintf(f, "%lld ", h[4096 * 14 + i * 2 + j]);
+                    fprintf(f, "\n");
+                }
+                fclose(f);
+            }
+        }
+    } dump{tbuf, tpath, st, a};
+#endif
     const bool tc = tc_ok(dt, a.k_total, a.n_total);
     int grid;
     if (a.mode != 1) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
@@ -1283,26 +1598,6 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
         else if (dt == SK_F16) k_gconv_simt<__half><<<grid, 256, 0, st>>>(a);
         else k_gconv_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(a);
         SK_LAUNCH_CHECK();
-    }
-    if (trace && tc) {
-        std::vector<long long> h(2048 * 4);
-        SK_CUDA(cudaMemcpyAsync(h.data(), tbuf.p, tbuf.bytes, cudaMemcpyDeviceToHost, st));
-        SK_CUDA(cudaStreamSynchronize(st));
-        const long long t0 = h[0];
-        int n = 0;
-        while (n < 2048 && h[n * 4 + 1]) ++n;
-        double issue_gap = 0, land = 0, wait_empty = 0, wait_idx = 0;
-        for (int i = 0; i < n; ++i) wait_idx += h[i * 4 + 3];
-        fprintf(stderr, "idx-ring wait %.0f cyc/step\n", n ? wait_idx / n : 0);
-        for (int i = 1; i < n; ++i) issue_gap += h[i * 4 + 1] - h[(i - 1) * 4 + 1];
-        for (int i = 0; i < n; ++i) {
-            land += h[i * 4 + 2] - h[i * 4 + 1];
-            wait_empty += h[i * 4 + 1] - h[i * 4 + 0];
-        }
-        fprintf(stderr, "trace k=%d n=%d bn=%d grid=%d steps(cta0)=%d: issue_gap %.0f cyc, "
-                "issue->mma %.0f cyc, empty_wait %.0f cyc, total %lld cyc\n", a.k_total,
-                a.n_total, a.bn, grid, n, n > 1 ? issue_gap / (n - 1) : 0, n ? land / n : 0,
-                n ? wait_empty / n : 0, n ? h[(n - 1) * 4 + 2] - t0 : 0);
     }
 }
 

@@ -3,12 +3,12 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2311_12862_b200 import sparse as sk
-from paper_2311_12862_b200.synth import uniform_voxels
+from paper_2311_12862_b200.synth import uniform_voxels, lidar_scan
 
 C = int(os.environ.get("C", 64))
 S = int(os.environ.get("SPLITS", 1))
 KIND = int(os.environ.get("KIND", 2))
-coords = torch.from_numpy(uniform_voxels(127_000, 64, 1)).cuda()
+coords = torch.from_numpy(lidar_scan() if os.environ.get("SCAN") == "lidar" else uniform_voxels(127_000, 64, 1)).cuda()
 c = sk.CoordSet.create(coords)
 m = sk.build_kmap(c, c, 3, 1)
 x = torch.randn(m.n_in, C, device="cuda").half()
