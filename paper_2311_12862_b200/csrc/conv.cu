@@ -56,6 +56,7 @@ constexpr int kZeroWarps = 2;
 constexpr int kEpiWarp0 = 20;         // warps 20-23: epilogue (TMEM lane quadrants 0-3)
 constexpr int kThreadsTC = 768;
 constexpr int kMaxStages = 10;       // launch_tc_kc caps the stage count
+constexpr int kCompactLag = 3;       // index warp compacts slot s-3 after publishing s
 constexpr int kIdxRing = 8;           // column steps in flight in the index ring (1 KB each)
 
 struct ConvArgs {
@@ -491,6 +492,38 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
         : "memory");
 }
 
+// Per ring slot, built by the index warp from the slot's 256 row indices:
+// for each producer warp's 16-row group the list of its real rows
+// ((idx << 5) | row-in-group) and their count, and the real-row bitmask of
+// every 32-row group (zero warps). Moves the ballot/compaction smem traffic
+// off the producers' per-step critical path (their LDS would queue behind
+// the SM's LDGSTS backlog in the MIO pipe).
+struct CSlot {
+    uint32_t list[kProducerWarps][kGroupRows];
+    int cnt[kProducerWarps];
+    uint32_t zmask[kItemM / 32];
+};
+// index warp: lane l covers rows 8l..8l+7 of the slot
+__device__ __forceinline__ void compact_slot(const int* ring, CSlot& cs, int lane) {
+    const int4 a = reinterpret_cast<const int4*>(ring)[2 * lane];
+    const int4 b = reinterpret_cast<const int4*>(ring)[2 * lane + 1];
+    const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t bits = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bits |= (v[i] >= 0 ? 1u : 0u) << i;
+    const uint32_t partner = __shfl_xor_sync(0xffffffffu, bits, 1);
+    int k = (lane & 1) ? __popc(partner) : 0;
+    uint32_t* L = cs.list[lane >> 1];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (bits >> i & 1u) L[k++] = ((uint32_t)v[i] << 5) | (uint32_t)((lane & 1) * 8 + i);
+    if (lane & 1) cs.cnt[lane >> 1] = k;
+    uint32_t m = bits << ((lane & 3) * 8);
+    m |= __shfl_xor_sync(0xffffffffu, m, 1);
+    m |= __shfl_xor_sync(0xffffffffu, m, 2);
+    if ((lane & 3) == 0) cs.zmask[lane >> 2] = m;
+}
+
 // per index-ring slot: {brow (first B row of this step, -1 = end of work), unused x3}
 struct alignas(16) StepDesc {
     int brow, pad0, pad1, pad2;
@@ -521,10 +554,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;
     uint64_t* tempty = tfull + 2;
-    uint64_t* ifull = tempty + 2;         // [R]
-    uint64_t* iempty = ifull + kIdxRing;  // [R]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iempty + kIdxRing);
-    uint32_t* scratch = tmem_slot + 4;  // [producer warps][kGroupRows] compacted row lists
+    uint64_t* ifull = tempty + 2;         // [R] ring slot landed (bulk copy / fill)
+    uint64_t* iempty = ifull + kIdxRing;  // [R] all gathering warps done with the slot
+    uint64_t* cfull = iempty + kIdxRing;  // [R] compacted row lists of the slot ready
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + kIdxRing);
+    CSlot* cslots = reinterpret_cast<CSlot*>(tmem_slot + 4);  // [R] compacted row lists
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -549,6 +583,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         for (int i = 0; i < kIdxRing; ++i) {
             mbar_init(&ifull[i], 1);
+            mbar_init(&cfull[i], 1);
 #ifdef SK_CONV_TRACE
             const int zw_n = (p.exp & 32) ? 0 : kZeroWarps;
 #else
@@ -580,6 +615,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // warp's dependent address math per step was the pipeline's pace. =====
         int slot = 0;
         uint32_t ph = 0;
+        int pub = 0, cmp = 0;  // steps published / compacted (compaction lags kCompactLag)
+        auto compact_one = [&]() {
+            const int sl = cmp % kIdxRing;
+            mbar_wait(&ifull[sl], (uint32_t)(cmp / kIdxRing) & 1u);
+            compact_slot(idx_ring + sl * kItemM, cslots[sl], lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&cfull[sl]);
+            ++cmp;
+        };
+#ifdef SK_CONV_TRACE
+        int tr_n = 0;
+#endif
         for (int local = 0, item; (item = item_of(local, n_items)) >= 0; ++local) {
             const Item it = decode(p, item);
             const uint64_t r0 = it.biw0 > 0 ? (__brevll(it.m0) >> (64 - it.biw0)) : 0ull;
@@ -613,6 +660,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     bulk_g2s_elect(smem_u32(ring), c0, kTileM * 4, &ifull[slot]);
                     if (half1 >= 0)
                         bulk_g2s_elect(smem_u32(ring + kTileM), c0 + half1, kTileM * 4, &ifull[slot]);
+                    SK_TR(7, lane == 0);
+#ifdef SK_CONV_TRACE
+                    ++tr_n;
+#endif
+                    if (++pub - cmp > kCompactLag) compact_one();
                     if (++slot == kIdxRing) {
                         slot = 0;
                         ph ^= 1;
@@ -620,10 +672,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 }
             }
         }
+        while (cmp < pub) compact_one();
         mbar_wait_sleep(&iempty[slot], ph ^ 1);
         if (lane == 0) {
             descs[slot].brow = -1;
             mbar_arrive(&ifull[slot]);
+            mbar_arrive(&cfull[slot]);
         }
     } else if (warp == kIndexWarp) {
         // ===== index warp (FOD/GGS pair tiles, dense, TMA variant): walks the column steps and streams each step's 256
@@ -636,6 +690,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const bool ident = (p.mode == 1 && p.a_identity) || p.mode == 2;
         int slot = 0;
         uint32_t ph = 0;
+        int pub = 0, cmp = 0;
+        auto compact_one = [&]() {
+            const int sl = cmp % kIdxRing;
+            mbar_wait(&ifull[sl], (uint32_t)(cmp / kIdxRing) & 1u);
+            compact_slot(idx_ring + sl * kItemM, cslots[sl], lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&cfull[sl]);
+            ++cmp;
+        };
         for (;;) {
 #ifdef SK_CONV_TRACE
             if (p.trace && blockIdx.x == 0 && lane == 0 && tr_n < 4096)
@@ -648,9 +711,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #endif
             int* ring = idx_ring + slot * kItemM;
             if (cur.done) {
+                if (!USE_TMA)
+                    while (cmp < pub) compact_one();
                 if (lane == 0) {
                     descs[slot].brow = -1;
                     mbar_arrive(&ifull[slot]);
+                    mbar_arrive(&cfull[slot]);
                 }
                 break;
             }
@@ -690,6 +756,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             ++tr_n;
 #endif
             cur.advance(p);
+            if (!USE_TMA && ++pub - cmp > kCompactLag) compact_one();
             if (++slot == kIdxRing) {
                 slot = 0;
                 ph ^= 1;
@@ -769,7 +836,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         constexpr uint32_t RB = KC * 2;   // bytes per stage row
         constexpr uint32_t SWB = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
         const int q = lane % CH, sub = lane / CH;
-        uint32_t* list = scratch + warp * kGroupRows;  // (idx << 5) | row
         const size_t row_bytes = (size_t)p.k_total * sizeof(T);
         const char* __restrict__ Ab = reinterpret_cast<const char*>(A) + q * 16;
         const uint32_t half_off = (uint32_t)(warp * kGroupRows / kTileM) * a_half;
@@ -782,23 +848,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint32_t ph = 0, phase = 0;
         const uint32_t base_u = smem_u32(stage_base);
         for (;;) {
-            mbar_wait_sleep(&ifull[slot], ph);
+#ifdef SK_CONV_TRACE
+            if (p.trace && blockIdx.x == 0 && t == 0 && tr_n < 4096)
+                p.trace[4096 * 12 + (size_t)tr_n * 2] = clock64();
+#endif
+            mbar_wait_sleep(&cfull[slot], ph);
+#ifdef SK_CONV_TRACE
+            if (p.trace && blockIdx.x == 0 && t == 0 && tr_n < 4096)
+                p.trace[4096 * 12 + (size_t)tr_n * 2 + 1] = clock64();
+#endif
             const int brow = descs[slot].brow;
             if (brow < 0) break;
-            const int my = lane < kGroupRows ? idx_ring[slot * kItemM + warp * kGroupRows + lane] : -1;
-            const uint32_t real = __ballot_sync(0xffffffffu, my >= 0);
-            if (my >= 0) list[__popc(real & ((1u << lane) - 1))] = ((uint32_t)my << 5) | (uint32_t)lane;
+            // count and list entries are independent loads: one MIO round trip
+            const int n = cslots[slot].cnt[warp];
+            uint32_t e[IT];
+#pragma unroll
+            for (int i = 0; i < IT; ++i) e[i] = cslots[slot].list[warp][(sub + i * RPI) % kGroupRows];
             __syncwarp();
             if (lane == 0) mbar_arrive(&iempty[slot]);
 #ifdef SK_CONV_TRACE
-            const int n_do = (p.exp & 1) ? 0 : __popc(real);
+            const int n_do = (p.exp & 1) ? 0 : n;
 #else
-            const int n_do = __popc(real);
+            const int n_do = n;
 #endif
-            uint32_t e[IT];
-#pragma unroll
-            for (int i = 0; i < IT; ++i) e[i] = (sub + i * RPI < n_do) ? list[sub + i * RPI] : 0u;
-            __syncwarp();  // list reused next step
             for (int c = 0; c < nchunks; ++c) {
                 SK_TR(0, t == 0);
                 mbar_wait_sleep(&empty[stage], phase ^ 1);
@@ -870,14 +942,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const uint32_t base_u = smem_u32(stage_base);
         for (;;) {
             SK_TZ(0);
-            mbar_wait_sleep(&ifull[slot], ph);
+            mbar_wait_sleep(&cfull[slot], ph);
             SK_TZ(1);
             if (descs[slot].brow < 0) break;
             uint32_t real[GROUPS];
 #pragma unroll
-            for (int g = 0; g < GROUPS; ++g)
-                real[g] = __ballot_sync(0xffffffffu,
-                                        idx_ring[slot * kItemM + (zw * GROUPS + g) * 32 + lane] >= 0);
+            for (int g = 0; g < GROUPS; ++g) real[g] = cslots[slot].zmask[zw * GROUPS + g];
+            __syncwarp();
             if (lane == 0) mbar_arrive(&iempty[slot]);
             for (int c = 0; c < nchunks; ++c) {
                 SK_TZ(2);
@@ -946,48 +1017,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const uint64_t desc0 = kmajor_desc<KC>(smem_u32(stage_base));
 #ifdef SK_CONV_TRACE
         int tr_n = 0;
-        long long tt0 = 0, tt1 = 0;
 #endif
         int local = 0;
         for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
             Item it = decode(p, item);
             const int acc = acc_bufs == 2 ? (local & 1) : 0;
             const uint32_t aph = acc_bufs == 2 ? (uint32_t)((local >> 1) & 1) : (uint32_t)(local & 1);
-#ifdef SK_CONV_TRACE
-            tt0 = clock64();
-#endif
             mbar_wait(&tempty[acc], aph ^ 1);
-#ifdef SK_CONV_TRACE
-            tt1 = clock64();
-#endif
             tc_fence_after();
             const uint32_t d0 = tmem + (uint32_t)(acc * 2 * BN);  // half 0; half 1 at +BN
-            unsigned long long m0 = it.m0, m1 = it.m1;
+            // the MMA needs only the step count: A and B come from the stage
+            const int nsteps = (__popcll(it.m0) + __popcll(it.m1)) * nchunks;
             uint32_t accumulate = 0;
-            for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
-                 j = next_col(m0, m1, it.biw0, it.bw1)) {
-                for (int c = 0; c < nchunks; ++c) {
-                    SK_TR(3, lane == 0);
-                    mbar_wait(&full[stage], phase);
-                    SK_TR(4, lane == 0);
-                    tc_fence_after();
-                    // descriptor start addresses advance in 16B units
-                    const uint64_t da = desc0 + ((uint64_t)stage * stage_bytes >> 4);
+            for (int st = 0; st < nsteps; ++st) {
+                SK_TR(3, lane == 0);
+                mbar_wait(&full[stage], phase);
+                SK_TR(4, lane == 0);
+                tc_fence_after();
+                // descriptor start addresses advance in 16B units
+                const uint64_t da = desc0 + ((uint64_t)stage * stage_bytes >> 4);
 #ifdef SK_CONV_TRACE
-                    if (p.exp & 4) tc_commit_elect(&empty[stage]); else
+                if (p.exp & 4) tc_commit_elect(&empty[stage]); else
 #endif
-                    tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, da, da + (a_half >> 4),
-                                        da + (a_bytes >> 4), idesc, accumulate, &empty[stage]);
-                    SK_TR(5, lane == 0);
+                tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, da, da + (a_half >> 4),
+                                    da + (a_bytes >> 4), idesc, accumulate, &empty[stage]);
+                SK_TR(5, lane == 0);
 #ifdef SK_CONV_TRACE
-                    tt0 = tt1 = 0;
-                    ++tr_n;
+                ++tr_n;
 #endif
-                    accumulate = 1;
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                accumulate = 1;
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
             tc_commit_elect(&tfull[acc]);
@@ -1513,7 +1574,7 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
     stages = std::max(stages, 2);
     const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
-                        (2 * stages + 4 + 2 * kIdxRing) * 8 + 16 + kProducerWarps * kGroupRows * 4;
+                        (2 * stages + 4 + 3 * kIdxRing) * 8 + 16 + kIdxRing * sizeof(CSlot);
     const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
     CUtensorMap ta, tb;
     if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
