@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsk200.so")
+# SK200_LIB: developer A/B runs against another build of the same ABI
+LIB_PATH = os.environ.get("SK200_LIB") or os.path.join(PKG, "libsk200.so")
 
 # exported symbols, in header order (include/sk200.h); tests check the .so
 # exports exactly these

@@ -478,11 +478,12 @@ __device__ __forceinline__ void tc_mma_step_f16(uint32_t d0, uint32_t d1, uint64
             "l"(b + (uint64_t)(kk * 2)), "r"(idesc), "r"(acc)
             : "memory");
     }
-    asm volatile(
-        "{\n.reg .pred E;\nelect.sync _|E, 0xffffffff;\n"
-        "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
-            smem_u32(bar))
-        : "memory");
+    if (bar)
+        asm volatile(
+            "{\n.reg .pred E;\nelect.sync _|E, 0xffffffff;\n"
+            "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+                smem_u32(bar))
+            : "memory");
 }
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
     asm volatile(
@@ -534,7 +535,7 @@ struct alignas(16) StepDesc {
 // from uniform warp code (shuffled operands, elect.sync inside the asm), and
 // warp 0 loads B with one 2D TMA tile. USE_TMA = false: warps 0-7 gather with
 // 16 B cp.async (reference path, kept for A/B measurement).
-template <typename T, int KC, bool USE_TMA>
+template <typename T, int KC, bool USE_TMA, int SLABS>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const ConvArgs p, int stages, int acc_bufs) {
@@ -545,7 +546,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t a_half = kTileM * KC * 2;   // one 128-row half
     const uint32_t a_bytes = 2 * a_half;       // 256-row A tile
     const uint32_t b_bytes = (uint32_t)BN * KC * 2;
-    const uint32_t stage_bytes = a_bytes + b_bytes;
+    // a stage holds NSL K-slabs of KC channels (cp.async path: the chunks of
+    // one column step together, fewer and fatter pipeline steps): A slabs
+    // first, then the B slabs
+    constexpr int NSL = USE_TMA ? 1 : SLABS;
+    const uint32_t a_all = (uint32_t)NSL * a_bytes;
+    const uint32_t stage_bytes = (uint32_t)NSL * (a_bytes + b_bytes);
     uint8_t* stage_base = smem;
     int* idx_ring = reinterpret_cast<int*>(smem + (size_t)stages * stage_bytes);  // [R][256]
     StepDesc* descs = reinterpret_cast<StepDesc*>(idx_ring + kIdxRing * kItemM);   // [R]
@@ -871,7 +877,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #else
             const int n_do = n;
 #endif
-            for (int c = 0; c < nchunks; ++c) {
+            for (int c0 = 0; c0 < nchunks; c0 += NSL) {
                 SK_TR(0, t == 0);
                 mbar_wait_sleep(&empty[stage], phase ^ 1);
                 SK_TR(1, t == 0);
@@ -881,22 +887,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     if (p.exp & 8) { if (lane == 0) mbar_arrive(&full[stage]); } else
 #endif
                     {
-                    if (lane == 0) mbar_expect_tx(&full[stage], b_bytes);
+                    if (lane == 0) mbar_expect_tx(&full[stage], NSL * b_bytes);
                     __syncwarp();
-                    tma_tile2d_elect(sa + a_bytes, &tm_b, c * KC, brow, &full[stage]);
+                    for (int sl = 0; sl < NSL; ++sl)
+                        tma_tile2d_elect(sa + a_all + sl * b_bytes, &tm_b, (c0 + sl) * KC, brow,
+                                         &full[stage]);
                     }
                 }
-                const uint32_t sa_w = sa + half_off;
-                const int col = c * KC + q * 8;
-                const uint32_t nbytes = col < p.k_total ? 16u : 0u;  // channel tail -> zeros
-                const char* src_c = Ab + (size_t)c * KC * sizeof(T);
+                for (int sl = 0; sl < NSL; ++sl) {
+                    const uint32_t sa_w = sa + sl * a_bytes + half_off;
+                    const int col = (c0 + sl) * KC + q * 8;
+                    const uint32_t nbytes = col < p.k_total ? 16u : 0u;  // channel tail -> zeros
+                    const char* src_c = Ab + (size_t)(c0 + sl) * KC * sizeof(T);
 #pragma unroll
-                for (int i = 0; i < IT; ++i) {
-                    if (sub + i * RPI >= n_do) break;
-                    const uint32_t r = row0 + (e[i] & 31u);            // row within the half
-                    const uint32_t off = r * RB + (uint32_t)q * 16;
-                    cp_async16(sa_w + (off ^ (((off >> 7) & SWB) << 4)),
-                               src_c + (size_t)(e[i] >> 5) * row_bytes, nbytes);
+                    for (int i = 0; i < IT; ++i) {
+                        if (sub + i * RPI >= n_do) break;
+                        const uint32_t r = row0 + (e[i] & 31u);            // row within the half
+                        const uint32_t off = r * RB + (uint32_t)q * 16;
+                        cp_async16(sa_w + (off ^ (((off >> 7) & SWB) << 4)),
+                                   src_c + (size_t)(e[i] >> 5) * row_bytes, nbytes);
+                    }
                 }
                 cp_async_arrive_noinc(&full[stage]);
                 SK_TR(2, t == 0);
@@ -950,7 +960,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             for (int g = 0; g < GROUPS; ++g) real[g] = cslots[slot].zmask[zw * GROUPS + g];
             __syncwarp();
             if (lane == 0) mbar_arrive(&iempty[slot]);
-            for (int c = 0; c < nchunks; ++c) {
+            for (int c0 = 0; c0 < nchunks; c0 += NSL) {
                 SK_TZ(2);
                 mbar_wait_sleep(&empty[stage], phase ^ 1);
                 SK_TZ(3);
@@ -979,12 +989,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     const uint32_t r = (uint32_t)(grp * 32 % kTileM + lane);
                     const uint32_t rb = sa + (uint32_t)(grp * 32 / kTileM) * a_half + r * RB;
                     const uint32_t x = ((r * RB >> 7) & SWB) << 4;  // Swizzle<B,4,3> of this row
+                    for (int sl = 0; sl < NSL; ++sl)
 #pragma unroll
-                    for (int qq = 0; qq < CH; ++qq)
-                        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
-                                         rb + (((uint32_t)qq * 16) ^ x)),
-                                     "r"(0)
-                                     : "memory");
+                        for (int qq = 0; qq < CH; ++qq)
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
+                                             rb + sl * a_bytes + (((uint32_t)qq * 16) ^ x)),
+                                         "r"(0)
+                                         : "memory");
                 }
 #ifdef SK_CONV_TRACE
                 if (!(p.exp & 16))
@@ -1027,7 +1038,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             tc_fence_after();
             const uint32_t d0 = tmem + (uint32_t)(acc * 2 * BN);  // half 0; half 1 at +BN
             // the MMA needs only the step count: A and B come from the stage
-            const int nsteps = (__popcll(it.m0) + __popcll(it.m1)) * nchunks;
+            const int nsteps = (__popcll(it.m0) + __popcll(it.m1)) * (nchunks / NSL);
             uint32_t accumulate = 0;
             for (int st = 0; st < nsteps; ++st) {
                 SK_TR(3, lane == 0);
@@ -1039,8 +1050,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #ifdef SK_CONV_TRACE
                 if (p.exp & 4) tc_commit_elect(&empty[stage]); else
 #endif
-                tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, da, da + (a_half >> 4),
-                                    da + (a_bytes >> 4), idesc, accumulate, &empty[stage]);
+                {
+                    for (int sl = 0; sl + 1 < NSL; ++sl) {
+                        const uint64_t ds = da + ((uint64_t)(sl * a_bytes) >> 4);
+                        tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, ds, ds + (a_half >> 4),
+                                            da + ((uint64_t)(a_all + sl * b_bytes) >> 4), idesc,
+                                            accumulate, nullptr);
+                        accumulate = 1;
+                    }
+                    const uint64_t ds = da + ((uint64_t)((NSL - 1) * a_bytes) >> 4);
+                    tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, ds, ds + (a_half >> 4),
+                                        da + ((uint64_t)(a_all + (NSL - 1) * b_bytes) >> 4), idesc,
+                                        accumulate, &empty[stage]);
+                }
                 SK_TR(5, lane == 0);
 #ifdef SK_CONV_TRACE
                 ++tr_n;
@@ -1569,23 +1591,38 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
         return e && std::string(e) == "tma";
     }();
     const int bn = a.bn;
-    const size_t stage_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
+    const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
+    // slabs: chunks per pipeline step (all of C_in when the stage still leaves
+    // >= min_stages in flight); per-step overheads, not bytes, pace this pipe
+    static const int min_stages = [] {
+        const char* e = getenv("SK_SLAB_MIN_STAGES");
+        return e ? std::max(1, atoi(e)) : 3;
+    }();
+    const int nchunks = (int)ceil_div(a.k_total, KC);
+    const size_t slab_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
+    // C_in = 96 (three 32-channel slabs) is the one width where fusing the
+    // chunks pays (measured: C = 64/128 gain nothing, and SLABS stays a
+    // compile-time constant so the single-slab kernel keeps its lean loops)
+    const int slabs = (!tma && KC == 32 && nchunks == 3 && ((size_t)bn * KC * 2) % 1024 == 0 &&
+                       (size_t)min_stages * 3 * slab_bytes <= 200 * 1024) ? 3 : 1;
+    const size_t stage_bytes = slabs * slab_bytes;
     int stages = (int)std::min<size_t>(kMaxStages, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
     const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
                         (2 * stages + 4 + 3 * kIdxRing) * 8 + 16 + kIdxRing * sizeof(CSlot);
-    const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
     CUtensorMap ta, tb;
     if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
     else memset(&ta, 0, sizeof(ta));
     tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
-    auto kern = tma ? k_gconv_tc<T, KC, true> : k_gconv_tc<T, KC, false>;
-    static size_t configured[2] = {0, 0};  // per template instantiation
-    if (smem > configured[tma]) {
+    auto kern = tma ? k_gconv_tc<T, KC, true, 1>
+                    : (slabs == 3 ? k_gconv_tc<T, KC, false, 3> : k_gconv_tc<T, KC, false, 1>);
+    const int variant = tma ? 0 : (slabs == 3 ? 2 : 1);
+    static size_t configured[3] = {0, 0, 0};  // per template instantiation
+    if (smem > configured[variant]) {
         SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-        configured[tma] = smem;
+        configured[variant] = smem;
     }
     kern<<<grid, kThreadsTC, smem, st>>>(ta, tb, a, stages, acc_bufs);
     SK_LAUNCH_CHECK();
