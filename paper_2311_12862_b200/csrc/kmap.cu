@@ -231,11 +231,13 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
         m1 |= __shfl_xor_sync(0xffffffffu, m1, o);
     }
     __syncthreads();
+    // streaming (evict-first) stores: the OS matrix is the bulk of the traffic
+    // and must not push the hash table out of L2 while other blocks probe it
     int* dst = os + (size_t)blockIdx.x * kQB * KD;
-    for (int i = t; i < kQB * KD; i += kQB * TPR) dst[i] = tile[i];
+    for (int i = t; i < kQB * KD; i += kQB * TPR) __stcs(dst + i, tile[i]);
     if (sub == 0) {
-        masks[(size_t)row * words] = m0;
-        if (words == 2) masks[(size_t)row * words + 1] = m1;
+        __stcs(masks + (size_t)row * words, m0);
+        if (words == 2) __stcs(masks + (size_t)row * words + 1, m1);
     }
     for (int k = t; k < KD; k += kQB * TPR) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
 }

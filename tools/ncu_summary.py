@@ -65,11 +65,12 @@ def full(path, out, algo=None, unit=None):
                     f.write(f"| {m} | {r[i]} | {units[i]} |\n")
             try:
                 dur_us = float(vals["gpu__time_duration.sum"].replace(",", ""))
-                rd = float(vals["dram__bytes_read.sum"].replace(",", ""))
-                wr = float(vals["dram__bytes_write.sum"].replace(",", ""))
-                ur = units[hdr.index("dram__bytes_read.sum")]
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-                f.write(f"\nDRAM traffic {(rd + wr) * scale / 1e6:.2f} MB in {dur_us:.1f} us\n")
+                sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                rd = float(vals["dram__bytes_read.sum"].replace(",", "")) * \
+                    sc.get(units[hdr.index("dram__bytes_read.sum")], 1)
+                wr = float(vals["dram__bytes_write.sum"].replace(",", "")) * \
+                    sc.get(units[hdr.index("dram__bytes_write.sum")], 1)
+                f.write(f"\nDRAM traffic {(rd + wr) / 1e6:.2f} MB in {dur_us:.1f} us\n")
                 if algo:
                     f.write(f"Algorithmic {algo} {unit} per launch -> "
                             f"{float(algo) / (dur_us * 1e-6) / 1e12:.2f} T{unit}/s under ncu\n")
