@@ -46,15 +46,21 @@ namespace sk {
 namespace {
 
 constexpr int kItemM = 2 * kTileM;  // rows per work item: two 128-row MMA halves
-constexpr int kProducerWarps = 16;    // warps 0-15: cp.async gathers of the real rows
-constexpr int kGroupRows = kItemM / kProducerWarps;  // rows per producer warp (16)
+// Warp roles of k_gconv_tc for PW producer warps (16: one CTA per SM, 768
+// threads; 8: two CTAs per SM, 512 threads, <= 64 registers). Epilogue warps
+// start at a multiple of 4 (TMEM lane quadrant = warp % 4).
+template <int PW>
+struct Roles {
+    static constexpr int kProducerWarps = PW;           // warps 0..PW-1: cp.async gathers
+    static constexpr int kGroupRows = 256 / PW;        // rows per producer warp (16 / 32)
+    static constexpr int kMmaWarp = PW;                 // TMEM owner + tcgen05.mma issuer
+    static constexpr int kIndexWarp = PW + 1;           // index/descriptor streamer
+    static constexpr int kZeroWarp0 = PW + 2;           // 2 zero warps
+    static constexpr int kEpiWarp0 = PW + 4;            // 4 epilogue warps
+    static constexpr int kThreads = (PW + 8) * 32;
+};
 constexpr int kTmaWarps = 4;          // warps 0-3: TMA gather4 producers (TMA variant)
-constexpr int kMmaWarp = 16;          // warp 16: TMEM owner + tcgen05.mma issuer
-constexpr int kIndexWarp = 17;        // warp 17: index/descriptor streamer
-constexpr int kZeroWarp0 = 18;        // warps 18-19: st.shared zeros for stale sentinel rows
 constexpr int kZeroWarps = 2;
-constexpr int kEpiWarp0 = 20;         // warps 20-23: epilogue (TMEM lane quadrants 0-3)
-constexpr int kThreadsTC = 768;
 constexpr int kMaxStages = 10;       // launch_tc_kc caps the stage count
 constexpr int kCompactLag = 3;       // index warp compacts slot s-3 after publishing s
 constexpr int kIdxRing = 8;           // column steps in flight in the index ring (1 KB each)
@@ -499,26 +505,36 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
 // every 32-row group (zero warps). Moves the ballot/compaction smem traffic
 // off the producers' per-step critical path (their LDS would queue behind
 // the SM's LDGSTS backlog in the MIO pipe).
+template <int PW>
 struct CSlot {
-    uint32_t list[kProducerWarps][kGroupRows];
-    int cnt[kProducerWarps];
+    uint32_t list[PW][256 / PW];
+    int cnt[PW];
     uint32_t zmask[kItemM / 32];
 };
-// index warp: lane l covers rows 8l..8l+7 of the slot
-__device__ __forceinline__ void compact_slot(const int* ring, CSlot& cs, int lane) {
+// index warp: lane l covers rows 8l..8l+7 of the slot; a producer group of
+// 256/PW rows spans LPG = 32/PW lanes (prefix over the group's lanes)
+template <int PW>
+__device__ __forceinline__ void compact_slot(const int* ring, CSlot<PW>& cs, int lane) {
+    constexpr int LPG = 32 / PW;
     const int4 a = reinterpret_cast<const int4*>(ring)[2 * lane];
     const int4 b = reinterpret_cast<const int4*>(ring)[2 * lane + 1];
     const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     uint32_t bits = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) bits |= (v[i] >= 0 ? 1u : 0u) << i;
-    const uint32_t partner = __shfl_xor_sync(0xffffffffu, bits, 1);
-    int k = (lane & 1) ? __popc(partner) : 0;
-    uint32_t* L = cs.list[lane >> 1];
+    const int c = __popc(bits);
+    int incl = c;  // inclusive scan over the group's lanes
+#pragma unroll
+    for (int o = 1; o < LPG; o <<= 1) {
+        const int up = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((lane % LPG) >= o) incl += up;
+    }
+    int k = incl - c;
+    uint32_t* L = cs.list[lane / LPG];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-        if (bits >> i & 1u) L[k++] = ((uint32_t)v[i] << 5) | (uint32_t)((lane & 1) * 8 + i);
-    if (lane & 1) cs.cnt[lane >> 1] = k;
+        if (bits >> i & 1u) L[k++] = ((uint32_t)v[i] << 5) | (uint32_t)((lane % LPG) * 8 + i);
+    if (lane % LPG == LPG - 1) cs.cnt[lane / LPG] = incl;
     uint32_t m = bits << ((lane & 3) * 8);
     m |= __shfl_xor_sync(0xffffffffu, m, 1);
     m |= __shfl_xor_sync(0xffffffffu, m, 2);
@@ -535,10 +551,16 @@ struct alignas(16) StepDesc {
 // from uniform warp code (shuffled operands, elect.sync inside the asm), and
 // warp 0 loads B with one 2D TMA tile. USE_TMA = false: warps 0-7 gather with
 // 16 B cp.async (reference path, kept for A/B measurement).
-template <typename T, int KC, bool USE_TMA, int SLABS>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+template <typename T, int KC, bool USE_TMA, int SLABS, int PW>
+__global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
     k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const ConvArgs p, int stages, int acc_bufs) {
+    constexpr int kProducerWarps = Roles<PW>::kProducerWarps;
+    constexpr int kGroupRows = Roles<PW>::kGroupRows;
+    constexpr int kMmaWarp = Roles<PW>::kMmaWarp;
+    constexpr int kIndexWarp = Roles<PW>::kIndexWarp;
+    constexpr int kZeroWarp0 = Roles<PW>::kZeroWarp0;
+    constexpr int kEpiWarp0 = Roles<PW>::kEpiWarp0;
     // dynamic smem starts 1024B-aligned (no static smem); checked below since
     // the swizzle atoms and UMMA descriptors rely on it
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -564,7 +586,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     uint64_t* iempty = ifull + kIdxRing;  // [R] all gathering warps done with the slot
     uint64_t* cfull = iempty + kIdxRing;  // [R] compacted row lists of the slot ready
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + kIdxRing);
-    CSlot* cslots = reinterpret_cast<CSlot*>(tmem_slot + 4);  // [R] compacted row lists
+    CSlot<PW>* cslots = reinterpret_cast<CSlot<PW>*>(tmem_slot + 4);  // [R] compacted row lists
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -1582,24 +1604,62 @@ CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, i
     return m;
 }
 
+template <typename T, int KC, bool TMA, int SLABS, int PW>
+void launch_tc_variant(const ConvArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
+                       int grid, int stages, int acc_bufs, size_t stage_bytes,
+                       cudaStream_t st) {
+    const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
+                        (2 * stages + 4 + 3 * kIdxRing) * 8 + 16 + kIdxRing * sizeof(CSlot<PW>);
+    auto kern = k_gconv_tc<T, KC, TMA, SLABS, PW>;
+    static size_t configured = 0;  // per template instantiation
+    if (smem > configured) {
+        SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        configured = smem;
+    }
+    kern<<<grid, Roles<PW>::kThreads, smem, st>>>(ta, tb, a, stages, acc_bufs);
+    SK_LAUNCH_CHECK();
+}
+
 template <typename T, int KC>
-void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
+void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStream_t st) {
     // cp.async measured faster than TMA gather4 for C <= 128 on B200
     // (tools/layer_bench.py, profiles/r01_gather_paths.md); SK_GATHER=tma selects TMA
     static const bool use_tma = [] {
         const char* e = getenv("SK_GATHER");
         return e && std::string(e) == "tma";
     }();
+    // two CTAs per SM (8 producer warps, half the smem each) for C_out <= 128:
+    // the pipeline is paced by single-warp latency, so a second independent
+    // pipeline per SM overlaps it (SK_CONV_2CTA=0 disables)
+    static const bool two_cta = [] {
+        const char* e = getenv("SK_CONV_2CTA");
+        return !e || atoi(e) != 0;
+    }();
     const int bn = a.bn;
     const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
-    // slabs: chunks per pipeline step (all of C_in when the stage still leaves
-    // >= min_stages in flight); per-step overheads, not bytes, pace this pipe
     static const int min_stages = [] {
         const char* e = getenv("SK_SLAB_MIN_STAGES");
         return e ? std::max(1, atoi(e)) : 3;
     }();
     const int nchunks = (int)ceil_div(a.k_total, KC);
     const size_t slab_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
+    CUtensorMap ta, tb;
+    if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
+    else memset(&ta, 0, sizeof(ta));
+    tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
+    const bool slab3 = !tma && KC == 32 && nchunks == 3;  // C = 96: three-slab path wins
+    if (!tma && two_cta && bn <= 128 && !slab3) {
+        // TMEM per CTA <= 256 columns: double-buffer only up to BN = 64
+        const int acc_bufs = 4 * bn <= 256 ? 2 : 1;
+        const int stages = (int)std::min<size_t>(kMaxStages, (96 * 1024) / slab_bytes);
+        if (stages >= 2) {
+            const int g2 = a.mode == 1 ? 2 * num_sms : std::min(a.items, 2 * num_sms);
+            launch_tc_variant<T, KC, false, 1, 8>(a, ta, tb, std::max(1, g2), stages, acc_bufs,
+                                                  slab_bytes, st);
+            return;
+        }
+    }
     // C_in = 96 (three 32-channel slabs) is the one width where fusing the
     // chunks pays (measured: C = 64/128 gain nothing, and SLABS stays a
     // compile-time constant so the single-slab kernel keeps its lean loops)
@@ -1609,30 +1669,17 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
     int stages = (int)std::min<size_t>(kMaxStages, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
     const int acc_bufs = 4 * bn <= 512 ? 2 : 1;  // double-buffered TMEM accumulators
-    const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
-                        (2 * stages + 4 + 3 * kIdxRing) * 8 + 16 + kIdxRing * sizeof(CSlot);
-    CUtensorMap ta, tb;
-    if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
-    else memset(&ta, 0, sizeof(ta));
-    tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
-    auto kern = tma ? k_gconv_tc<T, KC, true, 1>
-                    : (slabs == 3 ? k_gconv_tc<T, KC, false, 3> : k_gconv_tc<T, KC, false, 1>);
-    const int variant = tma ? 0 : (slabs == 3 ? 2 : 1);
-    static size_t configured[3] = {0, 0, 0};  // per template instantiation
-    if (smem > configured[variant]) {
-        SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        configured[variant] = smem;
-    }
-    kern<<<grid, kThreadsTC, smem, st>>>(ta, tb, a, stages, acc_bufs);
-    SK_LAUNCH_CHECK();
+    if (tma) launch_tc_variant<T, KC, true, 1, 16>(a, ta, tb, grid, stages, acc_bufs, stage_bytes, st);
+    else if (slabs == 3)
+        launch_tc_variant<T, KC, false, 3, 16>(a, ta, tb, grid, stages, acc_bufs, stage_bytes, st);
+    else launch_tc_variant<T, KC, false, 1, 16>(a, ta, tb, grid, stages, acc_bufs, stage_bytes, st);
 }
 
 template <typename T>
-void launch_tc(const ConvArgs& a, sk_dtype dt, int grid, cudaStream_t st) {
-    if (a.k_total % 64 == 0) launch_tc_kc<T, 64>(a, dt, grid, st);
-    else if (a.k_total % 32 == 0) launch_tc_kc<T, 32>(a, dt, grid, st);
-    else launch_tc_kc<T, 16>(a, dt, grid, st);
+void launch_tc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStream_t st) {
+    if (a.k_total % 64 == 0) launch_tc_kc<T, 64>(a, dt, grid, num_sms, st);
+    else if (a.k_total % 32 == 0) launch_tc_kc<T, 32>(a, dt, grid, num_sms, st);
+    else launch_tc_kc<T, 16>(a, dt, grid, num_sms, st);
 }
 
 bool tc_ok(sk_dtype dt, int k_total, int n_total) {
@@ -1689,8 +1736,8 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
     if (a.mode != 1) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
     else grid = ctx->num_sms * (tc ? 1 : 8);
     if (tc) {
-        if (dt == SK_F16) launch_tc<__half>(a, dt, grid, st);
-        else launch_tc<__nv_bfloat16>(a, dt, grid, st);
+        if (dt == SK_F16) launch_tc<__half>(a, dt, grid, ctx->num_sms, st);
+        else launch_tc<__nv_bfloat16>(a, dt, grid, ctx->num_sms, st);
     } else {
         if (dt == SK_F32) k_gconv_simt<float><<<grid, 256, 0, st>>>(a);
         else if (dt == SK_F16) k_gconv_simt<__half><<<grid, 256, 0, st>>>(a);
