@@ -1792,7 +1792,7 @@ void gather_rows(const void* x, int c, const int* idx, const int* tiles, void* b
 // Forward (dgrad = false) or dgrad (dgrad = true; m_fwd is the FORWARD map).
 void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
-                  const void* w_kmajor, const void* residual) {
+                  const void* w_kmajor, const void* residual, float* y_accum) {
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     validate(cfg.splits >= 0, "splits must be >= 0");
     validate(cfg.kind >= 0 && cfg.kind <= 2, "unknown dataflow kind");
@@ -1858,9 +1858,9 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         a.mode = 2;
         a.n_rows_valid = m->n_out;
         a.items = (int)ceil_div(m->n_out, kItemM) * a.n_ntiles;
-        a.y = y;
-        a.residual = residual;
-        a.out_mode = 0;
+        a.y = y_accum ? (void*)y_accum : y;
+        a.residual = y_accum ? nullptr : residual;
+        a.out_mode = y_accum ? 3 : 0;
         launch_gconv(ctx, dt, a, st);
         return;
     }
@@ -1878,18 +1878,18 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         const int pairs = (a.n_tiles + 1) / 2;  // 256-row items
         if (pr->num_splits == 1) {
             a.items = pairs * a.n_ntiles;
-            a.y = y;
-            a.residual = residual;
-            a.out_mode = dt == SK_F32 ? 1 : 0;
+            a.y = y_accum ? (void*)y_accum : y;
+            a.residual = y_accum ? nullptr : residual;
+            a.out_mode = y_accum ? 3 : (dt == SK_F32 ? 1 : 0);
             launch_gconv(ctx, dt, a, st);
         } else {
             DevBuf acc;
-            float* yf = dt == SK_F32 ? static_cast<float*>(y) : nullptr;
+            float* yf = y_accum ? y_accum : (dt == SK_F32 ? static_cast<float*>(y) : nullptr);
             if (!yf) {
                 acc.alloc((size_t)y_elems * 4, st);
                 yf = acc.as<float>();
             }
-            SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
+            if (!y_accum) SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
             a.y = yf;
             if (det) {
                 // splits accumulate in order so partial sums telescope
@@ -1905,7 +1905,8 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
                 a.items = pr->num_splits * pairs * a.n_ntiles;
                 launch_gconv(ctx, dt, a, st);
             }
-            if (dt != SK_F32 || residual) convert_from_f32(dt, yf, y_elems, y, residual, st);
+            if (!y_accum && (dt != SK_F32 || residual))
+                convert_from_f32(dt, yf, y_elems, y, residual, st);
         }
         return;
     }
@@ -1913,12 +1914,12 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     // WS-based dataflows over the per-offset, 128-padded pair lists
     kmap_ensure_ws(m, st);
     DevBuf acc;
-    float* yf = dt == SK_F32 ? static_cast<float*>(y) : nullptr;
+    float* yf = y_accum ? y_accum : (dt == SK_F32 ? static_cast<float*>(y) : nullptr);
     if (!yf) {
         acc.alloc((size_t)y_elems * 4, st);
         yf = acc.as<float>();
     }
-    SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
+    if (!y_accum) SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
     a.mode = 1;
     a.ws_tile_ptr = m->ws_tile_ptr.as<int>();
     a.in_pad = m->ws_in_pad.as<int>();
@@ -1970,7 +1971,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
             }
         }
     }
-    if (dt != SK_F32 || residual) convert_from_f32(dt, yf, y_elems, y, residual, st);
+    if (!y_accum && (dt != SK_F32 || residual)) convert_from_f32(dt, yf, y_elems, y, residual, st);
 }
 
 void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, void* wt,

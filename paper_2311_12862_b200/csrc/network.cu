@@ -588,6 +588,14 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
         conv_wgrad(n->ctx, n->exec_map[i], layer_cfg(n, 2, i), n->dt, l.c_in, l.c_out, n->x_ptr[i],
                    dy.p, wgrad_flat + n->wgrad_off[i], st, accumulate);
         if (l.inputs.empty()) continue;  // no gradient w.r.t. the network input
+        if (l.inputs.size() == 1) {
+            // single producer: dgrad accumulates straight into its fp32 gradient
+            // sum in the conv epilogue (no dx round trip, no k_accum launch)
+            const int j = n->spec.index(l.inputs[0]);
+            conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, i), n->dt, l.c_in, l.c_out, dy.p,
+                         n->w[i].p, nullptr, true, st, nullptr, nullptr, n->gout[j].as<float>());
+            continue;
+        }
         conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, i), n->dt, l.c_in, l.c_out, dy.p,
                      n->w[i].p, dx.p, true, st);
         for (const std::string& pn : l.inputs) {

@@ -102,7 +102,10 @@ int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st);
 // residual (optional): y = conv(x) + residual, same shape as y (fused skip add)
 void conv_forward(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
-                  const void* w_kmajor = nullptr, const void* residual = nullptr);
+                  const void* w_kmajor = nullptr, const void* residual = nullptr,
+                  float* y_accum = nullptr);
+// y_accum (optional): ADD the result into this fp32 [n_out][n] buffer instead
+// of writing y (training: dgrad straight into the input's gradient sum)
 // W [kd][c_in][c_out] -> W^T [kd][c_out][c_in]
 void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, void* wt,
                        cudaStream_t st);
