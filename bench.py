@@ -343,6 +343,20 @@ def run_train(args, rank, world, local):
     batches = [make_scans(B, 100 * s + 1) for s in range(args.warmup + args.steps)]
     net = NetworkRunner(minkunet18(), dtype=torch.float16, weight_seed=3)
     net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large()))
+    tuned = None
+    if not args.no_tune:
+        # tune_training (tuner.cpp:162-220, workload_pattern: forward, dgrad and
+        # wgrad configs per group) on a separate sample scan, before the trainer
+        # snapshots the weights
+        tscan = make_scans(1, 900_000 + rank)[0]
+        tcs = sk.CoordSet.create(torch.from_numpy(tscan).cuda())
+        tf = torch.from_numpy(np.random.default_rng(7).standard_normal((len(tscan), 4))
+                              .astype(np.float16)).cuda()
+        t0 = time.perf_counter()
+        lat, _ = net.tune(tcs, tf, training=1, warmup=1, runs=3)
+        tuned = {"tune_s": time.perf_counter() - t0, "tuned_train_ms_per_scan": lat,
+                 "configs": {ph: [net.config(g, ph).name() for g in range(net.num_groups)]
+                             for ph in ("forward", "dgrad", "wgrad")}}
     tr = DataParallelTrainer(net, lr=1e-3, momentum=0.9)
     rng = np.random.default_rng(rank)
     prepared = []
@@ -389,7 +403,8 @@ def run_train(args, rank, world, local):
                                    "wgrad, SGD), global batch 8 synthetic ~128k-voxel scans, "
                                    "scene-sharded DP with bucketed NCCL all-reduce",
                        "global_batch": B, "parallelism": f"dp{world}",
-                       "params": int(net.num_params)},
+                       "params": int(net.num_params),
+                       "dataflow": tuned if tuned else "implicit_gemm s1 (all groups, untuned)"},
             "gpu_launches": int(_lib.lib().sk_kernel_launches() - launches0),
             "clocks": clk}), flush=True)
     if world > 1:
