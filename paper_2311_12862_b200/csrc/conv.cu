@@ -1771,6 +1771,95 @@ void pad_cols(const void* src, long long rows, int k, int k_pad, void* dst, cuda
     SK_LAUNCH_CHECK();
 }
 
+// Implicit GEMM on CUDA cores for tiny C_in (<= 8, the 4-channel stem):
+// one thread per output row keeps its C_out fp32 accumulators in registers,
+// walks the raw OS row (unsorted map) and FMAs the neighbour's C_in values
+// against W_k staged in smem as fp32. The tensor-core path would move 16 B
+// rows through a 256-row pipeline step for 8 MACs per output channel.
+template <typename T, int CI, int CO>
+__global__ void __launch_bounds__(256) k_conv_small_cin(
+    const int* __restrict__ os, int n_out, int kd, const T* __restrict__ x, const T* __restrict__ w,
+    T* __restrict__ y, const T* __restrict__ residual, float* __restrict__ y_accum) {
+    // persistent blocks: W staged once per block as fp32; 4 threads per output
+    // row, each owning CO/4 output channels (latency hiding + short tails)
+    constexpr int KD = 27, TPR = 4, CQ = CO / TPR;
+    extern __shared__ float4 wsh4[];  // [kd][CI][CO/4] fp32
+    float* wsh = reinterpret_cast<float*>(wsh4);
+    for (int i = threadIdx.x; i < kd * CI * CO; i += blockDim.x) wsh[i] = to_f(w[i]);
+    __syncthreads();
+    const int sub = threadIdx.x % TPR;
+    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) / TPR; row < n_out;
+         row += gridDim.x * blockDim.x / TPR) {
+        float acc[CQ];
+#pragma unroll
+        for (int c = 0; c < CQ; ++c) acc[c] = 0.f;
+        const int* e = os + (size_t)row * kd;
+        int nb[KD];
+#pragma unroll
+        for (int k = 0; k < KD; ++k) nb[k] = k < kd ? __ldg(e + k) : -1;
+#pragma unroll
+        for (int k = 0; k < KD; ++k) {
+            if (nb[k] < 0) continue;
+            float xv[CI];
+            if constexpr (CI == 4 && sizeof(T) == 2) {
+                const uint2 u = __ldg(reinterpret_cast<const uint2*>(x) + nb[k]);
+                const float2 a = unpack2(u.x, (T*)nullptr), b = unpack2(u.y, (T*)nullptr);
+                xv[0] = a.x; xv[1] = a.y; xv[2] = b.x; xv[3] = b.y;
+            } else {
+#pragma unroll
+                for (int c = 0; c < CI; ++c) xv[c] = to_f(x[(size_t)nb[k] * CI + c]);
+            }
+            const float4* wk = wsh4 + k * CI * (CO / 4) + sub * (CQ / 4);
+#pragma unroll
+            for (int ci = 0; ci < CI; ++ci)
+#pragma unroll
+                for (int c4 = 0; c4 < CQ / 4; ++c4) {
+                    const float4 wv = wk[ci * (CO / 4) + c4];
+                    acc[4 * c4 + 0] = fmaf(xv[ci], wv.x, acc[4 * c4 + 0]);
+                    acc[4 * c4 + 1] = fmaf(xv[ci], wv.y, acc[4 * c4 + 1]);
+                    acc[4 * c4 + 2] = fmaf(xv[ci], wv.z, acc[4 * c4 + 2]);
+                    acc[4 * c4 + 3] = fmaf(xv[ci], wv.w, acc[4 * c4 + 3]);
+                }
+        }
+        const size_t o = (size_t)row * CO + sub * CQ;
+        if (y_accum) {
+#pragma unroll
+            for (int c = 0; c < CQ; ++c) y_accum[o + c] += acc[c];
+            continue;
+        }
+#pragma unroll
+        for (int c = 0; c < CQ; ++c) {
+            const float r = residual ? to_f(residual[o + c]) : 0.f;
+            y[o + c] = from_f<T>(acc[c] + r);
+        }
+    }
+}
+
+template <typename T>
+bool conv_small_cin(const sk_kmap* m, int c_in, int c_out, const void* x, const void* w, void* y,
+                    const void* residual, float* y_accum, cudaStream_t st) {
+    auto launch = [&](auto kern) {
+        const size_t smem = (size_t)m->kd * c_in * c_out * 4;
+        static size_t configured = 0;
+        if (smem > configured) {
+            SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            configured = smem;
+        }
+        const int grid = (int)std::min<int64_t>(ceil_div(m->n_out, 64), (int64_t)m->ctx->num_sms * 8);
+        kern<<<grid, 256, smem, st>>>(
+            m->os.as<int>(), m->n_out, m->kd, static_cast<const T*>(x), static_cast<const T*>(w),
+            static_cast<T*>(y), static_cast<const T*>(residual), y_accum);
+        SK_LAUNCH_CHECK();
+        return true;
+    };
+    if (m->kd > 27) return false;
+    if (c_in == 4 && c_out == 32) return launch(k_conv_small_cin<T, 4, 32>);
+    if (c_in == 3 && c_out == 32) return launch(k_conv_small_cin<T, 3, 32>);
+    if (c_in == 1 && c_out == 32) return launch(k_conv_small_cin<T, 1, 32>);
+    return false;
+}
+
 ConvArgs base_args() {
     ConvArgs a;
     memset(&a, 0, sizeof(a));
@@ -1803,6 +1892,14 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     const size_t es = elem_size(dt);
     const long long y_elems = (long long)m->n_out * n_total;
     if (m->n_out == 0) return;
+    if (cfg.kind == SK_IMPLICIT_GEMM && !dgrad && dt != SK_F32) {
+        // tiny C_in (the 4-channel stem): implicit GEMM on CUDA cores, raw OS map
+        const bool done = dt == SK_F16
+                              ? conv_small_cin<__half>(m, c_in, c_out, x, w, y, residual, y_accum, st)
+                              : conv_small_cin<__nv_bfloat16>(m, c_in, c_out, x, w, y, residual,
+                                                              y_accum, st);
+        if (done) return;
+    }
 
     // B operand [kd][n_total][k_total] (K-major): forward -> W^T per offset;
     // dgrad -> W itself with mirrored offsets (WeightTensor::transposed,
