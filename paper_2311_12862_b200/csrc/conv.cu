@@ -885,15 +885,15 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
             if (p.trace && blockIdx.x == 0 && t == 0 && tr_n < 4096)
                 p.trace[4096 * 12 + (size_t)tr_n * 2 + 1] = clock64();
 #endif
+            // descriptor, count and list entries are independent loads issued
+            // together: one MIO round trip (the slot is released at the end of
+            // the step, so no barrier has to wait for these loads here)
             const int brow = descs[slot].brow;
-            if (brow < 0) break;
-            // count and list entries are independent loads: one MIO round trip
             const int n = cslots[slot].cnt[warp];
             uint32_t e[IT];
 #pragma unroll
             for (int i = 0; i < IT; ++i) e[i] = cslots[slot].list[warp][(sub + i * RPI) % kGroupRows];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&iempty[slot]);
+            if (brow < 0) break;
 #ifdef SK_CONV_TRACE
             const int n_do = (p.exp & 1) ? 0 : n;
 #else
@@ -940,6 +940,8 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
                     phase ^= 1;
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&iempty[slot]);
             if (++slot == kIdxRing) {
                 slot = 0;
                 ph ^= 1;
@@ -976,12 +978,11 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
             SK_TZ(0);
             mbar_wait_sleep(&cfull[slot], ph);
             SK_TZ(1);
-            if (descs[slot].brow < 0) break;
+            const int brow = descs[slot].brow;
             uint32_t real[GROUPS];
 #pragma unroll
             for (int g = 0; g < GROUPS; ++g) real[g] = cslots[slot].zmask[zw * GROUPS + g];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&iempty[slot]);
+            if (brow < 0) break;
             for (int c0 = 0; c0 < nchunks; c0 += NSL) {
                 SK_TZ(2);
                 mbar_wait_sleep(&empty[stage], phase ^ 1);
@@ -1034,6 +1035,8 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
                     phase ^= 1;
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&iempty[slot]);
             if (++slot == kIdxRing) {
                 slot = 0;
                 ph ^= 1;
