@@ -26,6 +26,7 @@
 //   k_transpose        transpose_map (kmap.cpp:290-315) as a scatter
 //   k_split_keys/...   split_and_sort + pad_map (kmap.cpp:211-288): split-local
 //                      masks -> stable radix sort on (split, ~mask) -> reorder
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "sk_internal.hpp"
@@ -118,6 +119,142 @@ __global__ void k_down_compact(const int* __restrict__ flag, const int* __restri
     int p = pos[i];
     out[p] = q[i];
     *slot_val(table, slot[i]) = (unsigned)p;  // the table now maps out-coordinate -> out row
+}
+
+// ---- 4x4x4 block index (stride-1 query path) ---------------------------------
+constexpr int kBlkEmpty = 0x7FFFFFFF;
+
+// one thread per voxel: the first thread of a block claims it (CAS on the key),
+// takes an id, fills its 64 cells with kBlkEmpty and publishes the id; the
+// others wait for the id. Cells keep the FIRST row (atomicMin), like emplace.
+__global__ void k_block_insert(const int4* __restrict__ coords, int n, ulonglong2* __restrict__ bt,
+                               uint64_t mask, int* __restrict__ dense, int* __restrict__ count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < n;
+    const int4 c = live ? coords[i] : make_int4(0, 0, 0, 0);
+    const unsigned long long key = live ? pack_key(c.x, c.y >> 2, c.z >> 2, c.w >> 2) : kEmpty;
+    // neighbouring voxels mostly share a block: one lane per distinct key in
+    // the warp inserts, the others take its id (cuts CAS/spin contention)
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    const int lane = threadIdx.x & 31;
+    unsigned bid = 0;
+    if (live && lane == leader) {
+        uint64_t s = hash_slot(key, mask);
+        for (;;) {
+            const unsigned long long prev = atomicCAS(slot_key(bt, s), (unsigned long long)kEmpty, key);
+            if (prev == (unsigned long long)kEmpty) {
+                bid = (unsigned)atomicAdd(count, 1);
+                int4* d = reinterpret_cast<int4*>(dense + (size_t)bid * 64);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    d[j] = make_int4(kBlkEmpty, kBlkEmpty, kBlkEmpty, kBlkEmpty);
+                __threadfence();
+                atomicExch(slot_val(bt, s), bid);
+                break;
+            }
+            if (prev == key) {
+                volatile unsigned* v = slot_val(bt, s);
+                while ((bid = *v) == 0xFFFFFFFFu) {
+                }
+                __threadfence();
+                break;
+            }
+            s = (s + 1) & mask;
+        }
+    }
+    bid = __shfl_sync(0xffffffffu, bid, leader);
+    if (!live) return;
+    const int local = ((c.y & 3) << 4) | ((c.z & 3) << 2) | (c.w & 3);
+    atomicMin(dense + (size_t)bid * 64 + local, i);
+}
+
+__device__ __forceinline__ int block_lookup(const ulonglong2* __restrict__ bt, uint64_t mask,
+                                            unsigned long long key) {
+    uint64_t s = hash_slot(key, mask);
+    for (;;) {
+        const ulonglong2 e = __ldg(&bt[s]);
+        if (e.x == key) return (int)(unsigned)e.y;
+        if (e.x == (unsigned long long)kEmpty) return -1;
+        s = (s + 1) & mask;
+    }
+}
+
+// Stride-1 (submanifold or generative) query over the input's block index:
+// one thread per output row; the row's neighbour blocks (at most 2 per axis
+// for K=3, 3 for K=5) are looked up once, then every offset is a 4 B load from
+// a 256 B block array that neighbouring rows share (L1). Same outputs as
+// k_kmap_query: OS tile via smem, big-endian masks, per-block counts.
+template <int K>
+__global__ void __launch_bounds__(kQB) k_kmap_query_blk(
+    const int4* __restrict__ out_coords, int n_out, const ulonglong2* __restrict__ bt,
+    uint64_t mask, const int* __restrict__ dense, int words, int* __restrict__ os,
+    unsigned long long* __restrict__ masks, int* __restrict__ blk_counts) {
+    constexpr int KD = K * K * K, H = K / 2;
+    extern __shared__ int q_sh[];
+    int* tile = q_sh;            // kQB x KD
+    int* cnt = q_sh + kQB * KD;  // KD
+    const int t = threadIdx.x;
+    const int row = blockIdx.x * kQB + t;
+    for (int k = t; k < KD; k += kQB) cnt[k] = 0;
+    __syncthreads();
+    unsigned long long m0 = 0, m1 = 0;
+    if (row < n_out) {
+        const int4 q = out_coords[row];
+        const int lx = q.y & 3, ly = q.z & 3, lz = q.w & 3;
+        const int bx = q.y >> 2, by = q.z >> 2, bz = q.w >> 2;
+        // neighbour-block ids, index (dx+1)*9 + (dy+1)*3 + (dz+1); -1 = absent
+        int bid[27];
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                for (int dz = -1; dz <= 1; ++dz) {
+                    const bool need = ((lx - H) >> 2) <= dx && dx <= ((lx + H) >> 2) &&
+                                      ((ly - H) >> 2) <= dy && dy <= ((ly + H) >> 2) &&
+                                      ((lz - H) >> 2) <= dz && dz <= ((lz + H) >> 2);
+                    int id = -1;
+                    if (need && packable(q.x, bx + dx, by + dy, bz + dz))
+                        id = block_lookup(bt, mask, pack_key(q.x, bx + dx, by + dy, bz + dz));
+                    bid[(dx + 1) * 9 + (dy + 1) * 3 + (dz + 1)] = id;
+                }
+#pragma unroll
+        for (int a = -H; a <= H; ++a)
+#pragma unroll
+            for (int b = -H; b <= H; ++b)
+#pragma unroll
+                for (int c = -H; c <= H; ++c) {
+                    const int k = ((a + H) * K + (b + H)) * K + (c + H);  // lexicographic
+                    const int px = lx + a, py = ly + b, pz = lz + c;
+                    const int sx = px >> 2, sy = py >> 2, sz = pz >> 2;  // -1, 0, +1
+                    // 27-way select keeps the ids in registers (compile-time indices)
+                    int id = -1;
+#pragma unroll
+                    for (int u = 0; u < 27; ++u)
+                        if (u == (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1)) id = bid[u];
+                    int j = -1;
+                    if (id >= 0) {
+                        const int v = __ldg(dense + (size_t)id * 64 + ((px & 3) << 4) +
+                                            ((py & 3) << 2) + (pz & 3));
+                        j = v == kBlkEmpty ? -1 : v;
+                    }
+                    tile[t * KD + k] = j;
+                    if (j >= 0) {
+                        atomicAdd(&cnt[k], 1);
+                        if (k < 64) m0 |= 1ull << ((KD < 64 ? KD : 64) - 1 - k);
+                        else m1 |= 1ull << (KD - 64 - 1 - (k - 64));
+                    }
+                }
+    } else {
+        for (int k = 0; k < KD; ++k) tile[t * KD + k] = -1;
+    }
+    __syncthreads();
+    int* dst = os + (size_t)blockIdx.x * kQB * KD;
+    for (int i = t; i < kQB * KD; i += kQB) __stcs(dst + i, tile[i]);
+    __stcs(masks + (size_t)row * words, m0);
+    if (words == 2) __stcs(masks + (size_t)row * words + 1, m1);
+    for (int k = t; k < KD; k += kQB) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
 }
 
 // resolve a probe whose first slot (key + row) is already loaded
@@ -471,12 +608,70 @@ __global__ void k_iota(int* __restrict__ v, int n) {
 // load factor <= 1/4: short linear-probing chains keep warps convergent (a
 // warp waits for its longest chain); 16 B slots -> 64 n..128 n bytes, L2-resident
 int64_t pow2_cap(int64_t n) {
+    // slots per key (load factor 1/m); SK_HASH_SLOTS overrides for experiments
+    static const int64_t m = [] {
+        const char* e = getenv("SK_HASH_SLOTS");
+        return e ? std::max<int64_t>(2, atoll(e)) : 4;
+    }();
     int64_t c = 64;
-    while (c < 4 * n) c <<= 1;
+    while (c < m * n) c <<= 1;
     return c;
 }
 
+void coords_build_blocks(sk_coords* c, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (c->has_blocks) return;
+    int64_t cap = 64;
+    while (cap < 2 * (int64_t)c->n) cap <<= 1;  // n_blocks <= n: load <= 1/2 worst case
+    c->bcap = cap;
+    c->btable.alloc((size_t)cap * 16, st);
+    SK_CUDA(cudaMemsetAsync(c->btable.p, 0xFF, c->btable.bytes, st));
+    c->bdense.alloc((size_t)std::max(c->n, 1) * 64 * 4, st);  // cells initialised per block
+    c->bcount.alloc(4, st);
+    SK_CUDA(cudaMemsetAsync(c->bcount.p, 0, 4, st));
+    if (c->n > 0) {
+        k_block_insert<<<(int)ceil_div(c->n, 256), 256, 0, st>>>(
+            c->coords.as<int4>(), c->n, c->btable.as<ulonglong2>(), (uint64_t)cap - 1,
+            c->bdense.as<int>(), c->bcount.as<int>());
+        SK_LAUNCH_CHECK();
+    }
+    c->has_blocks = true;
+}
+
+// stride-1, non-transposed, 3-D, K in {3, 5}, large input sets: the block-
+// index query. Measured: its extra build pass costs more than it saves below
+// ~0.5M input voxels (MinkUNet scan: maps 0.72 -> 0.82 ms), above it the query
+// is ~12% faster (1M-voxel sweep point). SK_KMAP_BLOCKS=0/1 forces off/on.
+bool use_block_query(const sk_kmap* m) {
+    static const int mode = [] {
+        const char* e = getenv("SK_KMAP_BLOCKS");
+        return e ? atoi(e) : -1;
+    }();
+    const bool shape = !m->transposed && m->dims == 3 && (m->kernel == 3 || m->kernel == 5) &&
+                       m->stride[0] == 1 && m->stride[1] == 1 && m->stride[2] == 1;
+    if (!shape || mode == 0) return false;
+    return mode == 1 || m->n_in >= (1 << 19);
+}
+
 void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_t st) {
+    if (use_block_query(m)) {
+        coords_build_blocks(in, st);
+        const int grid = m->rows_pad / kQB;
+        const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
+        auto run = [&](auto kern) {
+            if (smem > 48 * 1024)
+                SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+            kern<<<grid, kQB, smem, st>>>(out_coords, m->n_out, in->btable.as<ulonglong2>(),
+                                          (uint64_t)in->bcap - 1, in->bdense.as<int>(), m->words,
+                                          m->os.as<int>(), m->masks.as<unsigned long long>(),
+                                          m->blk_counts.as<int>());
+            SK_LAUNCH_CHECK();
+        };
+        if (m->kernel == 3) run(k_kmap_query_blk<3>);
+        else run(k_kmap_query_blk<5>);
+        return;
+    }
     const int grid = m->rows_pad / kQB;
     const uint64_t mask = (uint64_t)in->cap - 1;
     const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;

@@ -47,6 +47,13 @@ struct sk_coords : sk::Refcounted {
     sk::DevBuf table;
     int64_t cap = 0;
     bool has_table = false;
+    // 4x4x4 block index for stride-1 queries (built on first use): block hash
+    // {u64 block key, u32 block id} [bcap] and per block the 64 rows of its
+    // cells (INT_MAX = empty) -- one hash probe per neighbour BLOCK instead of
+    // per neighbour voxel
+    sk::DevBuf btable, bdense, bcount;
+    int64_t bcap = 0;
+    bool has_blocks = false;
     std::mutex mu;
     // children: downsampled sets by stride (owned), maps by key (owned)
     std::map<std::tuple<int, int, int>, sk_coords*> down;

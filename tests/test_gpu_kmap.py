@@ -159,3 +159,47 @@ def test_large_scan_matches_reference(sk, reference):
     assert np.array_equal(got[0][3], want[0][3]) and np.array_equal(got[0][2], want[0][2])
     o = sk.build_out_coords(c, 2)
     assert np.array_equal(o.numpy(), reference.out_coords(3, c_np, [2, 2, 2]))
+
+
+BLOCK_CHECK = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle.oracle import Reference
+from paper_2311_12862_b200 import sparse as sk
+from paper_2311_12862_b200.synth import random_instance_coords, lidar_scan
+ref = Reference()
+cases = [(1, 300, 3, 1, 12), (4, 200, 5, 1, 12), (8, 20000, 3, 1, 60), (11, 6000, 5, 3, 25),
+         (12, 3000, 3, 2, 400)]
+for seed, n, k, batches, rng in cases:
+    c_np = random_instance_coords(seed, n, -rng, rng, batches)
+    c = sk.CoordSet.create(c_np)
+    o = sk.build_out_coords(c, 2)  # a different output set, still stride 1
+    o_np = o.numpy()
+    for out, out_np in ((c, c_np), (o, o_np)):
+        m = sk.build_kmap(c, out, k, 1)
+        rm = ref.kmap(3, k, c_np, out_np, [1, 1, 1])
+        assert np.array_equal(m.os()[0], rm.os()[0]), (seed, k)
+        assert np.array_equal(m.os()[1], rm.os()[1]), (seed, k)
+        ptr, inn, outs = m.ws()
+        for kk in range(rm.kd):
+            ri, ro = rm.pairs(kk)
+            assert np.array_equal(inn[ptr[kk]:ptr[kk + 1]], ri)
+            assert np.array_equal(outs[ptr[kk]:ptr[kk + 1]], ro)
+s_np = lidar_scan(60_000, seed=5)
+s = sk.CoordSet.create(s_np)
+m, rm = sk.build_kmap(s, s, 3, 1), ref.kmap(3, 3, s_np, s_np, [1, 1, 1])
+assert np.array_equal(m.os()[0], rm.os()[0]) and np.array_equal(m.os()[1], rm.os()[1])
+print("blocks ok")
+'''
+
+
+def test_block_index_query_matches_reference(reference):
+    """The 4x4x4 block-index query (used for stride-1 maps on >= 0.5M-voxel
+    sets) forced on small instances: K=3/5, batches, negative coordinates,
+    output set != input set, a LiDAR-shaped scan."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", BLOCK_CHECK, root], capture_output=True, text=True,
+                       env={**os.environ, "SK_KMAP_BLOCKS": "1"}, timeout=600)
+    assert r.returncode == 0 and "blocks ok" in r.stdout, r.stdout + r.stderr
