@@ -1442,16 +1442,22 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int 
             const long long v = v0 + g / kWgStepsPerTile;
             return (v % NT) * kTileWS + (g % kWgStepsPerTile) * kWgK + kk;
         };
-        int pre[8];
+        // indices for the next group of 8 steps are loaded while the current
+        // group is issued (no register shifting: a shift would wait for each
+        // load one step later, i.e. a lookahead of one)
+        int cur[8], nxt[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pre[i] = i < nsteps ? __ldg(idx + pair_of(i)) : -1;
+        for (int i = 0; i < 8; ++i) cur[i] = i < nsteps ? __ldg(idx + pair_of(i)) : -1;
         int stage = 0;
         uint32_t phase = 0;
-        for (long long g = 0; g < nsteps; ++g) {
-            const int row = pre[0];
+        for (long long g0 = 0; g0 < nsteps; g0 += 8) {
 #pragma unroll
-            for (int i = 0; i < 7; ++i) pre[i] = pre[i + 1];
-            pre[7] = g + 8 < nsteps ? __ldg(idx + pair_of(g + 8)) : -1;
+            for (int i = 0; i < 8; ++i) nxt[i] = g0 + 8 + i < nsteps ? __ldg(idx + pair_of(g0 + 8 + i)) : -1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long long g = g0 + i;
+            if (g >= nsteps) break;
+            const int row = cur[i];
             const long long v = v0 + g / kWgStepsPerTile;
             const long long mn = v / NT;
             const int c_lo = is_x ? (int)(mn / p.n_tiles) * 128 : (int)(mn % p.n_tiles) * BN;
@@ -1472,6 +1478,9 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int 
                 phase ^= 1;
             }
         }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+        }
     } else if (warp == 4) {
         // MMA issuer: runs of tiles with the same (mn tile, offset) accumulate
         const uint32_t idesc = (1u << 4) | (Fmt<T>::v << 7) | (Fmt<T>::v << 10) | (1u << 15) |
@@ -1486,7 +1495,7 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int 
             const long long mn = v / NT;
             const long long key = mn * (p.kd + 1) + wg_offset_of(p.tile_ptr, p.kd, (int)(v % NT));
             if (key != cur_key) {
-                if (run >= 0 && lane == 0) tc_commit(&tfull[acc]);
+                if (run >= 0) tc_commit_elect(&tfull[acc]);
                 ++run;
                 acc = run & 1;
                 mbar_wait(&tempty[acc], (uint32_t)(((run >> 1) & 1) ^ 1));
@@ -1497,24 +1506,33 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int 
             for (int sidx = 0; sidx < kWgStepsPerTile; ++sidx) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                if (lane == 0) {
+                {
+                    // warp-uniform issue, elected lane inside the asm (descriptors
+                    // stay in uniform registers); +2048 B per K=16 step
                     const uint32_t sa = smem_u32(smem) + (uint32_t)stage * stage_bytes;
+                    const uint64_t da = mnmajor_desc(sa), db = mnmajor_desc(sa + a_bytes);
 #pragma unroll
                     for (int k16 = 0; k16 < kWgK / 16; ++k16) {
-                        tc_mma_f16(tmem + acc * (uint32_t)BN, mnmajor_desc(sa + k16 * 2048),
-                                   mnmajor_desc(sa + a_bytes + k16 * 2048), idesc, accumulate);
+                        asm volatile(
+                            "{\n.reg .pred E, p;\n"
+                            "elect.sync _|E, 0xffffffff;\n"
+                            "setp.ne.b32 p, %4, 0;\n"
+                            "@E tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+                            "}\n" ::"r"(tmem + acc * (uint32_t)BN),
+                            "l"(da + (uint64_t)(k16 * 128)), "l"(db + (uint64_t)(k16 * 128)),
+                            "r"(idesc), "r"(accumulate)
+                            : "memory");
                         accumulate = 1;
                     }
-                    tc_commit(&empty[stage]);
+                    tc_commit_elect(&empty[stage]);
                 }
-                __syncwarp();
                 if (++stage == stages) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
         }
-        if (run >= 0 && lane == 0) tc_commit(&tfull[acc]);
+        if (run >= 0) tc_commit_elect(&tfull[acc]);
         __syncwarp();
     } else {
         // epilogue: TMEM lane = channel ci of the M tile; flush a run with red.add
