@@ -59,6 +59,8 @@ struct Roles {
     static constexpr int kEpiWarp0 = PW + 4;            // 4 epilogue warps
     static constexpr int kThreads = (PW + 8) * 32;
 };
+// compacted list entries: (A row << kRowBits) | row in the producer group (<= 64)
+constexpr uint32_t kRowBits = 6, kRowMask = 63;
 constexpr int kTmaWarps = 4;          // warps 0-3: TMA gather4 producers (TMA variant)
 constexpr int kZeroWarps = 2;
 constexpr int kMaxStages = 10;       // launch_tc_kc caps the stage count
@@ -501,7 +503,7 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
 
 // Per ring slot, built by the index warp from the slot's 256 row indices:
 // for each producer warp's 16-row group the list of its real rows
-// ((idx << 5) | row-in-group) and their count, and the real-row bitmask of
+// ((idx << kRowBits) | row-in-group) and their count, and the real-row bitmask of
 // every 32-row group (zero warps). Moves the ballot/compaction smem traffic
 // off the producers' per-step critical path (their LDS would queue behind
 // the SM's LDGSTS backlog in the MIO pipe).
@@ -533,7 +535,7 @@ __device__ __forceinline__ void compact_slot(const int* ring, CSlot<PW>& cs, int
     uint32_t* L = cs.list[lane / LPG];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-        if (bits >> i & 1u) L[k++] = ((uint32_t)v[i] << 5) | (uint32_t)((lane % LPG) * 8 + i);
+        if (bits >> i & 1u) L[k++] = ((uint32_t)v[i] << kRowBits) | (uint32_t)((lane % LPG) * 8 + i);
     if (lane % LPG == LPG - 1) cs.cnt[lane / LPG] = incl;
     uint32_t m = bits << ((lane & 3) * 8);
     m |= __shfl_xor_sync(0xffffffffu, m, 1);
@@ -552,7 +554,7 @@ struct alignas(16) StepDesc {
 // warp 0 loads B with one 2D TMA tile. USE_TMA = false: warps 0-7 gather with
 // 16 B cp.async (reference path, kept for A/B measurement).
 template <typename T, int KC, bool USE_TMA, int SLABS, int PW>
-__global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
+__global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
     k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const ConvArgs p, int stages, int acc_bufs) {
     constexpr int kProducerWarps = Roles<PW>::kProducerWarps;
@@ -924,10 +926,10 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 8 ? 2 : 1)
 #pragma unroll
                     for (int i = 0; i < IT; ++i) {
                         if (sub + i * RPI >= n_do) break;
-                        const uint32_t r = row0 + (e[i] & 31u);            // row within the half
+                        const uint32_t r = row0 + (e[i] & kRowMask);       // row within the half
                         const uint32_t off = r * RB + (uint32_t)q * 16;
                         cp_async16(sa_w + (off ^ (((off >> 7) & SWB) << 4)),
-                                   src_c + (size_t)(e[i] >> 5) * row_bytes, nbytes);
+                                   src_c + (size_t)(e[i] >> kRowBits) * row_bytes, nbytes);
                     }
                 }
                 cp_async_arrive_noinc(&full[stage]);
