@@ -117,6 +117,7 @@ __host__ __device__ inline int64_t floor_div(int64_t a, int64_t b) {
 
 // ---- PTX wrappers (sm_100a) ----------------------------------------------------
 #if defined(__CUDACC__)
+constexpr uint32_t kSuspendHintNs = 1000000;  // 1 ms: effectively 'until the phase completes'
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -130,16 +131,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp stays suspended until
+// the phase completes (or the hint expires) instead of re-polling, so waiting
+// warps do not compete for issue slots and MIO bandwidth
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendHintNs)
         : "memory");
 }
 // Waits of warps that are not on the tensor-core critical path: probe, then
