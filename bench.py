@@ -42,6 +42,18 @@ WORKLOAD = ("MinkUNet-18 inference (SURVEY App. B skeleton: 77 convs, 14 map gro
             "maps per scan")
 
 
+WORKLOAD_SECOND = ("SECOND/CenterPoint sparse 3D encoder (SURVEY App. A: subm 4->16, 16->16, three "
+                   "[s2 conv + 2 subm] stages at 32/64/64, s2 conv 64->128; kernel maps reused "
+                   "across each stride level) on a Waymo-shaped synthetic scan (planar_patches "
+                   "n=275k, extent 8, voxel 0.1x0.1x0.15 m, ~150k voxels), fp16 in / fp32 "
+                   "accumulate, cold maps per scan")
+
+
+def model_for(workload):
+    from paper_2311_12862_b200.models import minkunet18, second_encoder
+    return second_encoder() if workload == "second" else minkunet18()
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -50,8 +62,10 @@ def peaks():
                 "fallback": True}
 
 
-def make_scans(count, seed0, n_points=200_000):
-    from paper_2311_12862_b200.synth import lidar_scan
+def make_scans(count, seed0, n_points=200_000, workload="infer"):
+    from paper_2311_12862_b200.synth import lidar_scan, waymo_scan
+    if workload == "second":
+        return [waymo_scan(seed=seed0 + i) for i in range(count)]
     return [lidar_scan(n_points, seed=seed0 + i) for i in range(count)]
 
 
@@ -93,14 +107,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_time(coords, feats, threads, max_steps=1):
+def cpu_reference_time(coords, feats, threads, max_steps=1, workload="infer"):
     """Reference NetworkRunner::forward (cold) on the host cores; seconds/scan."""
     from oracle.oracle import Reference
-    from paper_2311_12862_b200.models import minkunet18, spec_text
+    from paper_2311_12862_b200.models import spec_text
     ref = Reference()
     times = []
     for i in range(max_steps):
-        net = ref.network(3, spec_text(minkunet18()), prec=0, threads=threads, weight_seed=3)
+        net = ref.network(3, spec_text(model_for(workload)), prec=0, threads=threads, weight_seed=3)
         net.set_input(coords[i % len(coords)], feats[i % len(feats)].astype(np.float64), prec=0)
         t0 = time.perf_counter()
         net.forward()
@@ -113,14 +127,15 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    scans = make_scans(max(1, min(args.steps, 4)), 1000)
+    wl = args.workload if args.workload == "second" else "infer"
+    scans = make_scans(max(1, min(args.steps, 4)), 1000, workload=wl)
     feats = [np.random.default_rng(i).standard_normal((len(c), 4)).astype(np.float32)
              for i, c in enumerate(scans)]
     # bounded sample: full cold scans, as many as fit ~120 s (at least 1)
-    t_one = cpu_reference_time(scans, feats, threads, 1)[0]
+    t_one = cpu_reference_time(scans, feats, threads, 1, wl)[0]
     n = max(1, min(args.steps, int(120.0 / max(t_one, 1e-3))))
     times = [t_one] + (cpu_reference_time(scans[1:] + scans[:1], feats[1:] + feats[:1], threads,
-                                          n - 1) if n > 1 else [])
+                                          n - 1, wl) if n > 1 else [])
     sec = statistics.median(times)
     value = 1.0 / sec
     line = {
@@ -128,11 +143,12 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": len(times), "steps_requested": args.steps, "warmup": 0,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "voxels_per_scan": int(np.mean([len(c) for c in scans])),
+        "config": {"workload": WORKLOAD_SECOND if wl == "second" else WORKLOAD,
+                   "voxels_per_scan": int(np.mean([len(c) for c in scans])),
                    "impl_detail": "compiled reference NetworkRunner::forward, default GGS "
                                   "assignment, f32, cold maps"},
         "cpu_baseline": {"value": value, "unit": "scans/s", "cores": threads, "kind": "reference",
-                         "sample": f"{len(times)} cold MinkUNet-18 scans (median)"},
+                         "sample": f"{len(times)} cold {'SECOND encoder' if wl == 'second' else 'MinkUNet-18'} scans (median)"},
         "e2e": {"value": value, "unit": "scans/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -147,9 +163,10 @@ def main():
     ap.add_argument("--impl", default="sk200", choices=["sk200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--splits", type=int, default=1)
-    ap.add_argument("--workload", default="infer", choices=["infer", "train"],
-                    help="infer: configs[1] MinkUNet inference (default); train: configs[3] "
-                         "mixed-precision DP training step, global batch 8 scans")
+    ap.add_argument("--workload", default="infer", choices=["infer", "second", "train"],
+                    help="infer: configs[1] MinkUNet inference (default); second: configs[2] "
+                         "SECOND encoder inference; train: configs[3] mixed-precision DP "
+                         "training step, global batch 8 scans")
     ap.add_argument("--no-tune", action="store_true",
                     help="skip the per-group autotuner; use implicit GEMM --splits everywhere")
     args = ap.parse_args()
@@ -172,10 +189,11 @@ def main():
     from paper_2311_12862_b200.network import NetworkRunner
 
     n_scans = args.warmup + args.steps
-    scans = make_scans(n_scans, 1 + rank * 10000)
+    wl = args.workload
+    scans = make_scans(n_scans, 1 + rank * 10000, workload=wl)
     rng = np.random.default_rng(rank)
     feats = [rng.standard_normal((len(c), 4)).astype(np.float16) for c in scans]
-    net = NetworkRunner(minkunet18(), dtype=torch.float16, weight_seed=3)
+    net = NetworkRunner(model_for(wl), dtype=torch.float16, weight_seed=3)
     net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, args.splits, sk.tile_large()))
     dev_coords = [torch.from_numpy(c).cuda() for c in scans]
     dev_feats = [torch.from_numpy(f).cuda() for f in feats]
@@ -183,7 +201,7 @@ def main():
     if not args.no_tune:
         # per-group autotuner (tune_inference, tuner.cpp:134-160) on a separate
         # sample scan; the chosen configs then serve every timed scan
-        tscan = make_scans(1, 900_000 + rank)[0]
+        tscan = make_scans(1, 900_000 + rank, workload=wl)[0]
         tcs = sk.CoordSet.create(torch.from_numpy(tscan).cuda())
         tf = torch.from_numpy(rng.standard_normal((len(tscan), 4)).astype(np.float16)).cuda()
         t0 = time.perf_counter()
@@ -282,10 +300,12 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            t = cpu_reference_time(scans[:1], [f.astype(np.float32) for f in feats[:1]], threads, 1)
+            t = cpu_reference_time(scans[:1], [f.astype(np.float32) for f in feats[:1]], threads,
+                                   1, wl)
             cpu = {"value": 1.0 / t[0], "unit": "scans/s", "cores": threads, "kind": "reference",
-                   "sample": "1 cold MinkUNet-18 forward on the first timed scan, f32, "
-                             "compiled reference NetworkRunner (default GGS assignment)"}
+                   "sample": f"1 cold {'SECOND encoder' if wl == 'second' else 'MinkUNet-18'} "
+                             "forward on the first timed scan, f32, compiled reference "
+                             "NetworkRunner (default GGS assignment)"}
         except Exception as e:  # reported, never fatal for the GPU line
             cpu = {"value": None, "unit": "scans/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -296,7 +316,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD,
+            "config": {"workload": WORKLOAD_SECOND if wl == "second" else WORKLOAD,
                        "voxels_per_scan": int(np.mean([len(c) for c in scans])),
                        "parallelism": f"scene-sharded dp{world} (no collective)",
                        "dataflow": (tuned if tuned else
