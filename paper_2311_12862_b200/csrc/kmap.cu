@@ -521,6 +521,25 @@ __global__ void k_split_keys(const int* __restrict__ os, int n, int kd, int ns,
     vals[i] = r;
 }
 
+// 32-bit sort keys straight from the query's full-width masks (kd <= 64,
+// W + split bits <= 32): split s's local big-endian mask is the bit field
+// [kd-e, kd-b) of the row mask -- 8 B per row instead of re-reading the
+// kd-wide OS row, and half the radix-sort key traffic.
+__global__ void k_split_keys32(const unsigned long long* __restrict__ masks, int n, int kd, int ns,
+                               const int* __restrict__ begin, int W,
+                               unsigned* __restrict__ keys, int* __restrict__ vals) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * ns) return;
+    const int s = (int)(i / n), r = (int)(i % n);
+    const int b = begin[s], e = begin[s + 1], w = e - b;
+    const unsigned long long m = masks[r];  // words == 1: column j <-> bit kd-1-j
+    const unsigned local = (unsigned)((m >> (kd - e)) & ((1ull << w) - 1));
+    unsigned key = ~local & ((1u << w) - 1);
+    if (ns > 1) key |= (unsigned)s << W;
+    keys[i] = key;
+    vals[i] = r;
+}
+
 __device__ void row_reorder(const int* __restrict__ os, int n, int kd, int rows_pad,
                             const int* __restrict__ begin, const int* __restrict__ word_off,
                             const int* __restrict__ order, int* __restrict__ entries,
@@ -972,7 +991,22 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
                                             (int)tot, 0, end_bit, st);
             SK_LAUNCH_CHECK();
         };
-        if (W <= 64) {
+        if (kd <= 64 && W + (ns > 1 ? sbits : 0) <= 32) {
+            const int end_bit = W + (ns > 1 ? sbits : 0);
+            k_split_keys32<<<g, 256, 0, st>>>(m->masks.as<unsigned long long>(), n, kd, ns,
+                                              d_begin.as<int>(), W, k_in.as<unsigned>(),
+                                              v_in.as<int>());
+            SK_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in.as<unsigned>(), k_out.as<unsigned>(),
+                                            v_in.as<int>(), order.as<int>(), (int)tot, 0, end_bit,
+                                            st);
+            tmp.alloc(tb, st);
+            cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.as<unsigned>(), k_out.as<unsigned>(),
+                                            v_in.as<int>(), order.as<int>(), (int)tot, 0, end_bit,
+                                            st);
+            SK_LAUNCH_CHECK();
+        } else if (W <= 64) {
             sort_pass(0, std::min(64, W + (ns > 1 ? sbits : 0)), nullptr, order.as<int>());
         } else {
             // one split wider than 64 columns (K=5, s=1): stable LSD over the
