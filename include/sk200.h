@@ -44,7 +44,9 @@ typedef enum {
     SK_ERR_INTERNAL = 5
 } sk_status;
 
-typedef enum { SK_F32 = 0, SK_F16 = 1, SK_BF16 = 2 } sk_dtype;
+/* SK_F64: quantize features only (the reference's f64 Features); conv paths
+ * take F32 / F16 / BF16. */
+typedef enum { SK_F32 = 0, SK_F16 = 1, SK_BF16 = 2, SK_F64 = 3 } sk_dtype;
 
 /* DataflowKind (exec.hpp:59) */
 typedef enum {
@@ -115,6 +117,23 @@ const int32_t* sk_coords_device_ptr(const sk_coords* c);
 sk_status sk_coords_stride_tag(const sk_coords* c, int32_t out[3]);
 /* D2H copy of the coordinates (syncs `stream`). */
 sk_status sk_coords_export(const sk_coords* c, int32_t* h_coords, void* stream);
+
+/* quantize (tensor.cpp:87-142, the step before the path): floor(raw / voxel)
+ * per axis (toward -inf), first-appearance dedup (emplace order). d_raw:
+ * device double[m][dims]; d_batch: device int32[m] or NULL (batch 0);
+ * d_point_rows (optional, device int32[m]) receives each point's output row.
+ * Non-finite input or a voxel outside the packable range -> SK_ERR_VALIDATION.
+ * Reads back the output count (one sync). */
+sk_status sk_quantize(sk_ctx* ctx, int dims, int m, const double* d_raw, const int32_t* d_batch,
+                      const double voxel[3], void* stream, sk_coords** out,
+                      int32_t* d_point_rows);
+/* Features of a quantized set (DedupRule, tensor.hpp:45): rule 0 = first
+ * (the first point's features), 1 = mean; channels 0 = one occupancy channel
+ * of ones. d_feats: device double[m][channels]; d_out: device [n][max(1,
+ * channels)] of dtype (caller-owned). */
+sk_status sk_quantize_features(sk_ctx* ctx, int m, int channels, const double* d_feats,
+                               const int32_t* d_point_rows, int n, int rule, sk_dtype dtype,
+                               void* d_out, void* stream);
 
 /* build_out_coords (kmap.cpp:73-94): stride 1 returns the same set
  * (retained); stride > 1 returns unique(floor_div(p, s)) in first-appearance

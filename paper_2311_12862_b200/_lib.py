@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("SK200_LIB") or os.path.join(PKG, "libsk200.so")
 SYMBOLS = [
     "sk_last_error", "sk_version", "sk_kernel_launches", "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_deterministic",
     "sk_coords_create", "sk_coords_create_host", "sk_coords_retain", "sk_coords_release",
+    "sk_quantize", "sk_quantize_features",
     "sk_coords_n", "sk_coords_dims", "sk_coords_id", "sk_coords_device_ptr",
     "sk_coords_stride_tag", "sk_coords_export", "sk_out_coords", "sk_kmap_build",
     "sk_kmap_transpose", "sk_kmap_prepare", "sk_kmap_retain", "sk_kmap_release",
@@ -95,6 +96,10 @@ def lib():
         "sk_coords_stride_tag": ([vp, i32p], C.c_int),
         "sk_coords_export": ([vp, vp, vp], C.c_int),
         "sk_out_coords": ([vp, vp, i32p, vp, pp], C.c_int),
+        "sk_quantize": ([vp, C.c_int, C.c_int, vp, vp, C.POINTER(C.c_double), vp, pp, vp],
+                        C.c_int),
+        "sk_quantize_features": ([vp, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, vp,
+                                  vp], C.c_int),
         "sk_kmap_build": ([vp, vp, vp, C.c_int, i32p, C.c_int, vp, pp], C.c_int),
         "sk_kmap_transpose": ([vp, vp, vp, pp], C.c_int),
         "sk_kmap_prepare": ([vp, vp, C.c_int, C.c_int, vp], C.c_int),

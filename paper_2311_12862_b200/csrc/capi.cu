@@ -153,6 +153,27 @@ sk_status sk_coords_create_host(sk_ctx* ctx, int dims, int n, const int32_t* h_c
     return guard([&] { *out = make_coords(ctx, dims, n, h_coords, true, stride_tag, S(stream)); });
 }
 
+sk_status sk_quantize(sk_ctx* ctx, int dims, int m, const double* d_raw, const int32_t* d_batch,
+                      const double voxel[3], void* stream, sk_coords** out,
+                      int32_t* d_point_rows) {
+    return guard([&] {
+        sk::validate(ctx && out && voxel, "null argument");
+        sk::validate(m == 0 || d_raw, "null raw points");
+        *out = sk::coords_quantize(ctx, dims, m, d_raw, d_batch, voxel, d_point_rows, S(stream));
+    });
+}
+
+sk_status sk_quantize_features(sk_ctx* ctx, int m, int channels, const double* d_feats,
+                               const int32_t* d_point_rows, int n, int rule, sk_dtype dtype,
+                               void* d_out, void* stream) {
+    return guard([&] {
+        sk::validate(ctx != nullptr, "null context");
+        sk::validate(n == 0 || d_out, "null output");
+        sk::validate(channels == 0 || n == 0 || d_feats, "null features");
+        sk::quantize_features(m, channels, d_feats, d_point_rows, n, rule, dtype, d_out, S(stream));
+    });
+}
+
 sk_status sk_coords_retain(sk_coords* c) {
     return guard([&] {
         sk::validate(c != nullptr, "null coords");
@@ -336,6 +357,8 @@ sk_status sk_conv_forward(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg,
                           void* stream) {
     return guard([&] {
         sk::validate(ctx && map && cfg, "null argument");
+        sk::validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
+                     "convolution dtype must be f32, f16 or bf16");
         sk::conv_forward(ctx, map, *cfg, dtype, c_in, c_out, d_x, d_w, d_y, false, S(stream));
     });
 }
@@ -345,6 +368,8 @@ sk_status sk_conv_dgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, s
                         void* stream) {
     return guard([&] {
         sk::validate(ctx && map && cfg, "null argument");
+        sk::validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
+                     "convolution dtype must be f32, f16 or bf16");
         sk::conv_forward(ctx, map, *cfg, dtype, c_in, c_out, d_dy, d_w, d_dx, true, S(stream));
     });
 }
@@ -354,6 +379,8 @@ sk_status sk_conv_wgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, s
                         void* stream) {
     return guard([&] {
         sk::validate(ctx && map && cfg, "null argument");
+        sk::validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
+                     "convolution dtype must be f32, f16 or bf16");
         sk::conv_wgrad(ctx, map, *cfg, dtype, c_in, c_out, d_x, d_dy, d_dw, S(stream));
     });
 }

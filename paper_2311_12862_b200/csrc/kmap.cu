@@ -257,6 +257,102 @@ __global__ void __launch_bounds__(kQB) k_kmap_query_blk(
     for (int k = t; k < KD; k += kQB) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
 }
 
+
+// ---- quantize (tensor.cpp:87-142): floor(raw / voxel) + first-appearance dedup
+// err bit 1: non-finite coordinate, bit 2: outside the packable range
+__global__ void k_quant_insert(const double* __restrict__ raw, const int* __restrict__ batch,
+                               int m, int dims, double vx, double vy, double vz,
+                               ulonglong2* __restrict__ table, uint64_t mask,
+                               int* __restrict__ slot_out, int4* __restrict__ q_out,
+                               int* __restrict__ err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const double v[3] = {vx, vy, vz};
+    long long c[3] = {0, 0, 0};
+    bool finite = true;
+    for (int d = 0; d < dims; ++d) {
+        const double r = raw[(size_t)i * dims + d];
+        finite &= isfinite(r);
+        c[d] = finite ? (long long)floor(r / v[d]) : 0;
+    }
+    const int b = batch ? batch[i] : 0;
+    if (!finite) {
+        atomicOr(err, 1);
+        slot_out[i] = -1;
+        return;
+    }
+    if (!packable(b, (int)max(min(c[0], (long long)INT_MAX), (long long)INT_MIN),
+                  (int)max(min(c[1], (long long)INT_MAX), (long long)INT_MIN),
+                  (int)max(min(c[2], (long long)INT_MAX), (long long)INT_MIN)) ||
+        c[0] != (int)c[0] || c[1] != (int)c[1] || c[2] != (int)c[2]) {
+        atomicOr(err, 2);
+        slot_out[i] = -1;
+        return;
+    }
+    const int4 q = make_int4(b, (int)c[0], (int)c[1], (int)c[2]);
+    q_out[i] = q;
+    const unsigned long long key = pack_key(q.x, q.y, q.z, q.w);
+    uint64_t s = hash_slot(key, mask);
+    for (;;) {
+        const unsigned long long prev = atomicCAS(slot_key(table, s), (unsigned long long)kEmpty, key);
+        if (prev == (unsigned long long)kEmpty || prev == key) {
+            atomicMin(slot_val(table, s), (unsigned)i);
+            slot_out[i] = (int)s;
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+// point -> output row (after compaction the table maps key -> out row)
+__global__ void k_point_rows(const int* __restrict__ slot, const ulonglong2* __restrict__ table,
+                             int m, int* __restrict__ rows) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    rows[i] = (int)*slot_val(const_cast<ulonglong2*>(table), slot[i]);
+}
+
+// DedupRule::first: the first point of each row (min point index)
+__global__ void k_first_point(const int* __restrict__ rows, int m, int* __restrict__ first) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) atomicMin(first + rows[i], i);
+}
+
+template <typename T>
+__global__ void k_quant_feats_first(const double* __restrict__ feats, int channels,
+                                    const int* __restrict__ first, int n, T* __restrict__ out) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * channels) return;
+    const int r = (int)(t / channels), c = (int)(t % channels);
+    out[t] = (T)feats[(size_t)first[r] * channels + c];
+}
+
+// DedupRule::mean: f64 sums and counts (the reference's running mean is the
+// same mean up to f64 rounding)
+__global__ void k_quant_sum(const double* __restrict__ feats, int channels,
+                            const int* __restrict__ rows, int m, double* __restrict__ sum,
+                            int* __restrict__ count) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)m * channels) return;
+    const int i = (int)(t / channels), c = (int)(t % channels);
+    atomicAdd(sum + (size_t)rows[i] * channels + c, feats[t]);
+    if (c == 0) atomicAdd(count + rows[i], 1);
+}
+
+template <typename T>
+__global__ void k_quant_mean(const double* __restrict__ sum, const int* __restrict__ count,
+                             int channels, int n, T* __restrict__ out) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * channels) return;
+    out[t] = (T)(sum[t] / (double)count[t / channels]);
+}
+
+template <typename T>
+__global__ void k_fill(T* __restrict__ out, long long n, double v) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = (T)v;
+}
+
 // resolve a probe whose first slot (key + row) is already loaded
 __device__ __forceinline__ int probe(const ulonglong2* __restrict__ table, uint64_t mask,
                                      unsigned long long key, uint64_t s, ulonglong2 first) {
@@ -802,6 +898,116 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     SK_LAUNCH_CHECK();
     out->has_table = true;
     return out;
+}
+
+
+sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, const int32_t* batch,
+                           const double voxel[3], int32_t* point_rows, cudaStream_t st) {
+    validate(dims == 2 || dims == 3, "dims must be 2 or 3");
+    validate(m >= 0, "negative point count");
+    for (int d = 0; d < dims; ++d)
+        validate(voxel[d] > 0.0, "voxel size components must be positive");
+    auto* out = new sk_coords();
+    out->ctx = ctx;
+    out->dims = dims;
+    out->id = next_coord_set_id();
+    out->cap = pow2_cap(m);
+    out->table.alloc((size_t)out->cap * 16, st);
+    SK_CUDA(cudaMemsetAsync(out->table.p, 0xFF, out->table.bytes, st));
+    if (m == 0) {
+        out->n = 0;
+        out->coords.alloc(16, st);
+        out->has_table = true;
+        return out;
+    }
+    DevBuf slot, q, flag, pos, tmp, err;
+    slot.alloc((size_t)m * 4, st);
+    q.alloc((size_t)m * 16, st);
+    flag.alloc((size_t)m * 4, st);
+    pos.alloc((size_t)m * 4 + 4, st);
+    err.alloc(4, st);
+    SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    const int g = (int)ceil_div(m, 256);
+    k_quant_insert<<<g, 256, 0, st>>>(raw, batch, m, dims, voxel[0], voxel[1],
+                                      dims == 3 ? voxel[2] : 1.0, out->table.as<ulonglong2>(),
+                                      (uint64_t)out->cap - 1, slot.as<int>(), q.as<int4>(),
+                                      err.as<int>());
+    SK_LAUNCH_CHECK();
+    int h_err = 0;
+    SK_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (h_err) {
+        delete out;
+        validate(!(h_err & 1), "non-finite input coordinate");
+        validate(false, "quantized coordinate outside the packable range "
+                        "(batch [0,4096), xyz [-65536,65536))");
+    }
+    k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), m, flag.as<int>());
+    SK_LAUNCH_CHECK();
+    size_t tbytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tbytes, flag.as<int>(), pos.as<int>(), m, st);
+    tmp.alloc(tbytes, st);
+    cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, flag.as<int>(), pos.as<int>(), m, st);
+    SK_LAUNCH_CHECK();
+    int h_last_pos = 0, h_last_flag = 0;
+    SK_CUDA(cudaMemcpyAsync(&h_last_pos, pos.as<int>() + m - 1, 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaMemcpyAsync(&h_last_flag, flag.as<int>() + m - 1, 4, cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    out->n = h_last_pos + h_last_flag;
+    out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
+    k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(), q.as<int4>(),
+                                      m, out->table.as<ulonglong2>(), out->coords.as<int4>());
+    SK_LAUNCH_CHECK();
+    out->has_table = true;
+    if (point_rows) {
+        k_point_rows<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), m, point_rows);
+        SK_LAUNCH_CHECK();
+    }
+    return out;
+}
+
+void quantize_features(int m, int channels, const double* feats, const int32_t* point_rows,
+                       int n, int rule, sk_dtype dt, void* out, cudaStream_t st) {
+    validate(rule == 0 || rule == 1, "unknown dedup rule");
+    validate(channels >= 0, "negative channel count");
+    if (n == 0) return;
+    validate(m > 0 && point_rows, "point rows required");
+    auto launch = [&](auto tag) {
+        using T = decltype(tag);
+        T* o = static_cast<T*>(out);
+        if (channels == 0) {  // occupancy: one channel of ones
+            k_fill<T><<<(int)ceil_div(n, 256), 256, 0, st>>>(o, n, 1.0);
+            SK_LAUNCH_CHECK();
+            return;
+        }
+        const long long tot = (long long)n * channels;
+        const int g = (int)ceil_div(tot, 256);
+        if (rule == 0) {
+            DevBuf first;
+            first.alloc((size_t)n * 4, st);
+            SK_CUDA(cudaMemsetAsync(first.p, 0x7F, (size_t)n * 4, st));
+            k_first_point<<<(int)ceil_div(m, 256), 256, 0, st>>>(point_rows, m, first.as<int>());
+            SK_LAUNCH_CHECK();
+            k_quant_feats_first<T><<<g, 256, 0, st>>>(feats, channels, first.as<int>(), n, o);
+            SK_LAUNCH_CHECK();
+        } else {
+            DevBuf sum, cnt;
+            sum.alloc((size_t)tot * 8, st);
+            cnt.alloc((size_t)n * 4, st);
+            SK_CUDA(cudaMemsetAsync(sum.p, 0, sum.bytes, st));
+            SK_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, st));
+            k_quant_sum<<<(int)ceil_div((long long)m * channels, 256), 256, 0, st>>>(
+                feats, channels, point_rows, m, sum.as<double>(), cnt.as<int>());
+            SK_LAUNCH_CHECK();
+            k_quant_mean<T><<<g, 256, 0, st>>>(sum.as<double>(), cnt.as<int>(), channels, n, o);
+            SK_LAUNCH_CHECK();
+        }
+    };
+    if (dt == SK_F32) launch(float());
+    else if (dt == SK_F64) launch(double());
+    else if (dt == SK_F16) launch(__half());
+    else if (dt == SK_BF16) launch(__nv_bfloat16());
+    else fail(SK_ERR_VALIDATION, "unknown feature dtype");
 }
 
 sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],

@@ -650,6 +650,8 @@ extern "C" {
 
 sk_status sk_net_create(sk_ctx* ctx, int dims, const char* spec_text, sk_dtype dtype, sk_net** out) {
     return nguard([&] {
+        validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
+                 "network dtype must be f32, f16 or bf16");
         validate(ctx && out, "null argument");
         auto n = std::make_unique<sk_net>();
         n->ctx = ctx;

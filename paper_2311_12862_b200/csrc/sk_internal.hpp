@@ -97,6 +97,12 @@ constexpr int kTileWS = 256; // pairs per FOD/GGS tile (padded per offset)
 void coords_build_table(sk_coords* c, cudaStream_t st);
 void coords_check_range(sk_ctx* ctx, const int32_t* d, int n, cudaStream_t st);
 sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_t st);
+// quantize (tensor.cpp:87-142): coordinates in first-appearance order and the
+// output row of every point (optional); features reduced by DedupRule
+sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, const int32_t* batch,
+                           const double voxel[3], int32_t* point_rows, cudaStream_t st);
+void quantize_features(int m, int channels, const double* feats, const int32_t* point_rows,
+                       int n, int rule, sk_dtype dt, void* out, cudaStream_t st);
 sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],
                     int transposed, cudaStream_t st);
 sk_kmap* kmap_transpose(sk_kmap* m, cudaStream_t st);

@@ -30,7 +30,7 @@ from ._lib import (ContractError, DataflowCfg, KmapInfo, SkError, Tile, Validati
                    i32x3, lib)
 
 __all__ = ["Context", "CoordSet", "KernelMap", "DataflowConfig", "TilePreset", "tile_small",
-           "tile_large", "build_out_coords", "build_kmap", "conv_forward", "conv_dgrad",
+           "tile_large", "quantize", "build_out_coords", "build_kmap", "conv_forward", "conv_dgrad",
            "conv_wgrad", "ValidationError", "ContractError", "SkError", "GATHER_GEMM_SCATTER",
            "FETCH_ON_DEMAND", "IMPLICIT_GEMM"]
 
@@ -149,6 +149,39 @@ def _stride3(stride, dims=3):
     if dims == 2:
         s[2] = 1
     return s
+
+
+def quantize(raw, dims: int = 3, feats=None, voxel=(1.0, 1.0, 1.0), rule: str = "first",
+             batch=None, dtype=torch.float32, ctx: Context | None = None):
+    """quantize (tensor.cpp:87-142; DedupRule tensor.hpp:45) on the GPU:
+    floor(raw / voxel) per axis, first-appearance dedup, features of the
+    first point ("first") or the mean ("mean"); no features -> one occupancy
+    channel of ones. raw: [m, dims] float64 (host or CUDA); batch: [m] int32
+    or None; feats: [m, C] float64 or None. Returns (CoordSet, features [n,
+    max(C, 1)] of `dtype` on the GPU)."""
+    ctx = ctx or Context.get()
+    if rule not in ("first", "mean"):
+        raise ValidationError("unknown dedup rule")
+    r = torch.as_tensor(raw, dtype=torch.float64).reshape(-1, dims).to("cuda").contiguous()
+    m = r.shape[0]
+    b = None if batch is None else torch.as_tensor(batch, dtype=torch.int32).to("cuda").contiguous()
+    rows = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+    vox = (C.c_double * 3)(*[float(v) for v in (list(voxel) + [1.0] * 3)[:3]])
+    p = C.c_void_p()
+    check(lib().sk_quantize(ctx.ptr, dims, m, _ptr(r) if m else None,
+                            _ptr(b) if b is not None and m else None, vox, _stream(), C.byref(p),
+                            _ptr(rows)))
+    cs = CoordSet(p, ctx)
+    ch = 0 if feats is None else int(np.asarray(feats).shape[-1] if not torch.is_tensor(feats)
+                                     else feats.shape[-1])
+    out = torch.empty(cs.n, max(ch, 1), dtype=dtype, device="cuda")
+    f = None
+    if ch:
+        f = torch.as_tensor(feats, dtype=torch.float64).reshape(m, ch).to("cuda").contiguous()
+    check(lib().sk_quantize_features(ctx.ptr, m, ch, _ptr(f) if f is not None else None,
+                                     _ptr(rows), cs.n, 0 if rule == "first" else 1,
+                                     {**_DTYPES, torch.float64: 3}[dtype], _ptr(out), _stream()))
+    return cs, out
 
 
 def build_out_coords(coords: CoordSet, stride) -> CoordSet:
