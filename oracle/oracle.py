@@ -318,6 +318,12 @@ class Reference:
                                       C.POINTER(C.c_double)]
         L.ref_net_output.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                      C.POINTER(C.c_int)]
+        self.has_io = hasattr(L, "ref_tspw_write")  # io.cpp compiled in (json.hpp found)
+        if self.has_io:
+            L.ref_tspw_write.argtypes = [C.c_char_p, C.c_int, _i32p, _f64p]
+            L.ref_tspw_read.argtypes = [C.c_char_p, C.POINTER(C.c_int), _i32p, C.c_int, C.c_void_p]
+            L.ref_tune_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+            L.ref_tune_sample.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_int)]
 
     def _check(self, rc):
         if rc:
@@ -325,6 +331,41 @@ class Reference:
             if rc == 1:
                 raise ValueError(msg)
             raise RuntimeError(f"reference error {rc}: {msg}")
+
+    # ---- io.cpp: TSPW weights, TuneResult JSON (write_tspw / read_tspw,
+    # tune_result_to_json / _from_json)
+    def tspw_write(self, path, layers):
+        shapes = _c(np.array([w.shape for w in layers], np.int32).reshape(-1), np.int32)
+        vals = _c(np.concatenate([np.asarray(w, np.float64).ravel() for w in layers]), np.float64)
+        self._check(self.lib.ref_tspw_write(path.encode(), len(layers), shapes, vals))
+
+    def tspw_read(self, path):
+        n = C.c_int()
+        shapes = np.zeros(3 * 1024, np.int32)
+        self._check(self.lib.ref_tspw_read(path.encode(), C.byref(n), shapes, 1024, None))
+        sh = shapes[:3 * n.value].reshape(-1, 3)
+        vals = np.zeros(int(np.prod(sh, axis=1).sum()), np.float64)
+        self._check(self.lib.ref_tspw_read(path.encode(), C.byref(n), shapes, 1024,
+                                           vals.ctypes.data))
+        out, off = [], 0
+        for kd, ci, co in sh:
+            cnt = int(kd) * int(ci) * int(co)
+            out.append(vals[off:off + cnt].reshape(kd, ci, co))
+            off += cnt
+        return out
+
+    def _text(self, fn, *args):
+        ln = C.c_int()
+        self._check(fn(*args, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value + 1)
+        self._check(fn(*args, buf, ln.value + 1, C.byref(ln)))
+        return buf.value.decode()
+
+    def tune_roundtrip(self, text):
+        return self._text(self.lib.ref_tune_roundtrip, text.encode())
+
+    def tune_sample(self):
+        return self._text(self.lib.ref_tune_sample)
 
     def out_coords(self, dims, coords, stride):
         coords = _c(coords, np.int32).reshape(-1, 4)

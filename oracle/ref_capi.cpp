@@ -26,6 +26,9 @@
 #include "sparsekit/cost.hpp"
 #include "sparsekit/exec.hpp"
 #include "sparsekit/gen.hpp"
+#ifdef SK_REF_IO
+#include "sparsekit/io.hpp"
+#endif
 #include "sparsekit/kmap.hpp"
 #include "sparsekit/network.hpp"
 #include "sparsekit/tensor.hpp"
@@ -446,4 +449,73 @@ int ref_net_output(RefNet* n, double* y, int* n_rows, int* c_out) {
     });
 }
 
+
+#ifdef SK_REF_IO
+// ---- io.cpp (TSPW weights, DataflowConfig / TuneResult JSON) ----------------
+int ref_tspw_write(const char* path, int n_layers, const int32_t* shapes, const double* vals) {
+    return guard([&] {
+        std::vector<WeightTensor> w;
+        size_t off = 0;
+        for (int i = 0; i < n_layers; ++i) {
+            const int kd = shapes[3 * i], ci = shapes[3 * i + 1], co = shapes[3 * i + 2];
+            const size_t cnt = (size_t)kd * ci * co;
+            w.emplace_back(kd, ci, co, std::vector<double>(vals + off, vals + off + cnt),
+                           Precision::f64);
+            off += cnt;
+        }
+        write_tspw(path, w);
+    });
+}
+
+// two calls: vals == nullptr returns the layer count and shapes (cap layers)
+int ref_tspw_read(const char* path, int* n_layers, int32_t* shapes, int cap, double* vals) {
+    return guard([&] {
+        std::vector<WeightTensor> w = read_tspw(path, Precision::f64);
+        *n_layers = static_cast<int>(w.size());
+        size_t off = 0;
+        for (int i = 0; i < (int)w.size() && i < cap; ++i) {
+            shapes[3 * i] = w[i].num_offsets();
+            shapes[3 * i + 1] = w[i].c_in();
+            shapes[3 * i + 2] = w[i].c_out();
+            if (vals) {
+                std::vector<double> v = w[i].as_f64();
+                std::memcpy(vals + off, v.data(), v.size() * sizeof(double));
+                off += v.size();
+            }
+        }
+    });
+}
+
+// parse a TuneResult JSON and dump it again (canonical form); out_len = bytes
+int ref_tune_roundtrip(const char* text, char* out, int cap, int* out_len) {
+    return guard([&] {
+        const std::string t = tune_result_to_json(tune_result_from_json(text));
+        *out_len = static_cast<int>(t.size());
+        if (out && cap > (int)t.size()) std::memcpy(out, t.c_str(), t.size() + 1);
+    });
+}
+
+// the test_net_io.cpp "tune result JSON round-trips" sample, dumped
+int ref_tune_sample(char* out, int cap, int* out_len) {
+    return guard([&] {
+        TuneResult res;
+        GroupChoice g;
+        g.id = 0;
+        g.layer_names = {"c1", "c2"};
+        g.forward.kind = DataflowKind::implicit_gemm;
+        g.forward.splits = 3;
+        g.forward.tile = tile_large();
+        DataflowConfig d;
+        d.kind = DataflowKind::fetch_on_demand;
+        g.dgrad = d;
+        res.groups.push_back(g);
+        res.latency_ms = 12.5;
+        res.seed = 42;
+        res.log.push_back({0, 0, g.forward, 3.25});
+        const std::string t = tune_result_to_json(res);
+        *out_len = static_cast<int>(t.size());
+        if (out && cap > (int)t.size()) std::memcpy(out, t.c_str(), t.size() + 1);
+    });
+}
+#endif
 }  // extern "C"

@@ -185,3 +185,29 @@ def test_tuner_contracts(env):
         assert net.config(g) == space[best]
     lat2, log2 = net.tune(cs, x, training=2, warmup=0, runs=1)
     assert len(log2) == 2 * G * len(space)
+
+
+def test_tune_result_and_tspw_weights_roundtrip(env, tmp_path):
+    """A tuned assignment and the weights leave one runner as reference-format
+    files (TuneResult JSON, TSPW) and reproduce the same network in another."""
+    torch, sk, N, M = env
+    from paper_2311_12862_b200 import io
+    cs = sk.CoordSet.create(scan(3000, seed=13))
+    x = torch.randn(cs.n, 1, device="cuda").half()
+    net = N.NetworkRunner(M.toy_unet(), dtype=torch.float16)
+    net.init_weights(5)
+    lat, log = net.tune(cs, x, training=0, warmup=0, runs=1)
+    text = io.tune_result_to_json(io.tune_result_of(net, lat, log))
+    p = str(tmp_path / "w.tspw")
+    io.write_tspw(p, [net.weight(i).float().cpu().numpy() for i in range(net.num_layers)])
+    net2 = N.NetworkRunner(M.toy_unet(), dtype=torch.float16)
+    io.apply_tune_result(net2, io.tune_result_from_json(text))
+    for i, w in enumerate(io.read_tspw(p)):
+        net2.set_weight(i, torch.from_numpy(w).half().cuda())
+    net2.weights_updated()
+    for g in range(net.num_groups):
+        assert net2.config(g) == net.config(g)
+    y1, _ = net.forward(cs, x)
+    y2, _ = net2.forward(cs, x)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
