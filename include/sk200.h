@@ -151,6 +151,14 @@ sk_status sk_out_coords(sk_ctx* ctx, sk_coords* in, const int32_t stride[3], voi
  * the context by MapKey (kmap.hpp:99-107). Odd kernel only, K <= 5. */
 sk_status sk_kmap_build(sk_ctx* ctx, sk_coords* in, sk_coords* out, int kernel_size,
                         const int32_t stride[3], int transposed, void* stream, sk_kmap** map);
+/* kmap_from_edges (kmap.cpp:317-336): a graph (R-GCN) map over relations.
+ * d_edges: device int32[E][3] = (src, dst, relation); per relation the pairs
+ * are stably sorted by dst. WS form only: forward through GGS / FOD and
+ * wgrad; implicit GEMM, prepare, OS export, transpose and dgrad raise
+ * SK_ERR_CONTRACT like the reference ("graph maps cannot be transposed"). Out-of-range ids ->
+ * SK_ERR_VALIDATION (one sync). */
+sk_status sk_kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int num_edges,
+                             int num_relations, int n_in, int n_out, void* stream, sk_kmap** out);
 /* transpose_map (kmap.cpp:290-315): swap (in, out), mirror offsets. */
 sk_status sk_kmap_transpose(sk_ctx* ctx, sk_kmap* map, void* stream, sk_kmap** out);
 /* split_and_sort + pad_map (kmap.cpp:211-288), i.e. prepare_os_map

@@ -285,6 +285,8 @@ class Reference:
         L.ref_map_build.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _i32p, _i32p,
                                     C.c_int, C.POINTER(C.c_void_p)]
         L.ref_map_transpose.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+        L.ref_map_from_edges.argtypes = [C.c_int, _i32p, C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(C.c_void_p)]
         L.ref_map_free.argtypes = [C.c_void_p]
         L.ref_map_free.restype = None
         for f in ("ref_map_num_offsets", "ref_map_n_in", "ref_map_n_out", "ref_prep_num_splits"):
@@ -382,6 +384,13 @@ class Reference:
         self._check(self.lib.ref_map_build(dims, k, len(in_coords), in_coords, len(out_coords),
                                            out_coords, _c(stride, np.int32), int(transposed),
                                            C.byref(p)))
+        return RefMap(self, p)
+
+    def graph_map(self, edges, relations, n_in, n_out) -> RefMap:
+        """kmap_from_edges (kmap.cpp:317-336)."""
+        e = _c(np.asarray(edges, np.int32).reshape(-1, 3), np.int32)
+        p = C.c_void_p()
+        self._check(self.lib.ref_map_from_edges(len(e), e, relations, n_in, n_out, C.byref(p)))
         return RefMap(self, p)
 
     # kind: 0 gather_gemm_scatter, 1 fetch_on_demand, 2 implicit_gemm

@@ -13,6 +13,7 @@
 // reference Precision inside; every entry point returns 0 on success,
 // 1 on sparsekit::ValidationError, 2 on sparsekit::ContractError, 5 other.
 
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <random>
@@ -129,12 +130,23 @@ int ref_map_build(int dims, int kernel, int n_in, const int32_t* in_coords, int 
     });
 }
 
+int ref_map_from_edges(int E, const int32_t* edges, int relations, int n_in, int n_out,
+                       RefMap** out) {
+    return guard([&] {
+        std::vector<std::array<int32_t, 3>> ev(E);
+        for (int i = 0; i < E; ++i) ev[i] = {edges[3 * i], edges[3 * i + 1], edges[3 * i + 2]};
+        auto* m = new RefMap();
+        m->ws = kmap_from_edges(ev, relations, n_in, n_out);
+        *out = m;
+    });
+}
+
 int ref_map_transpose(const RefMap* m, RefMap** out) {
     return guard([&] {
         auto t = std::make_unique<RefMap>();
         t->dims = m->dims;
         t->ws = transpose_map(m->ws);
-        t->os = transpose_map(m->os);
+        if (!m->ws.graph) t->os = transpose_map(m->os);
         *out = t.release();
     });
 }

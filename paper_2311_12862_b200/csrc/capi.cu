@@ -294,8 +294,18 @@ sk_status sk_kmap_get_info(sk_kmap* m, void* stream, sk_kmap_info* info) {
     });
 }
 
+sk_status sk_kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int num_edges,
+                             int num_relations, int n_in, int n_out, void* stream, sk_kmap** out) {
+    return guard([&] {
+        sk::validate(ctx && out, "null argument");
+        sk::validate(num_edges == 0 || d_edges, "null edges");
+        *out = sk::kmap_from_edges(ctx, d_edges, num_edges, num_relations, n_in, n_out, S(stream));
+    });
+}
+
 sk_status sk_kmap_export_os(sk_kmap* m, int32_t* h_entries, uint64_t* h_masks, void* stream) {
     return guard([&] {
+        sk::contract(!m->graph, "graph maps have no OS form");
         cudaStream_t st = S(stream);
         if (m->n_out) {
             SK_CUDA(cudaMemcpyAsync(h_entries, m->os.p, (size_t)m->n_out * m->kd * 4,

@@ -1908,6 +1908,8 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     validate(cfg.splits >= 0, "splits must be >= 0");
     validate(cfg.kind >= 0 && cfg.kind <= 2, "unknown dataflow kind");
+    contract(!(m_fwd->graph && cfg.kind == SK_IMPLICIT_GEMM),
+             "graph maps run through the pair-list dataflows (GGS / FOD) only");
     sk_kmap* m = dgrad ? kmap_transpose(m_fwd, st) : m_fwd;
     // GEMM shape: A rows carry k_total channels, the output n_total
     const int k_total = dgrad ? c_out : c_in;
@@ -2145,8 +2147,11 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
     }
     // pair chunking: enough blocks to fill the machine; deterministic mode
     // uses one chunk per offset (no cross-block float atomics on one cell)
-    const int chunk = ctx->deterministic ? (int)std::max<int64_t>(1, (int64_t)m->n_out) : 2048;
-    const int chunks = (int)ceil_div(std::max(m->n_out, 1), chunk);
+    // pairs per offset are bounded by n_out for conv maps (one per (out,
+    // offset)); a graph relation can hold up to all E edges
+    const int64_t per_off = m->graph ? std::max<int64_t>(m->total_pairs_host, 1) : m->n_out;
+    const int chunk = ctx->deterministic ? (int)std::max<int64_t>(1, per_off) : 2048;
+    const int chunks = (int)ceil_div(std::max<int64_t>(per_off, 1), chunk);
     dim3 grid(chunks, (unsigned)(ceil_div(c_in, 32) * ceil_div(c_out, 32)), m->kd);
     const long long* ptr = m->ws_ptr.as<long long>();
     if (dt == SK_F32)

@@ -353,6 +353,55 @@ __global__ void k_fill(T* __restrict__ out, long long n, double v) {
     if (t < n) out[t] = (T)v;
 }
 
+
+// ---- graph maps (kmap_from_edges, kmap.cpp:317-336) -----------------------------
+__global__ void k_edge_keys(const int* __restrict__ edges, int E, int R, int n_in, int n_out,
+                            unsigned long long* __restrict__ keys, int* __restrict__ vals,
+                            int* __restrict__ counts, int* __restrict__ err) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int src = edges[3 * e], dst = edges[3 * e + 1], rel = edges[3 * e + 2];
+    if (rel < 0 || rel >= R) atomicOr(err, 1);
+    if (src < 0 || src >= n_in || dst < 0 || dst >= n_out) atomicOr(err, 2);
+    const int r = min(max(rel, 0), R - 1);
+    keys[e] = ((unsigned long long)r << 32) | (unsigned)max(dst, 0);
+    vals[e] = e;
+    atomicAdd(counts + r, 1);
+}
+
+// exclusive scans of the per-relation counts (pairs and 256-pair tiles); one thread
+__global__ void k_edge_scan(const int* __restrict__ counts, int R, long long* __restrict__ ptr,
+                            int* __restrict__ tile_ptr) {
+    long long acc = 0;
+    int tiles = 0;
+    for (int r = 0; r < R; ++r) {
+        ptr[r] = acc;
+        tile_ptr[r] = tiles;
+        acc += counts[r];
+        tiles += (counts[r] + kTileWS - 1) / kTileWS;
+    }
+    ptr[R] = acc;
+    tile_ptr[R] = tiles;
+}
+
+__global__ void k_edge_scatter(const int* __restrict__ edges, const unsigned long long* __restrict__ keys,
+                               const int* __restrict__ order, int E, const long long* __restrict__ ptr,
+                               const int* __restrict__ tile_ptr, int* __restrict__ ws_in,
+                               int* __restrict__ ws_out, int* __restrict__ in_pad,
+                               int* __restrict__ out_pad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E) return;
+    const int e = order[i];
+    const int rel = (int)(keys[i] >> 32);
+    const long long j = i - ptr[rel];
+    ws_in[i] = edges[3 * e];
+    ws_out[i] = edges[3 * e + 1];
+    const long long pp = (long long)tile_ptr[rel] * kTileWS + j;
+    in_pad[pp] = edges[3 * e];
+    out_pad[pp] = edges[3 * e + 1];
+}
+
+
 // resolve a probe whose first slot (key + row) is already loaded
 __device__ __forceinline__ int probe(const ulonglong2* __restrict__ table, uint64_t mask,
                                      unsigned long long key, uint64_t s, ulonglong2 first) {
@@ -1010,6 +1059,81 @@ void quantize_features(int m, int channels, const double* feats, const int32_t* 
     else fail(SK_ERR_VALIDATION, "unknown feature dtype");
 }
 
+
+sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int n_in, int n_out,
+                         cudaStream_t st) {
+    validate(R >= 1, "need at least one relation");
+    validate(E >= 0 && n_in >= 0 && n_out >= 0, "negative size");
+    auto* m = new sk_kmap();
+    m->ctx = ctx;
+    m->graph = true;
+    m->kernel = 0;
+    m->kd = R;
+    m->n_in = n_in;
+    m->n_out = n_out;
+    m->rows_pad = (int)ceil_div(std::max(n_out, 1), kTileM) * kTileM;
+    m->words = (R + 63) / 64;
+    m->ws_ptr.alloc((size_t)(R + 1) * 8, st);
+    m->ws_tile_ptr.alloc((size_t)(R + 1) * 4, st);
+    m->ws_in.alloc((size_t)std::max(E, 1) * 4, st);
+    m->ws_out.alloc((size_t)std::max(E, 1) * 4, st);
+    const size_t cap_pad = (size_t)E + (size_t)R * kTileWS;
+    m->ws_in_pad.alloc(cap_pad * 4, st);
+    m->ws_out_pad.alloc(cap_pad * 4, st);
+    SK_CUDA(cudaMemsetAsync(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st));
+    SK_CUDA(cudaMemsetAsync(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st));
+    DevBuf counts, err, keys, keys2, vals, order, tmp;
+    counts.alloc((size_t)R * 4, st);
+    err.alloc(4, st);
+    SK_CUDA(cudaMemsetAsync(counts.p, 0, counts.bytes, st));
+    SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    if (E > 0) {
+        keys.alloc((size_t)E * 8, st);
+        keys2.alloc((size_t)E * 8, st);
+        vals.alloc((size_t)E * 4, st);
+        order.alloc((size_t)E * 4, st);
+        const int g = (int)ceil_div(E, 256);
+        k_edge_keys<<<g, 256, 0, st>>>(d_edges, E, R, n_in, n_out, keys.as<unsigned long long>(),
+                                       vals.as<int>(), counts.as<int>(), err.as<int>());
+        SK_LAUNCH_CHECK();
+        int h_err = 0;
+        SK_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        if (h_err) {
+            delete m;
+            validate(!(h_err & 1), "relation id out of range");
+            validate(false, "edge node id out of range");
+        }
+        int rbits = 1;
+        while ((1 << rbits) < R) ++rbits;
+        size_t tb = 0;
+        // LSD radix sort is stable: equal (relation, dst) keep the edge order
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<unsigned long long>(),
+                                        keys2.as<unsigned long long>(), vals.as<int>(),
+                                        order.as<int>(), E, 0, 32 + rbits, st);
+        tmp.alloc(tb, st);
+        cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<unsigned long long>(),
+                                        keys2.as<unsigned long long>(), vals.as<int>(),
+                                        order.as<int>(), E, 0, 32 + rbits, st);
+        SK_LAUNCH_CHECK();
+        k_edge_scan<<<1, 1, 0, st>>>(counts.as<int>(), R, m->ws_ptr.as<long long>(),
+                                     m->ws_tile_ptr.as<int>());
+        SK_LAUNCH_CHECK();
+        k_edge_scatter<<<g, 256, 0, st>>>(d_edges, keys2.as<unsigned long long>(), order.as<int>(),
+                                          E, m->ws_ptr.as<long long>(), m->ws_tile_ptr.as<int>(),
+                                          m->ws_in.as<int>(), m->ws_out.as<int>(),
+                                          m->ws_in_pad.as<int>(), m->ws_out_pad.as<int>());
+        SK_LAUNCH_CHECK();
+    } else {
+        k_edge_scan<<<1, 1, 0, st>>>(counts.as<int>(), R, m->ws_ptr.as<long long>(),
+                                     m->ws_tile_ptr.as<int>());
+        SK_LAUNCH_CHECK();
+    }
+    m->has_ws = true;
+    m->total_pairs_host = E;
+    return m;
+}
+
 sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],
                     int transposed, cudaStream_t st) {
     validate(in->dims == out->dims, "offset dims mismatch");
@@ -1041,6 +1165,8 @@ sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t str
 }
 
 sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
+    // transpose_map rejects graph maps (kmap.cpp:290-295): so does conv_dgrad on them
+    contract(!src->graph, "graph maps cannot be transposed");
     std::lock_guard<std::mutex> lock(src->mu);
     if (src->transpose_cache) return src->transpose_cache;
     auto* m = new sk_kmap();
@@ -1115,6 +1241,7 @@ int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st) {
 }
 
 Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
+    contract(!m->graph, "graph maps have no OS form (pair-list dataflows only)");
     validate(splits >= 0, "split count must be >= 0");
     validate(splits <= m->kd, "split count exceeds number of kernel offsets");
     validate(pad >= 1, "pad multiple must be >= 1");

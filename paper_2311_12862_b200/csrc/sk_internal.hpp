@@ -69,6 +69,7 @@ struct sk_kmap : sk::Refcounted {
     int n_in = 0, n_out = 0;
     int rows_pad = 0;       // n_out rounded up to 128 (the raw OS is stored padded)
     bool identity = false;  // K=1, stride 1, in set == out set: entries[q][0] == q
+    bool graph = false;     // kmap_from_edges (kmap.cpp:317-336): WS lists only, kd = relations
     int words = 1;          // mask words of the full-width map
     int n_blocks = 0;       // query blocks (for per-block pair counts)
     sk::DevBuf os;          // rows_pad x kd int32
@@ -106,6 +107,10 @@ void quantize_features(int m, int channels, const double* feats, const int32_t* 
 sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],
                     int transposed, cudaStream_t st);
 sk_kmap* kmap_transpose(sk_kmap* m, cudaStream_t st);
+// kmap_from_edges (kmap.cpp:317-336): edges int32 [E][3] = (src, dst, relation)
+// on the device; per relation, pairs stably sorted by dst (WS only)
+sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int relations, int n_in,
+                         int n_out, cudaStream_t st);
 void kmap_ensure_ws(sk_kmap* m, cudaStream_t st);
 Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st);
 int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st);

@@ -30,7 +30,7 @@ from ._lib import (ContractError, DataflowCfg, KmapInfo, SkError, Tile, Validati
                    i32x3, lib)
 
 __all__ = ["Context", "CoordSet", "KernelMap", "DataflowConfig", "TilePreset", "tile_small",
-           "tile_large", "quantize", "build_out_coords", "build_kmap", "conv_forward", "conv_dgrad",
+           "tile_large", "quantize", "build_out_coords", "build_kmap", "kmap_from_edges", "conv_forward", "conv_dgrad",
            "conv_wgrad", "ValidationError", "ContractError", "SkError", "GATHER_GEMM_SCATTER",
            "FETCH_ON_DEMAND", "IMPLICIT_GEMM"]
 
@@ -200,6 +200,18 @@ def build_kmap(inp: CoordSet, out: CoordSet, kernel_size: int, stride=1,
                               i32x3(_stride3(stride, inp.dims)), int(transposed), _stream(),
                               C.byref(p)))
     return KernelMap(p, inp.ctx)
+
+
+def kmap_from_edges(edges, num_relations: int, n_in: int, n_out: int,
+                    ctx: Context | None = None) -> "KernelMap":
+    """kmap_from_edges (kmap.cpp:317-336): graph (R-GCN) map; edges [E, 3] =
+    (src, dst, relation). Runs through GATHER_GEMM_SCATTER / FETCH_ON_DEMAND."""
+    ctx = ctx or Context.get()
+    e = torch.as_tensor(np.asarray(edges, dtype=np.int32).reshape(-1, 3)).cuda().contiguous()
+    p = C.c_void_p()
+    check(lib().sk_kmap_from_edges(ctx.ptr, _ptr(e) if e.numel() else None, e.shape[0],
+                                   num_relations, n_in, n_out, _stream(), C.byref(p)))
+    return KernelMap(p, ctx)
 
 
 class KernelMap:
