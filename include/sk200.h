@@ -151,6 +151,15 @@ sk_status sk_out_coords(sk_ctx* ctx, sk_coords* in, const int32_t stride[3], voi
  * the context by MapKey (kmap.hpp:99-107). Odd kernel only, K <= 5. */
 sk_status sk_kmap_build(sk_ctx* ctx, sk_coords* in, sk_coords* out, int kernel_size,
                         const int32_t stride[3], int transposed, void* stream, sk_kmap** map);
+/* EXTENSION beyond the reference (the reference accepts
+ * odd symmetric K only and has no dilation): per-axis kernel sizes in [1, 8]
+ * (odd or even; axis offsets dil * (lo .. lo+k-1), lo = -((k-1)/2), i.e.
+ * {-1,0,1} for 3 and {0,1} for 2 as in MinkowskiEngine / TorchSparse) and
+ * dilation per axis; kernel volume <= 128; lexicographic offset order.
+ * Standard shapes return the same cached map as sk_kmap_build. */
+sk_status sk_kmap_build_ex(sk_ctx* ctx, sk_coords* in, sk_coords* out, const int32_t kernel[3],
+                           const int32_t stride[3], const int32_t dilation[3], int transposed,
+                           void* stream, sk_kmap** map);
 /* kmap_from_edges (kmap.cpp:317-336): a graph (R-GCN) map over relations.
  * d_edges: device int32[E][3] = (src, dst, relation); per relation the pairs
  * are stably sorted by dst. WS form only: forward through GGS / FOD and

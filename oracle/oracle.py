@@ -57,6 +57,8 @@ class Restatement:
         L = self.lib = C.CDLL(path)
         L.sko_offsets.argtypes = [C.c_int, C.c_int, _i32p]
         L.sko_out_coords.argtypes = [C.c_int, C.c_int, _i32p, _i32p, _i32p, C.POINTER(C.c_int)]
+        L.sko_kmap_os_ex.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _i32p, C.c_int, _i32p,
+                                     _i32p, C.c_int, _i32p]
         L.sko_kmap_os.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _i32p, _i32p,
                                   C.c_int, _i32p]
         L.sko_masks.argtypes = [C.c_int, C.c_int, _i32p, _u64p]
@@ -109,6 +111,21 @@ class Restatement:
         return ent
 
     # compute_masks (kmap.cpp:34-47)
+    def kmap_os_ex(self, dims, kernel, dilation, in_coords, out_coords, stride,
+                   transposed=False):
+        """EXTENSION: per-axis / even kernel sizes and
+        dilation; restated definition, not pinned by the reference."""
+        in_coords = _c(in_coords, np.int32).reshape(-1, 4)
+        out_coords = _c(out_coords, np.int32).reshape(-1, 4)
+        kd = int(kernel[0] * kernel[1] * (kernel[2] if dims == 3 else 1))
+        ent = np.zeros((len(out_coords), kd), np.int32)
+        rc = self.lib.sko_kmap_os_ex(dims, _c(kernel, np.int32), _c(dilation, np.int32),
+                                     len(in_coords), in_coords, len(out_coords), out_coords,
+                                     _c(stride, np.int32), int(transposed), ent)
+        if rc:
+            raise ValueError(f"sko_kmap_os_ex failed ({rc})")
+        return ent
+
     def masks(self, entries):
         entries = _c(entries, np.int32)
         n, w = entries.shape

@@ -171,6 +171,61 @@ int sko_kmap_os(int dims, int K, int n_in, const int32_t *in, int n_out, const i
     return 0;
 }
 
+/* ---- EXTENSION beyond the reference (the reference
+ * accepts odd, symmetric K only and has no dilation: kmap.cpp:58-71,
+ * SPEC.md:213). Per-axis kernel sizes k[d] (odd or even) and dilations
+ * dil[d]: axis offsets dil * (lo, lo+1, ..., lo+k-1) with lo = -((k-1)/2)
+ * (k=3: -1,0,1; k=2: 0,1; k=4: -1..2 -- the MinkowskiEngine / TorchSparse
+ * even-kernel convention), lexicographic over (x, y, z) like OffsetSet.
+ * Same relation as build_kmap_ws otherwise: forward p_in = s*q + delta;
+ * transposed q_in = (p_out + delta) / s when every axis divides. This is a
+ * restatement of an extended definition (parity unpinned by the reference). */
+int sko_offsets_ex(int dims, const int32_t *k, const int32_t *dil, int32_t *off) {
+    int kz = dims == 3 ? k[2] : 1, n = 0;
+    for (int d = 0; d < dims; ++d)
+        if (k[d] < 1 || dil[d] < 1) return 1;
+    for (int a = 0; a < k[0]; ++a)
+        for (int b = 0; b < k[1]; ++b)
+            for (int c = 0; c < kz; ++c) {
+                off[3 * n] = dil[0] * (a - (k[0] - 1) / 2);
+                off[3 * n + 1] = dil[1] * (b - (k[1] - 1) / 2);
+                off[3 * n + 2] = dims == 3 ? dil[2] * (c - (kz - 1) / 2) : 0;
+                ++n;
+            }
+    return 0;
+}
+
+int sko_kmap_os_ex(int dims, const int32_t *kernel, const int32_t *dil, int n_in,
+                   const int32_t *in, int n_out, const int32_t *out, const int32_t *stride,
+                   int transposed, int32_t *entries) {
+    int32_t off[128 * 3];
+    int KD = kernel[0] * kernel[1] * (dims == 3 ? kernel[2] : 1);
+    if (KD > 128 || sko_offsets_ex(dims, kernel, dil, off)) return 1;
+    table_t t;
+    if (table_init(&t, n_in)) return 5;
+    for (int j = 0; j < n_in; ++j) table_put(&t, in + 4 * j, j);
+    for (int64_t i = 0; i < (int64_t)n_out * KD; ++i) entries[i] = SENT;
+    for (int k = 0; k < KD; ++k)
+        for (int r = 0; r < n_out; ++r) {
+            int32_t c[4] = {out[4 * r], out[4 * r + 1], out[4 * r + 2], out[4 * r + 3]};
+            int ok = 1;
+            for (int d = 0; d < dims; ++d) {
+                if (!transposed) {
+                    c[1 + d] = out[4 * r + 1 + d] * stride[d] + off[3 * k + d];
+                } else {
+                    int32_t num = out[4 * r + 1 + d] + off[3 * k + d];
+                    if (num % stride[d] != 0) { ok = 0; break; }
+                    c[1 + d] = num / stride[d];
+                }
+            }
+            if (!ok) continue;
+            int32_t j = table_get(&t, c);
+            if (j != SENT) entries[(int64_t)r * KD + k] = j;
+        }
+    table_free(&t);
+    return 0;
+}
+
 /* ---- compute_masks (kmap.cpp:34-47): column j of a width-w split occupies
  * bit (bits_in_word-1-(j-64*wi)) of word wi, words big-endian ---- */
 void sko_masks(int n_rows, int width, const int32_t *entries, uint64_t *masks) {

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SK200_LIB") or os.path.join(PKG, "libsk200.so")
 SYMBOLS = [
     "sk_last_error", "sk_version", "sk_kernel_launches", "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_deterministic",
     "sk_coords_create", "sk_coords_create_host", "sk_coords_retain", "sk_coords_release",
-    "sk_quantize", "sk_quantize_features", "sk_kmap_from_edges",
+    "sk_quantize", "sk_quantize_features", "sk_kmap_from_edges", "sk_kmap_build_ex",
     "sk_coords_n", "sk_coords_dims", "sk_coords_id", "sk_coords_device_ptr",
     "sk_coords_stride_tag", "sk_coords_export", "sk_out_coords", "sk_kmap_build",
     "sk_kmap_transpose", "sk_kmap_prepare", "sk_kmap_retain", "sk_kmap_release",
@@ -102,6 +102,7 @@ def lib():
                                   vp], C.c_int),
         "sk_kmap_build": ([vp, vp, vp, C.c_int, i32p, C.c_int, vp, pp], C.c_int),
         "sk_kmap_transpose": ([vp, vp, vp, pp], C.c_int),
+        "sk_kmap_build_ex": ([vp, vp, vp, i32p, i32p, i32p, C.c_int, vp, pp], C.c_int),
         "sk_kmap_from_edges": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, pp], C.c_int),
         "sk_kmap_prepare": ([vp, vp, C.c_int, C.c_int, vp], C.c_int),
         "sk_kmap_retain": ([vp], C.c_int),

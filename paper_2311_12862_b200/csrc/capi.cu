@@ -1,3 +1,4 @@
+#include <functional>
 // sk200 C ABI (include/sk200.h): handle lifetimes, error mapping, caches.
 // No C++ exception crosses this boundary.
 #include <cstring>
@@ -233,27 +234,58 @@ sk_status sk_out_coords(sk_ctx* ctx, sk_coords* in, const int32_t stride[3], voi
     });
 }
 
+namespace {
+// MapCache (kmap.cpp:359-391): one build per key; kcode = K for the standard
+// odd symmetric kernels, 256 + (kx | ky << 4 | kz << 8) for generalized ones
+sk_kmap* cached_map(sk_coords* in, sk_coords* out, int kcode, const int32_t stride[3],
+                    int transposed, int dcode, const std::function<sk_kmap*()>& build) {
+    auto key = std::make_tuple(out->id, kcode, stride[0], stride[1],
+                               in->dims == 3 ? stride[2] : 1, transposed ? 1 : 0, dcode);
+    sk_kmap* m = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(in->mu);
+        auto it = in->maps.find(key);
+        if (it != in->maps.end()) m = it->second;
+    }
+    if (!m) {
+        sk_kmap* built = build();
+        std::lock_guard<std::mutex> lock(in->mu);
+        auto ins = in->maps.emplace(key, built);
+        if (!ins.second) release_kmap(built);  // lost a race: builds once per key
+        m = ins.first->second;
+    }
+    m->refs.fetch_add(1);
+    return m;
+}
+}  // namespace
+
 sk_status sk_kmap_build(sk_ctx* ctx, sk_coords* in, sk_coords* out, int kernel_size,
                         const int32_t stride[3], int transposed, void* stream, sk_kmap** map) {
     return guard([&] {
         sk::validate(ctx && in && out && map, "null argument");
-        auto key = std::make_tuple(out->id, kernel_size, stride[0], stride[1],
-                                   in->dims == 3 ? stride[2] : 1, transposed ? 1 : 0);
-        sk_kmap* m = nullptr;
-        {
-            std::lock_guard<std::mutex> lock(in->mu);
-            auto it = in->maps.find(key);
-            if (it != in->maps.end()) m = it->second;
-        }
-        if (!m) {
-            sk_kmap* built = sk::kmap_build(in, out, kernel_size, stride, transposed, S(stream));
-            std::lock_guard<std::mutex> lock(in->mu);
-            auto ins = in->maps.emplace(key, built);
-            if (!ins.second) release_kmap(built);  // lost a race: builds once per key
-            m = ins.first->second;
-        }
-        m->refs.fetch_add(1);
-        *map = m;
+        *map = cached_map(in, out, kernel_size, stride, transposed, 0, [&] {
+            return sk::kmap_build(in, out, kernel_size, stride, transposed, S(stream));
+        });
+    });
+}
+
+sk_status sk_kmap_build_ex(sk_ctx* ctx, sk_coords* in, sk_coords* out, const int32_t kernel[3],
+                           const int32_t stride[3], const int32_t dilation[3], int transposed,
+                           void* stream, sk_kmap** map) {
+    return guard([&] {
+        sk::validate(ctx && in && out && map && kernel && stride && dilation, "null argument");
+        const int dims = in->dims;
+        const int kz = dims == 3 ? kernel[2] : 1, dz = dims == 3 ? dilation[2] : 1;
+        for (int d = 0; d < dims; ++d)
+            sk::validate(kernel[d] >= 1 && kernel[d] <= 8 && dilation[d] >= 1 && dilation[d] < 1024,
+                         "kernel sizes must be in [1, 8] and dilations in [1, 1024)");
+        const bool standard = kernel[0] == kernel[1] && kernel[1] == kz && kernel[0] % 2 == 1 &&
+                              kernel[0] <= 5 && dilation[0] == 1 && dilation[1] == 1 && dz == 1;
+        const int kcode = standard ? kernel[0] : 256 + (kernel[0] | kernel[1] << 4 | kz << 8);
+        const int dcode = standard ? 0 : (dilation[0] | dilation[1] << 10 | dz << 20);
+        *map = cached_map(in, out, kcode, stride, transposed, dcode, [&] {
+            return sk::kmap_build_ex(in, out, kernel, stride, dilation, transposed, S(stream));
+        });
     });
 }
 

@@ -420,6 +420,75 @@ __device__ __forceinline__ int probe(const ulonglong2* __restrict__ table, uint6
     }
 }
 
+// ---- generalized offsets: per-axis kernel sizes (odd or
+// even) and dilation; offsets come from a device table (lexicographic). One
+// thread per (row, offset subset); same outputs as k_kmap_query.
+template <int TPR>
+__global__ void __launch_bounds__(kQB * TPR) k_kmap_query_gen(
+    const int4* __restrict__ out_coords, int n_out, const ulonglong2* __restrict__ table,
+    uint64_t mask, const int4* __restrict__ offs, int KD, int dims, int sx, int sy, int sz,
+    int transposed, int words, int* __restrict__ os, unsigned long long* __restrict__ masks,
+    int* __restrict__ blk_counts) {
+    extern __shared__ int q_sh[];
+    int* tile = q_sh;                                       // kQB x KD
+    int* cnt = q_sh + kQB * KD;                             // KD
+    int4* soff = reinterpret_cast<int4*>(cnt + ((KD + 3) & ~3));  // KD
+    const int t = threadIdx.x;
+    const int rl = t / TPR, sub = t % TPR;
+    const int row = blockIdx.x * kQB + rl;
+    for (int k = t; k < KD; k += kQB * TPR) {
+        cnt[k] = 0;
+        soff[k] = offs[k];
+    }
+    __syncthreads();
+    const bool live = row < n_out;
+    const int4 q = live ? out_coords[row] : make_int4(0, 0, 0, 0);
+    unsigned long long m0 = 0, m1 = 0;
+    for (int k = sub; k < KD; k += TPR) {
+        int j = -1;
+        if (live) {
+            const int4 o = soff[k];
+            int px, py, pz;
+            bool ok = true;
+            if (!transposed) {
+                px = q.y * sx + o.x;
+                py = q.z * sy + o.y;
+                pz = q.w * sz + o.z;
+            } else {
+                const int nx = q.y + o.x, ny = q.z + o.y, nz = q.w + o.z;
+                ok = nx % sx == 0 && ny % sy == 0 && (dims != 3 || nz % sz == 0);
+                px = nx / sx;
+                py = ny / sy;
+                pz = dims == 3 ? nz / sz : 0;
+            }
+            if (ok && packable(q.x, px, py, pz)) {
+                const unsigned long long key = pack_key(q.x, px, py, pz);
+                const uint64_t s0 = hash_slot(key, mask);
+                j = probe(table, mask, key, s0, __ldg(&table[s0]));
+            }
+        }
+        tile[rl * KD + k] = j;
+        if (j >= 0) {
+            atomicAdd(&cnt[k], 1);
+            if (k < 64) m0 |= 1ull << ((KD < 64 ? KD : 64) - 1 - k);
+            else m1 |= 1ull << (KD - 64 - 1 - (k - 64));
+        }
+    }
+#pragma unroll
+    for (int o = TPR / 2; o >= 1; o >>= 1) {
+        m0 |= __shfl_xor_sync(0xffffffffu, m0, o);
+        m1 |= __shfl_xor_sync(0xffffffffu, m1, o);
+    }
+    __syncthreads();
+    int* dst = os + (size_t)blockIdx.x * kQB * KD;
+    for (int i = t; i < kQB * KD; i += kQB * TPR) __stcs(dst + i, tile[i]);
+    if (sub == 0) {
+        __stcs(masks + (size_t)row * words, m0);
+        if (words == 2) __stcs(masks + (size_t)row * words + 1, m1);
+    }
+    for (int k = t; k < KD; k += kQB * TPR) blk_counts[(size_t)blockIdx.x * KD + k] = cnt[k];
+}
+
 // TPR threads per output row (offsets k = sub, sub+TPR, ...; up to
 // ceil(KD/TPR) independent probes in flight per thread), 128 rows per block.
 // Writes the OS entries + masks of the block (pad rows get -1 / 0) and the
@@ -1161,6 +1230,60 @@ sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t str
     } else {
         launch_query(m, out->coords.as<int4>(), in, st);
     }
+    return m;
+}
+
+// build_kmap with per-axis kernel sizes and dilation (extension). Odd,
+// symmetric kernels with dilation 1 take the standard path.
+sk_kmap* kmap_build_ex(sk_coords* in, sk_coords* out, const int32_t kernel[3],
+                       const int32_t stride[3], const int32_t dilation[3], int transposed,
+                       cudaStream_t st) {
+    validate(in->dims == out->dims, "offset dims mismatch");
+    const int dims = in->dims;
+    int k3[3] = {kernel[0], kernel[1], dims == 3 ? kernel[2] : 1};
+    int d3[3] = {dilation[0], dilation[1], dims == 3 ? dilation[2] : 1};
+    for (int d = 0; d < 3; ++d) {
+        validate(k3[d] >= 1 && k3[d] <= 8, "kernel size per axis must be in [1, 8]");
+        validate(d3[d] >= 1, "dilation components must be >= 1");
+    }
+    for (int d = 0; d < dims; ++d) validate(stride[d] >= 1, "stride components must be >= 1");
+    const int KD = k3[0] * k3[1] * k3[2];
+    validate(KD <= 128, "kernel volume > 128 unsupported");
+    const bool standard = k3[0] == k3[1] && (dims == 2 || k3[1] == k3[2]) && k3[0] % 2 == 1 &&
+                          k3[0] <= 5 && d3[0] == 1 && d3[1] == 1 && d3[2] == 1;
+    if (standard) return kmap_build(in, out, k3[0], stride, transposed, st);
+    coords_build_table(in, st);
+    auto* m = new sk_kmap();
+    m->ctx = in->ctx;
+    m->dims = dims;
+    m->kernel = -1;  // generalized offsets (see kmap_build_ex)
+    m->kd = KD;
+    for (int d = 0; d < 3; ++d) m->stride[d] = d < dims ? stride[d] : 1;
+    m->transposed = transposed;
+    m->n_in = in->n;
+    m->n_out = out->n;
+    alloc_map(m, st);
+    std::vector<int4> h(KD);
+    int n = 0;
+    for (int a = 0; a < k3[0]; ++a)
+        for (int b = 0; b < k3[1]; ++b)
+            for (int c = 0; c < k3[2]; ++c)
+                h[n++] = make_int4(d3[0] * (a - (k3[0] - 1) / 2), d3[1] * (b - (k3[1] - 1) / 2),
+                                   dims == 3 ? d3[2] * (c - (k3[2] - 1) / 2) : 0, 0);
+    DevBuf offs;
+    offs.alloc((size_t)KD * 16, st);
+    SK_CUDA(cudaMemcpyAsync(offs.p, h.data(), (size_t)KD * 16, cudaMemcpyHostToDevice, st));
+    constexpr int TPR = 4;
+    const size_t smem = (size_t)(kQB * KD + ((KD + 3) & ~3)) * 4 + (size_t)KD * 16;
+    if (smem > 48 * 1024)
+        SK_CUDA(cudaFuncSetAttribute(k_kmap_query_gen<TPR>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_kmap_query_gen<TPR><<<m->rows_pad / kQB, kQB * TPR, smem, st>>>(
+        out->coords.as<int4>(), m->n_out, in->table.as<ulonglong2>(), (uint64_t)in->cap - 1,
+        offs.as<int4>(), KD, dims, m->stride[0], m->stride[1], m->stride[2], transposed, m->words,
+        m->os.as<int>(), m->masks.as<unsigned long long>(), m->blk_counts.as<int>());
+    SK_LAUNCH_CHECK();
+    // the offsets table must outlive the kernel: a stream-ordered free
     return m;
 }
 

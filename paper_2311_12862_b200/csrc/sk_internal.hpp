@@ -57,7 +57,8 @@ struct sk_coords : sk::Refcounted {
     std::mutex mu;
     // children: downsampled sets by stride (owned), maps by key (owned)
     std::map<std::tuple<int, int, int>, sk_coords*> down;
-    std::map<std::tuple<uint64_t, int, int, int, int, int>, sk_kmap*> maps;
+    // key: (out id, kernel code, stride xyz, transposed, dilation code)
+    std::map<std::tuple<uint64_t, int, int, int, int, int, int>, sk_kmap*> maps;
     ~sk_coords() override;
 };
 
@@ -107,6 +108,11 @@ void quantize_features(int m, int channels, const double* feats, const int32_t* 
 sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t stride[3],
                     int transposed, cudaStream_t st);
 sk_kmap* kmap_transpose(sk_kmap* m, cudaStream_t st);
+// build_kmap with per-axis (odd or even) kernel sizes and dilation (extension,
+// SURVEY §8(f) rank 3); standard shapes delegate to kmap_build
+sk_kmap* kmap_build_ex(sk_coords* in, sk_coords* out, const int32_t kernel[3],
+                       const int32_t stride[3], const int32_t dilation[3], int transposed,
+                       cudaStream_t st);
 // kmap_from_edges (kmap.cpp:317-336): edges int32 [E][3] = (src, dst, relation)
 // on the device; per relation, pairs stably sorted by dst (WS only)
 sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int relations, int n_in,

@@ -192,13 +192,24 @@ def build_out_coords(coords: CoordSet, stride) -> CoordSet:
     return CoordSet(p, coords.ctx)
 
 
-def build_kmap(inp: CoordSet, out: CoordSet, kernel_size: int, stride=1,
-               transposed: bool = False) -> "KernelMap":
-    """build_kmap_os / build_kmap_ws (kmap.cpp:96-143); cached per MapKey."""
+def build_kmap(inp: CoordSet, out: CoordSet, kernel_size, stride=1,
+               transposed: bool = False, dilation=1) -> "KernelMap":
+    """build_kmap_os / build_kmap_ws (kmap.cpp:96-143); cached per MapKey.
+    kernel_size may be a per-axis triple (odd or even) and dilation an int or
+    triple -- an extension beyond the reference (sk_kmap_build_ex)."""
     p = C.c_void_p()
-    check(lib().sk_kmap_build(inp.ctx.ptr, inp.ptr, out.ptr, kernel_size,
-                              i32x3(_stride3(stride, inp.dims)), int(transposed), _stream(),
-                              C.byref(p)))
+    if isinstance(kernel_size, int) and dilation in (1, (1, 1, 1), [1, 1, 1]):
+        check(lib().sk_kmap_build(inp.ctx.ptr, inp.ptr, out.ptr, kernel_size,
+                                  i32x3(_stride3(stride, inp.dims)), int(transposed), _stream(),
+                                  C.byref(p)))
+    else:
+        k = (kernel_size,) * 3 if isinstance(kernel_size, int) else tuple(kernel_size)
+        d = (dilation,) * 3 if isinstance(dilation, int) else tuple(dilation)
+        if inp.dims == 2:
+            k, d = (k[0], k[1], 1), (d[0], d[1], 1)
+        check(lib().sk_kmap_build_ex(inp.ctx.ptr, inp.ptr, out.ptr, i32x3(k),
+                                     i32x3(_stride3(stride, inp.dims)), i32x3(d), int(transposed),
+                                     _stream(), C.byref(p)))
     return KernelMap(p, inp.ctx)
 
 
