@@ -35,6 +35,124 @@ std::atomic<unsigned long long>& launch_counter() {
     static std::atomic<unsigned long long> c{0};
     return c;
 }
+
+namespace {
+// 4 size classes per octave (<= 25% slack), 4 KB minimum
+size_t size_class(size_t n) {
+    if (n <= 4096) return 4096;
+    const int b = 63 - __builtin_clzll((unsigned long long)(n - 1));
+    const size_t q = (size_t)1 << (b - 2);
+    return (n + q - 1) / q * q;
+}
+struct BlockCache {
+    std::mutex mu;
+    std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free;
+    size_t cached = 0;
+    size_t cap = [] {
+        const char* e = getenv("SK_CACHE_MB");
+        return (size_t)(e ? atol(e) : 4096) << 20;
+    }();
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache();  // never destroyed: no frees after CUDA teardown
+    return *c;
+}
+}  // namespace
+
+void* cache_alloc(size_t n, cudaStream_t s) {
+    const size_t c = size_class(n);
+    BlockCache& bc = block_cache();
+    {
+        std::lock_guard<std::mutex> g(bc.mu);
+        auto it = bc.free.find({s, c});
+        if (it != bc.free.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            bc.cached -= c;
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, c, s) != cudaSuccess) {
+        (void)cudaGetLastError();
+        cache_trim();  // give the cached blocks back to the pool and retry once
+        SK_CUDA(cudaDeviceSynchronize());
+        SK_CUDA(cudaMallocAsync(&p, c, s));
+    }
+    return p;
+}
+
+void cache_free(void* p, size_t n, cudaStream_t s) {
+    const size_t c = size_class(n);
+    BlockCache& bc = block_cache();
+    {
+        std::lock_guard<std::mutex> g(bc.mu);
+        if (bc.cached + c <= bc.cap) {
+            bc.free[{s, c}].push_back(p);
+            bc.cached += c;
+            return;
+        }
+    }
+    cudaFreeAsync(p, s);
+}
+
+void cache_trim() {
+    BlockCache& bc = block_cache();
+    std::lock_guard<std::mutex> g(bc.mu);
+    for (auto& kv : bc.free)
+        for (void* p : kv.second) cudaFreeAsync(p, kv.first.first);
+    bc.free.clear();
+    bc.cached = 0;
+}
+
+namespace {
+struct RbArgs {
+    const uint8_t* src[4];
+    int bytes[4];
+    int n;
+};
+__global__ void k_read_back(RbArgs a, volatile uint8_t* dst) {
+    int o = 0;
+    for (int k = 0; k < a.n; ++k) {
+        for (int i = threadIdx.x; i < a.bytes[k]; i += blockDim.x) dst[o + i] = a.src[k][i];
+        o += a.bytes[k];
+    }
+}
+struct Mapped {
+    uint8_t* h = nullptr;
+    uint8_t* d = nullptr;
+    std::atomic<unsigned> next{0};
+};
+constexpr int kRbSlots = 256, kRbSlotBytes = 64;
+Mapped& mapped() {
+    static Mapped* m = [] {
+        auto* r = new Mapped();
+        SK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&r->h), kRbSlots * kRbSlotBytes,
+                              cudaHostAllocMapped));
+        SK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->d), r->h, 0));
+        return r;
+    }();
+    return *m;
+}
+}  // namespace
+
+void read_back(cudaStream_t st, std::initializer_list<RbSeg> segs, void* dst) {
+    RbArgs a{};
+    size_t total = 0;
+    for (const RbSeg& g : segs) {
+        validate(a.n < 4, "read_back: too many segments");
+        a.src[a.n] = static_cast<const uint8_t*>(g.src);
+        a.bytes[a.n++] = (int)g.bytes;
+        total += g.bytes;
+    }
+    validate(total <= (size_t)kRbSlotBytes, "read_back: too many bytes");
+    Mapped& m = mapped();
+    const unsigned slot = m.next.fetch_add(1) % kRbSlots;
+    k_read_back<<<1, 32, 0, st>>>(a, m.d + slot * kRbSlotBytes);
+    SK_LAUNCH_CHECK();
+    SK_CUDA(cudaStreamSynchronize(st));
+    memcpy(dst, m.h + slot * kRbSlotBytes, total);
+}
 }  // namespace sk
 
 namespace {

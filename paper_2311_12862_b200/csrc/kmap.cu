@@ -962,8 +962,7 @@ void coords_build_table(sk_coords* c, cudaStream_t st) {
         SK_LAUNCH_CHECK();
     }
     int h_err = 0;
-    SK_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
+    read_back(st, {{err.p, 4}}, &h_err);
     validate(h_err == 0,
              "coordinate outside the packable range (batch [0,4096), xyz [-65536,65536))");
     c->has_table = true;
@@ -1004,11 +1003,9 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     // count lands in pos[n] via an inclusive trick: exclusive over n then add
     cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, flag.as<int>(), pos.as<int>(), n, st);
     SK_LAUNCH_CHECK();
-    int h_last_pos = 0, h_last_flag = 0;
-    SK_CUDA(cudaMemcpyAsync(&h_last_pos, pos.as<int>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaMemcpyAsync(&h_last_flag, flag.as<int>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
-    out->n = h_last_pos + h_last_flag;
+    int h_last[2] = {0, 0};
+    read_back(st, {{pos.as<int>() + n - 1, 4}, {flag.as<int>() + n - 1, 4}}, h_last);
+    out->n = h_last[0] + h_last[1];
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
     k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(),
                                       q.as<int4>(), n, out->table.as<ulonglong2>(),
@@ -1052,8 +1049,7 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
                                       err.as<int>());
     SK_LAUNCH_CHECK();
     int h_err = 0;
-    SK_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
+    read_back(st, {{err.p, 4}}, &h_err);
     if (h_err) {
         delete out;
         validate(!(h_err & 1), "non-finite input coordinate");
@@ -1067,11 +1063,9 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
     tmp.alloc(tbytes, st);
     cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, flag.as<int>(), pos.as<int>(), m, st);
     SK_LAUNCH_CHECK();
-    int h_last_pos = 0, h_last_flag = 0;
-    SK_CUDA(cudaMemcpyAsync(&h_last_pos, pos.as<int>() + m - 1, 4, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaMemcpyAsync(&h_last_flag, flag.as<int>() + m - 1, 4, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
-    out->n = h_last_pos + h_last_flag;
+    int h_last[2] = {0, 0};
+    read_back(st, {{pos.as<int>() + m - 1, 4}, {flag.as<int>() + m - 1, 4}}, h_last);
+    out->n = h_last[0] + h_last[1];
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
     k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(), q.as<int4>(),
                                       m, out->table.as<ulonglong2>(), out->coords.as<int4>());
@@ -1166,8 +1160,7 @@ sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int 
                                        vals.as<int>(), counts.as<int>(), err.as<int>());
         SK_LAUNCH_CHECK();
         int h_err = 0;
-        SK_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
-        SK_CUDA(cudaStreamSynchronize(st));
+        read_back(st, {{err.p, 4}}, &h_err);
         if (h_err) {
             delete m;
             validate(!(h_err & 1), "relation id out of range");
@@ -1357,8 +1350,7 @@ int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st) {
     kmap_ensure_ws(m, st);
     if (m->total_pairs_host >= 0) return m->total_pairs_host;
     long long v = 0;
-    SK_CUDA(cudaMemcpyAsync(&v, m->ws_ptr.as<long long>() + m->kd, 8, cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
+    read_back(st, {{m->ws_ptr.as<long long>() + m->kd, 8}}, &v);
     m->total_pairs_host = v;
     return v;
 }

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <initializer_list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -51,7 +52,25 @@ std::atomic<unsigned long long>& launch_counter();
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// ---- device buffer (stream-ordered allocator) ------------------------------
+// ---- device buffer (stream-ordered allocator + host-side block cache) -------
+// Freed blocks stay in a host-side cache per (stream, size class) and go back
+// to the next allocation of that class on the same stream (stream order makes
+// the reuse safe). A run of similar scans then makes no cudaMallocAsync /
+// cudaFreeAsync calls: each costs 1-2 us of host time, and the ~200 per
+// MinkUNet scan fell right after a sync, with the GPU idle (capi.cu).
+void* cache_alloc(size_t n, cudaStream_t s);
+void cache_free(void* p, size_t n, cudaStream_t s);
+void cache_trim();
+// Small device->host reads (counts, error flags) through host-mapped pinned
+// memory written by a one-thread kernel, then a stream sync: no copy engine,
+// so they never queue behind a large D2H on another stream (capi.cu).
+// Segments are concatenated into dst (<= 4 segments, <= 64 bytes in all).
+struct RbSeg {
+    const void* src;
+    size_t bytes;
+};
+void read_back(cudaStream_t st, std::initializer_list<RbSeg> segs, void* dst);
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -73,10 +92,10 @@ struct DevBuf {
         reset();
         stream = s;
         bytes = n;
-        if (n) SK_CUDA(cudaMallocAsync(&p, n, s));
+        if (n) p = cache_alloc(n, s);
     }
     void reset() {
-        if (p) cudaFreeAsync(p, stream);
+        if (p) cache_free(p, bytes, stream);
         p = nullptr;
         bytes = 0;
     }

@@ -211,3 +211,34 @@ def test_tune_result_and_tspw_weights_roundtrip(env, tmp_path):
     y2, _ = net2.forward(cs, x)
     torch.cuda.synchronize()
     assert torch.equal(y1, y2)
+
+
+def test_scan_pipeline_matches_serial_forward(env):
+    """pipeline.ScanPipeline (copy-in / compute / copy-out streams) returns,
+    scan by scan, exactly what a serial H2D -> forward -> D2H returns, in order,
+    including a smaller scan after a larger one and depth 3."""
+    torch, sk, N, M = env
+    from paper_2311_12862_b200.pipeline import ScanPipeline
+    net = N.NetworkRunner(M.minkunet18(), dtype=torch.float16, weight_seed=2)
+    net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large()))  # no red.add: bitwise stable
+    rng = np.random.default_rng(0)
+    scans = []
+    for s, n_pts in enumerate([20000, 8000, 20000, 12000, 5000]):
+        c = scan(n_pts, seed=10 + s)
+        f = rng.standard_normal((len(c), 4)).astype(np.float16)
+        scans.append((torch.from_numpy(c).pin_memory(), torch.from_numpy(f).pin_memory()))
+    want = []
+    for c, f in scans:
+        y, _ = net.forward(sk.CoordSet.create(c.cuda()), f.cuda())
+        want.append(y.cpu().numpy())
+    for depth in (2, 3):
+        pipe = ScanPipeline(net, max(len(c) for c, _ in scans), 4, depth=depth)
+        got = {}
+        pipe.run(scans, on_result=lambda i, h: got.__setitem__(i, h.numpy().copy()))
+        assert sorted(got) == list(range(len(scans)))
+        for i in range(len(scans)):
+            assert got[i].shape == want[i].shape
+            assert np.array_equal(got[i], want[i]), i
+        assert pipe.d2h_bytes == sum(w.nbytes for w in want)
+    with pytest.raises(sk.ValidationError):
+        ScanPipeline(net, 10, 4).run(scans[:1])
