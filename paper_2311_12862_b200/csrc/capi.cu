@@ -36,6 +36,17 @@ std::atomic<unsigned long long>& launch_counter() {
     return c;
 }
 
+void ensure_smem(const void* kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> done;
+    std::lock_guard<std::mutex> g(mu);
+    size_t& have = done[kern];
+    if (smem > have) {
+        SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        have = smem;
+    }
+}
+
 namespace {
 // 4 size classes per octave (<= 25% slack), 4 KB minimum
 size_t size_class(size_t n) {
@@ -50,7 +61,7 @@ struct BlockCache {
     size_t cached = 0;
     size_t cap = [] {
         const char* e = getenv("SK_CACHE_MB");
-        return (size_t)(e ? atol(e) : 4096) << 20;
+        return (size_t)(e ? atol(e) : 32768) << 20;
     }();
 };
 BlockCache& block_cache() {
@@ -241,9 +252,13 @@ sk_status sk_ctx_create(int device, sk_ctx** out) {
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t thr = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            // pre-grow the pool once so steady-state scans never map new memory
+            // pre-grow the pool once so steady-state scans never map new
+            // memory: growing it mid-run blocked the whole device for
+            // 10-100 ms per cudaMallocAsync (several runners in flight)
+            const char* pg = getenv("SK_POOL_MB");
+            const size_t grow = (size_t)(pg ? atol(pg) : 16384) << 20;
             void* p = nullptr;
-            if (cudaMallocAsync(&p, (size_t)2 << 30, nullptr) == cudaSuccess)
+            if (grow && cudaMallocAsync(&p, grow, nullptr) == cudaSuccess)
                 cudaFreeAsync(p, nullptr);
             cudaStreamSynchronize(nullptr);
         }

@@ -1634,12 +1634,7 @@ void launch_tc_variant(const ConvArgs& a, const CUtensorMap& ta, const CUtensorM
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
                         (2 * stages + 4 + 3 * kIdxRing) * 8 + 16 + kIdxRing * sizeof(CSlot<PW>);
     auto kern = k_gconv_tc<T, KC, TMA, SLABS, PW>;
-    static size_t configured = 0;  // per template instantiation
-    if (smem > configured) {
-        SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        configured = smem;
-    }
+    ensure_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, Roles<PW>::kThreads, smem, st>>>(ta, tb, a, stages, acc_bufs);
     SK_LAUNCH_CHECK();
 }
@@ -1863,12 +1858,7 @@ bool conv_small_cin(const sk_kmap* m, int c_in, int c_out, const void* x, const 
                     const void* residual, float* y_accum, cudaStream_t st) {
     auto launch = [&](auto kern) {
         const size_t smem = (size_t)m->kd * c_in * c_out * 4;
-        static size_t configured = 0;
-        if (smem > configured) {
-            SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-            configured = smem;
-        }
+        ensure_smem(reinterpret_cast<const void*>(kern), smem);
         const int grid = (int)std::min<int64_t>(ceil_div(m->n_out, 64), (int64_t)m->ctx->num_sms * 8);
         kern<<<grid, 256, smem, st>>>(
             m->os.as<int>(), m->n_out, m->kd, static_cast<const T*>(x), static_cast<const T*>(w),
@@ -2135,12 +2125,7 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
         const int stages = (int)std::max<size_t>(2, std::min<size_t>(8, (200 * 1024) / stage_bytes));
         const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
         auto kern = dt == SK_F16 ? k_wgrad_tc<__half> : k_wgrad_tc<__nv_bfloat16>;
-        static size_t configured = 0;
-        if (smem > configured) {
-            SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-            configured = smem;
-        }
+        ensure_smem(reinterpret_cast<const void*>(kern), smem);
         kern<<<ctx->num_sms, kWgThreads, smem, st>>>(a, stages);
         SK_LAUNCH_CHECK();
         return;

@@ -892,9 +892,7 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
         const int grid = m->rows_pad / kQB;
         const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
         auto run = [&](auto kern) {
-            if (smem > 48 * 1024)
-                SK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
+            ensure_smem(reinterpret_cast<const void*>(kern), smem);
             kern<<<grid, kQB, smem, st>>>(out_coords, m->n_out, in->btable.as<ulonglong2>(),
                                           (uint64_t)in->bcap - 1, in->bdense.as<int>(), m->words,
                                           m->os.as<int>(), m->masks.as<unsigned long long>(),
@@ -909,9 +907,7 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
     const uint64_t mask = (uint64_t)in->cap - 1;
     const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
 #define SK_Q(KDV, TPRV)                                                                      \
-    if (smem > 48 * 1024)                                                                    \
-        SK_CUDA(cudaFuncSetAttribute(k_kmap_query<KDV, TPRV>,                                \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    ensure_smem(reinterpret_cast<const void*>(k_kmap_query<KDV, TPRV>), smem);               \
     k_kmap_query<KDV, TPRV><<<grid, kQB * TPRV, smem, st>>>(                                 \
         out_coords, m->n_out, in->table.as<ulonglong2>(), mask,                              \
         m->kernel, m->dims, m->stride[0], m->stride[1], m->stride[2], m->transposed, m->words, \
@@ -1268,9 +1264,7 @@ sk_kmap* kmap_build_ex(sk_coords* in, sk_coords* out, const int32_t kernel[3],
     SK_CUDA(cudaMemcpyAsync(offs.p, h.data(), (size_t)KD * 16, cudaMemcpyHostToDevice, st));
     constexpr int TPR = 4;
     const size_t smem = (size_t)(kQB * KD + ((KD + 3) & ~3)) * 4 + (size_t)KD * 16;
-    if (smem > 48 * 1024)
-        SK_CUDA(cudaFuncSetAttribute(k_kmap_query_gen<TPR>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem(reinterpret_cast<const void*>(k_kmap_query_gen<TPR>), smem);
     k_kmap_query_gen<TPR><<<m->rows_pad / kQB, kQB * TPR, smem, st>>>(
         out->coords.as<int4>(), m->n_out, in->table.as<ulonglong2>(), (uint64_t)in->cap - 1,
         offs.as<int4>(), KD, dims, m->stride[0], m->stride[1], m->stride[2], transposed, m->words,
@@ -1304,9 +1298,7 @@ sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
         SK_LAUNCH_CHECK();
     }
     size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
-    if (smem > 48 * 1024)
-        SK_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+    ensure_smem(reinterpret_cast<const void*>(k_finalize), smem);
     k_finalize<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd, m->words,
                                                m->masks.as<unsigned long long>(),
                                                m->blk_counts.as<int>());
@@ -1334,9 +1326,7 @@ void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
                                   m->ws_tile_ptr.as<int>());
     SK_LAUNCH_CHECK();
     size_t smem = (size_t)kQB * m->kd * 4;
-    if (smem > 48 * 1024)
-        SK_CUDA(cudaFuncSetAttribute(k_ws_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+    ensure_smem(reinterpret_cast<const void*>(k_ws_scatter), smem);
     k_ws_scatter<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd,
                                                  m->blk_off.as<long long>(),
                                                  m->ws_ptr.as<long long>(), m->ws_tile_ptr.as<int>(),

@@ -71,6 +71,11 @@ struct RbSeg {
 };
 void read_back(cudaStream_t st, std::initializer_list<RbSeg> segs, void* dst);
 
+// Raise a kernel's dynamic shared memory limit to >= smem, once per (kernel,
+// high-water mark). Serialised and keyed by the kernel's address: runners on
+// several host threads launch the same kernels concurrently (capi.cu).
+void ensure_smem(const void* kern, size_t smem);
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import DataflowCfg, check, lib
+from ._lib import DataflowCfg, ValidationError, check, lib
 from .models import spec_text
 from .sparse import (Context, CoordSet, DataflowConfig, TilePreset, _DTYPES, _ptr, _stream)
 
@@ -129,8 +129,11 @@ class NetworkRunner:
         return cfg_from_c(c)
 
     # ---- execution ----
-    def forward(self, coords: CoordSet, feats: torch.Tensor, stats: bool = False):
-        """NetworkRunner::forward; returns (features [n_out, c_out] torch copy, stats)."""
+    def forward(self, coords: CoordSet, feats: torch.Tensor, stats: bool = False,
+                out: torch.Tensor | None = None):
+        """NetworkRunner::forward; returns (features [n_out, c_out] torch copy, stats).
+        out: optional preallocated [>= n_out, c_out] device tensor the result is
+        copied into (on the current stream) instead of a fresh allocation."""
         feats = feats.to(device="cuda", dtype=self.dtype).contiguous()
         out_p, n_out = C.c_void_p(), C.c_int()
         mp = np.zeros(self.num_groups) if stats else None
@@ -141,7 +144,13 @@ class NetworkRunner:
                                    kr.ctypes.data_as(C.c_void_p) if stats else None))
         self._last_in = feats
         co = self.layer_shapes[-1][2]
-        y = self._wrap(out_p.value, n_out.value, co)
+        if out is not None:
+            if out.shape[0] < n_out.value or out.shape[1] != co or out.dtype != self.dtype:
+                raise ValidationError("out must be [>= n_out, c_out] in the runner's dtype")
+            y = out[:n_out.value]
+            y.copy_(device_view(out_p.value, (n_out.value, co), self.dtype))
+        else:
+            y = self._wrap(out_p.value, n_out.value, co)
         return y, ({"mapping_ms": mp, "kernel_ms": kr} if stats else None)
 
     def _wrap(self, ptr, rows, cols):

@@ -214,9 +214,10 @@ def test_tune_result_and_tspw_weights_roundtrip(env, tmp_path):
 
 
 def test_scan_pipeline_matches_serial_forward(env):
-    """pipeline.ScanPipeline (copy-in / compute / copy-out streams) returns,
-    scan by scan, exactly what a serial H2D -> forward -> D2H returns, in order,
-    including a smaller scan after a larger one and depth 3."""
+    """pipeline.ScanPipeline (copy-in / compute / copy-out streams, 1-3 worker
+    threads with replicated runners) returns, scan by scan, exactly what a
+    serial H2D -> forward -> D2H returns, including a smaller scan after a
+    larger one and depth 3."""
     torch, sk, N, M = env
     from paper_2311_12862_b200.pipeline import ScanPipeline
     net = N.NetworkRunner(M.minkunet18(), dtype=torch.float16, weight_seed=2)
@@ -231,8 +232,10 @@ def test_scan_pipeline_matches_serial_forward(env):
     for c, f in scans:
         y, _ = net.forward(sk.CoordSet.create(c.cuda()), f.cuda())
         want.append(y.cpu().numpy())
-    for depth in (2, 3):
-        pipe = ScanPipeline(net, max(len(c) for c, _ in scans), 4, depth=depth)
+    from paper_2311_12862_b200.pipeline import replicate
+    for depth, workers in ((2, 1), (3, 1), (2, 2), (2, 3)):
+        pipe = ScanPipeline(replicate(net, workers), max(len(c) for c, _ in scans), 4,
+                            depth=depth)
         got = {}
         pipe.run(scans, on_result=lambda i, h: got.__setitem__(i, h.numpy().copy()))
         assert sorted(got) == list(range(len(scans)))

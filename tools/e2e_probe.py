@@ -95,6 +95,48 @@ def main():
     window(piped(True), "ScanPipeline, flush")
     window(piped(False), "ScanPipeline, no flush")
     window(piped(True), "ScanPipeline, flush (again)")
+    # W host threads, each with its own NetworkRunner (same configs) on its
+    # own CUDA stream: one runner's sync bubbles are filled by the other's work
+    import threading
+    for W in (2, 3):
+        nets = [net]
+        for _ in range(W - 1):
+            n2 = NetworkRunner(bench.model_for("infer"), dtype=torch.float16, weight_seed=3)
+            for g in range(net.num_groups):
+                n2.set_config(g, net.config(g))
+            nets.append(n2)
+        streams = [torch.cuda.Stream() for _ in range(W)]
+
+        def conc(flushing, idxs):
+            start = torch.cuda.Event()
+            start.record()
+
+            def worker(w):
+                with torch.cuda.stream(streams[w]):
+                    torch.cuda.current_stream().wait_event(start)
+                    for i in idxs[w::W]:
+                        if flushing:
+                            flush.zero_()
+                        cs = sk.CoordSet.create(dev_c[i])
+                        nets[w].forward(cs, dev_f[i])
+            th = [threading.Thread(target=worker, args=(w,)) for w in range(W)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            for st_ in streams:
+                torch.cuda.current_stream().wait_stream(st_)
+
+        for flushing in (True, False):
+            conc(flushing, list(range(3 * W)))
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            conc(flushing, list(range(3, n)))
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"{W} threads x streams, flush={flushing}: window "
+                  f"{e0.elapsed_time(e1) / (n - 3):7.3f} ms/scan")
     if os.environ.get("E2E_TRACE"):
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
