@@ -442,7 +442,7 @@ def run_train(args, rank, world, local):
         tuned = {"tune_s": time.perf_counter() - t0, "tuned_train_ms_per_scan": lat,
                  "configs": {ph: [net.config(g, ph).name() for g in range(net.num_groups)]
                              for ph in ("forward", "dgrad", "wgrad")}}
-    tr = DataParallelTrainer(net, lr=1e-3, momentum=0.9)
+    tr = DataParallelTrainer(net, lr=1e-3, momentum=0.9, replicas=max(1, args.concurrency))
     rng = np.random.default_rng(rank)
     prepared = []
     for scans in batches:
@@ -488,6 +488,8 @@ def run_train(args, rank, world, local):
                                    "wgrad, SGD), global batch 8 synthetic ~128k-voxel scans, "
                                    "scene-sharded DP with bucketed NCCL all-reduce",
                        "global_batch": B, "parallelism": f"dp{world}",
+                       "concurrency": f"{len(tr.nets)} runner replicas per GPU (host threads x "
+                                      "CUDA streams), gradients folded before the last scene",
                        "params": int(net.num_params),
                        "dataflow": tuned if tuned else "implicit_gemm s1 (all groups, untuned)"},
             "gpu_launches": int(_lib.lib().sk_kernel_launches() - launches0),

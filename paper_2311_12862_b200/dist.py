@@ -9,12 +9,20 @@ bucket is all-reduced asynchronously (NCCL over NVLink via torch.distributed),
 so communication overlaps the remaining dgrad/wgrad. fp32 master weights take
 an SGD-momentum step and are written back to the runner's fp16 weights.
 
+With replicas=W > 1 a rank also keeps W NetworkRunners on its GPU (same
+weights and configs, pipeline.replicate), each on its own host thread and CUDA
+stream with its own fp32 gradient buffer: the rank's scenes are dealt to them
+round-robin, so one runner's host syncs (output-coordinate counts) are filled
+by the others' kernels. Their gradients are summed into the main buffer before
+the main runner's last scene, whose bucketed backward still overlaps NCCL.
+
 The bucketing / sharding / reduction logic is device-agnostic so it is
 covered on CPU with gloo (tests/test_dist_cpu.py).
 """
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import torch
@@ -90,8 +98,10 @@ class DataParallelTrainer:
     weights and gradients, SGD with momentum."""
 
     def __init__(self, net, lr: float = 1e-2, momentum: float = 0.9,
-                 bucket_bytes: int = 25 << 20, group=None):
+                 bucket_bytes: int = 25 << 20, group=None, replicas: int = 1):
         self.net = net
+        from .pipeline import replicate
+        self.nets = replicate(net, max(1, replicas))
         self.lr, self.momentum = lr, momentum
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -104,18 +114,46 @@ class DataParallelTrainer:
             dist.broadcast(self.master, src=0, group=group)
             self._push_weights()
         self.grad = torch.zeros_like(self.master)
+        self.rgrads = [torch.zeros_like(self.master) for _ in self.nets[1:]]
+        self.rstreams = [torch.cuda.Stream() for _ in self.nets[1:]]
         self.mom = torch.zeros_like(self.master)
         self.reducer = GradReducer(self.grad, group)
 
     def _push_weights(self):
-        for i, (kd, ci, co, off) in enumerate(self.net.layer_shapes):
-            self.net.weight(i).copy_(self.master[off:off + kd * ci * co].view(kd, ci, co))
-        self.net.weights_updated()
+        for n in self.nets:
+            for i, (kd, ci, co, off) in enumerate(n.layer_shapes):
+                n.weight(i).copy_(self.master[off:off + kd * ci * co].view(kd, ci, co))
+            n.weights_updated()
+
+    @staticmethod
+    def _scene_grad(net, cs, x, tgt, global_batch):
+        y, _ = net.forward(cs, x)
+        diff = y.float() - tgt.float()
+        return (diff * diff).mean(), (2.0 / (diff.numel() * global_batch)) * diff
+
+    def _replica_scenes(self, r, scenes, global_batch, start, out):
+        """Replica r >= 1: its scenes on its own stream into rgrads[r-1]."""
+        try:
+            torch.cuda.set_device(self.grad.device)
+            st = self.rstreams[r - 1]
+            with torch.cuda.stream(st):
+                st.wait_event(start)
+                loss = torch.zeros((), device="cuda")
+                for k, (cs, x, tgt) in enumerate(scenes):
+                    l, g = self._scene_grad(self.nets[r], cs, x, tgt, global_batch)
+                    loss += l
+                    self.nets[r].backward(g, self.rgrads[r - 1], accumulate=k > 0)
+                out[r] = loss
+        except BaseException as e:
+            out[r] = e
 
     def train_step(self, scenes, global_batch: int):
         """scenes: this rank's [(CoordSet, feats, target)]; loss = mean over the
         global batch of per-scan mean squared error. Returns the local loss sum."""
         loss_sum = torch.zeros((), device="cuda")
+        W = len(self.nets)
+        if W > 1 and len(scenes) > 1:
+            return self._train_step_replicas(scenes, global_batch)
         for si, (cs, x, tgt) in enumerate(scenes):
             y, _ = self.net.forward(cs, x)
             diff = y.float() - tgt.float()
@@ -134,6 +172,48 @@ class DataParallelTrainer:
                 self.reducer.launch(b)
         self.reducer.wait()
         # SGD with momentum on the fp32 master copy
+        self.mom.mul_(self.momentum).add_(self.grad)
+        self.master.add_(self.mom, alpha=-self.lr)
+        self._push_weights()
+        return loss_sum
+
+    def _train_step_replicas(self, scenes, global_batch: int):
+        W = min(len(self.nets), len(scenes))
+        mine = scenes[0::W]
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(cur)
+        out = [None] * W
+        th = [threading.Thread(target=self._replica_scenes,
+                               args=(r, scenes[r::W], global_batch, start, out))
+              for r in range(1, W)]
+        for t in th:
+            t.start()
+        loss_sum = torch.zeros((), device="cuda")
+        for si, (cs, x, tgt) in enumerate(mine[:-1]):  # concurrently with the replicas
+            l, g = self._scene_grad(self.net, cs, x, tgt, global_batch)
+            loss_sum += l
+            self.net.backward(g, self.grad, accumulate=si > 0)
+        for t in th:
+            t.join()
+        for r in range(1, W):
+            if isinstance(out[r], BaseException):
+                raise out[r]
+            cur.wait_stream(self.rstreams[r - 1])
+            loss_sum += out[r]
+        # fold the replicas' gradients in, then the main runner's last scene
+        # runs bucket by bucket with each finished bucket all-reduced
+        if len(mine) == 1:
+            self.grad.zero_()
+        for rg in self.rgrads[:W - 1]:
+            self.grad.add_(rg)
+        cs, x, tgt = mine[-1]
+        l, g = self._scene_grad(self.net, cs, x, tgt, global_batch)
+        loss_sum += l
+        for b in self.buckets:
+            self.net.backward(g, self.grad, b.layer_hi, b.layer_lo, accumulate=True)
+            self.reducer.launch(b)
+        self.reducer.wait()
         self.mom.mul_(self.momentum).add_(self.grad)
         self.master.add_(self.mom, alpha=-self.lr)
         self._push_weights()
