@@ -32,12 +32,16 @@ def scan(n_points, seed=1):
 
 
 def timeit(fn, warm=2, reps=5):
+    """Device time of fn: a ~50 us GPU sleep is queued ahead of the start event
+    so the host's Python/ctypes/launch overhead overlaps it instead of being
+    counted (it dominated layers under ~50 us)."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(100_000)
         a.record()
         fn()
         b.record()
@@ -95,7 +99,8 @@ def main():
                           f"{res[best]:.4f} ms {flops / res[best] / 1e9:.1f} TF/s", flush=True)
     names = [cfg.name() for cfg in space()]
     lines = ["# Layer sweep (BASELINE configs[4]): forward ms per dataflow, fp16 in / fp32 acc",
-             "", "tools/sweep.py on one B200; warm maps; algorithmic TFLOP/s = "
+             "", "tools/sweep.py on one B200; warm maps; device time per call (a GPU sleep "
+             "ahead of the start event hides host launch overhead); algorithmic TFLOP/s = "
              "2*pairs*C^2 / best time (padded MACs not credited).", "",
              "| N | K | mode | C | pairs | " + " | ".join(n.replace("implicit_gemm_", "ig_")
                                                       .replace("_offline", "") for n in names)
