@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--workers", type=int, nargs="+", default=[1, 2, 3])
     a = ap.parse_args()
     if os.environ.get("NO_GC"):
         import gc
@@ -43,8 +44,8 @@ def main():
     dev_c = [torch.from_numpy(c).cuda() for c in scans]
     dev_f = [torch.from_numpy(f).cuda() for f in feats]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    nets = replicate(net, 3)
-    streams = [torch.cuda.Stream() for _ in range(3)]
+    nets = replicate(net, max(a.workers))
+    streams = [torch.cuda.Stream() for _ in range(max(a.workers))]
     if os.environ.get("GC_FREEZE"):
         import gc
         gc.collect()
@@ -83,11 +84,11 @@ def main():
         for s in streams[:W]:
             cur.wait_stream(s)
 
-    for W in (1, 2, 3):
+    for W in a.workers:
         run(W, True)
     torch.cuda.synchronize()
-    for W in (1, 2, 3):
-        for flushing in (True, False):
+    for W in a.workers:
+        for flushing in (True,):
             res = []
             for _ in range(a.reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
