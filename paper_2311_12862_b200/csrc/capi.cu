@@ -36,6 +36,15 @@ std::atomic<unsigned long long>& launch_counter() {
     return c;
 }
 
+void stream_after(const BuiltOn& on, cudaStream_t st) {
+    if (!on.set || on.s == st) return;
+    cudaEvent_t ev;
+    SK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SK_CUDA(cudaEventRecord(ev, on.s));
+    SK_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    SK_CUDA(cudaEventDestroy(ev));  // released once the recorded work completes
+}
+
 void ensure_smem(const void* kern, size_t smem) {
     static std::mutex mu;
     static std::map<const void*, size_t> done;
@@ -294,6 +303,7 @@ sk_status sk_quantize(sk_ctx* ctx, int dims, int m, const double* d_raw, const i
         sk::validate(ctx && out && voxel, "null argument");
         sk::validate(m == 0 || d_raw, "null raw points");
         *out = sk::coords_quantize(ctx, dims, m, d_raw, d_batch, voxel, d_point_rows, S(stream));
+        (*out)->built_on.mark(S(stream));
     });
 }
 
@@ -359,9 +369,12 @@ sk_status sk_out_coords(sk_ctx* ctx, sk_coords* in, const int32_t stride[3], voi
         std::lock_guard<std::mutex> lock(in->mu);
         auto it = in->down.find(key);
         if (it == in->down.end()) {
+            sk::stream_after(in->built_on, S(stream));
             sk_coords* c = sk::coords_downsample(in, stride, S(stream));
+            c->built_on.mark(S(stream));
             it = in->down.emplace(key, c).first;
         }
+        sk::stream_after(it->second->built_on, S(stream));
         it->second->refs.fetch_add(1);
         *out = it->second;
     });
@@ -371,7 +384,8 @@ namespace {
 // MapCache (kmap.cpp:359-391): one build per key; kcode = K for the standard
 // odd symmetric kernels, 256 + (kx | ky << 4 | kz << 8) for generalized ones
 sk_kmap* cached_map(sk_coords* in, sk_coords* out, int kcode, const int32_t stride[3],
-                    int transposed, int dcode, const std::function<sk_kmap*()>& build) {
+                    int transposed, int dcode, cudaStream_t st,
+                    const std::function<sk_kmap*()>& build) {
     auto key = std::make_tuple(out->id, kcode, stride[0], stride[1],
                                in->dims == 3 ? stride[2] : 1, transposed ? 1 : 0, dcode);
     sk_kmap* m = nullptr;
@@ -381,12 +395,16 @@ sk_kmap* cached_map(sk_coords* in, sk_coords* out, int kcode, const int32_t stri
         if (it != in->maps.end()) m = it->second;
     }
     if (!m) {
+        sk::stream_after(in->built_on, st);  // sets built lazily on another stream
+        sk::stream_after(out->built_on, st);
         sk_kmap* built = build();
+        built->built_on.mark(st);
         std::lock_guard<std::mutex> lock(in->mu);
         auto ins = in->maps.emplace(key, built);
         if (!ins.second) release_kmap(built);  // lost a race: builds once per key
         m = ins.first->second;
     }
+    sk::stream_after(m->built_on, st);
     m->refs.fetch_add(1);
     return m;
 }
@@ -396,7 +414,7 @@ sk_status sk_kmap_build(sk_ctx* ctx, sk_coords* in, sk_coords* out, int kernel_s
                         const int32_t stride[3], int transposed, void* stream, sk_kmap** map) {
     return guard([&] {
         sk::validate(ctx && in && out && map, "null argument");
-        *map = cached_map(in, out, kernel_size, stride, transposed, 0, [&] {
+        *map = cached_map(in, out, kernel_size, stride, transposed, 0, S(stream), [&] {
             return sk::kmap_build(in, out, kernel_size, stride, transposed, S(stream));
         });
     });
@@ -416,7 +434,7 @@ sk_status sk_kmap_build_ex(sk_ctx* ctx, sk_coords* in, sk_coords* out, const int
                               kernel[0] <= 5 && dilation[0] == 1 && dilation[1] == 1 && dz == 1;
         const int kcode = standard ? kernel[0] : 256 + (kernel[0] | kernel[1] << 4 | kz << 8);
         const int dcode = standard ? 0 : (dilation[0] | dilation[1] << 10 | dz << 20);
-        *map = cached_map(in, out, kcode, stride, transposed, dcode, [&] {
+        *map = cached_map(in, out, kcode, stride, transposed, dcode, S(stream), [&] {
             return sk::kmap_build_ex(in, out, kernel, stride, dilation, transposed, S(stream));
         });
     });
@@ -534,6 +552,7 @@ sk_status sk_conv_forward(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg,
         sk::validate(ctx && map && cfg, "null argument");
         sk::validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
                      "convolution dtype must be f32, f16 or bf16");
+        sk::stream_after(map->built_on, S(stream));  // map fetched on another stream
         sk::conv_forward(ctx, map, *cfg, dtype, c_in, c_out, d_x, d_w, d_y, false, S(stream));
     });
 }
@@ -545,6 +564,7 @@ sk_status sk_conv_dgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, s
         sk::validate(ctx && map && cfg, "null argument");
         sk::validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
                      "convolution dtype must be f32, f16 or bf16");
+        sk::stream_after(map->built_on, S(stream));  // map fetched on another stream
         sk::conv_forward(ctx, map, *cfg, dtype, c_in, c_out, d_dy, d_w, d_dx, true, S(stream));
     });
 }
@@ -556,6 +576,7 @@ sk_status sk_conv_wgrad(sk_ctx* ctx, sk_kmap* map, const sk_dataflow_cfg* cfg, s
         sk::validate(ctx && map && cfg, "null argument");
         sk::validate(dtype == SK_F32 || dtype == SK_F16 || dtype == SK_BF16,
                      "convolution dtype must be f32, f16 or bf16");
+        sk::stream_after(map->built_on, S(stream));  // map fetched on another stream
         sk::conv_wgrad(ctx, map, *cfg, dtype, c_in, c_out, d_x, d_dy, d_dw, S(stream));
     });
 }

@@ -853,7 +853,11 @@ int64_t pow2_cap(int64_t n) {
 
 void coords_build_blocks(sk_coords* c, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(c->mu);
-    if (c->has_blocks) return;
+    if (c->has_blocks) {
+        stream_after(c->blocks_on, st);
+        return;
+    }
+    c->blocks_on.mark(st);
     int64_t cap = 64;
     while (cap < 2 * (int64_t)c->n) cap <<= 1;  // n_blocks <= n: load <= 1/2 worst case
     c->bcap = cap;
@@ -1188,6 +1192,8 @@ sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int 
         SK_LAUNCH_CHECK();
     }
     m->has_ws = true;
+    m->ws_on.mark(st);
+    m->built_on.mark(st);
     m->total_pairs_host = E;
     return m;
 }
@@ -1278,7 +1284,10 @@ sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
     // transpose_map rejects graph maps (kmap.cpp:290-295): so does conv_dgrad on them
     contract(!src->graph, "graph maps cannot be transposed");
     std::lock_guard<std::mutex> lock(src->mu);
-    if (src->transpose_cache) return src->transpose_cache;
+    if (src->transpose_cache) {
+        stream_after(src->transpose_cache->built_on, st);
+        return src->transpose_cache;
+    }
     auto* m = new sk_kmap();
     m->ctx = src->ctx;
     m->dims = src->dims;
@@ -1303,13 +1312,18 @@ sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
                                                m->masks.as<unsigned long long>(),
                                                m->blk_counts.as<int>());
     SK_LAUNCH_CHECK();
+    m->built_on.mark(st);
     src->transpose_cache = m;  // owned by src, released in ~sk_kmap
     return m;
 }
 
 void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(m->mu);
-    if (m->has_ws) return;
+    if (m->has_ws) {
+        stream_after(m->ws_on, st);
+        return;
+    }
+    m->ws_on.mark(st);
     m->ws_ptr.alloc((size_t)(m->kd + 1) * 8, st);
     m->ws_tile_ptr.alloc((size_t)(m->kd + 1) * 4, st);
     m->blk_off.alloc((size_t)m->n_blocks * m->kd * 8, st);
@@ -1353,7 +1367,10 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(m->mu);
     auto key = std::make_pair(splits, pad);
     auto it = m->prepared.find(key);
-    if (it != m->prepared.end()) return it->second.get();
+    if (it != m->prepared.end()) {
+        stream_after(it->second->built_on, st);
+        return it->second.get();
+    }
 
     auto p = std::make_unique<Prepared>();
     p->splits = splits;
@@ -1463,6 +1480,7 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
         p->masks.as<unsigned long long>(), p->tile_masks.as<unsigned long long>());
     SK_LAUNCH_CHECK();
     Prepared* raw = p.get();
+    raw->built_on.mark(st);
     m->prepared[key] = std::move(p);
     return raw;
 }

@@ -61,6 +61,21 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 void* cache_alloc(size_t n, cudaStream_t s);
 void cache_free(void* p, size_t n, cudaStream_t s);
 void cache_trim();
+// Cross-stream readiness of a lazily built, cached object (map, prepared map,
+// transposed map, pair lists, down-sampled set, block index): `on` is the
+// stream it was built on. A caller on another stream waits for everything
+// enqueued on `on` so far (an event recorded now: it may over-wait, never
+// under-wait). Same stream: nothing to do, so the single-stream hot path pays
+// nothing (capi.cu).
+struct BuiltOn {
+    cudaStream_t s = nullptr;
+    bool set = false;  // unset: built synchronously / not lazily, nothing to wait for
+    void mark(cudaStream_t st) {
+        s = st;
+        set = true;
+    }
+};
+void stream_after(const BuiltOn& on, cudaStream_t st);
 // Small device->host reads (counts, error flags) through host-mapped pinned
 // memory written by a one-thread kernel, then a stream sync: no copy engine,
 // so they never queue behind a large D2H on another stream (capi.cu).

@@ -32,6 +32,7 @@ struct Prepared {
     std::vector<int> word_off;
     DevBuf tile_masks;       // num_splits x n_tiles(of 128) x 2 u64 (OR of row masks)
     int tile_rows = 128;
+    BuiltOn built_on;
 };
 
 }  // namespace sk
@@ -55,6 +56,8 @@ struct sk_coords : sk::Refcounted {
     int64_t bcap = 0;
     bool has_blocks = false;
     std::mutex mu;
+    sk::BuiltOn built_on;   // stream of a lazily built (down-sampled / quantized) set
+    sk::BuiltOn blocks_on;  // stream the block index was built on
     // children: downsampled sets by stride (owned), maps by key (owned)
     std::map<std::tuple<int, int, int>, sk_coords*> down;
     // key: (out id, kernel code, stride xyz, transposed, dilation code)
@@ -87,6 +90,8 @@ struct sk_kmap : sk::Refcounted {
     std::map<std::pair<int, int>, std::unique_ptr<sk::Prepared>> prepared;
     sk_kmap* transpose_cache = nullptr;  // owned
     std::mutex mu;
+    sk::BuiltOn built_on;  // stream the map was built on (stream_after)
+    sk::BuiltOn ws_on;     // stream the pair lists were built on
     ~sk_kmap() override;
 };
 

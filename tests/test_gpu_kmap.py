@@ -133,6 +133,60 @@ def test_map_cache_builds_once(sk):
     assert sk.build_out_coords(c, 1).id == c.id  # submanifold keeps the set
 
 
+def test_map_cache_threads_and_streams(sk):
+    """MapCache once-per-key under an 8-thread race (test_kmap.cpp:227-264),
+    with every thread on its own CUDA stream: all threads get the same cached
+    map / down-sampled set / prepared map, and the convs they launch right
+    after the cache hit on their own stream see the complete structures
+    (stream_after: the cached object's build stream is waited for)."""
+    import threading
+    import torch
+    from paper_2311_12862_b200.synth import lidar_scan
+    coords = torch.from_numpy(lidar_scan(120_000, seed=9)).cuda()
+    x = torch.randn(coords.shape[0], 32, device="cuda").half()
+    w = (torch.randn(27, 32, 32, device="cuda") / 30).half()
+    cfg = sk.DataflowConfig(sk.IMPLICIT_GEMM, 2, sk.tile_large())
+    det = sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large())  # no red.add: bitwise stable
+    c0 = sk.CoordSet.create(coords)
+    m0 = sk.build_kmap(c0, c0, 3, 1)
+    d0 = sk.build_out_coords(c0, 2)
+    md0 = sk.build_kmap(c0, d0, 3, 2)
+    want = [sk.conv_forward(m0, x, w, det).cpu(), sk.conv_forward(md0, x, w, det).cpu(),
+            sk.conv_forward(m0, x, w, cfg).float().cpu()]
+    shared = sk.CoordSet.create(coords)
+    torch.cuda.synchronize()
+    T = 8
+    barrier = threading.Barrier(T)
+    out = [None] * T
+
+    def work(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                barrier.wait()
+                m = sk.build_kmap(shared, shared, 3, 1)
+                d = sk.build_out_coords(shared, 2)
+                md = sk.build_kmap(shared, d, 3, 2)
+                ys = [sk.conv_forward(m, x, w, det), sk.conv_forward(md, x, w, det),
+                      sk.conv_forward(m, x, w, cfg).float()]
+                s.synchronize()
+                out[t] = (m.ptr.value, d.id, md.ptr.value, [y.cpu() for y in ys])
+        except BaseException as e:
+            out[t] = e
+    th = [threading.Thread(target=work, args=(t,)) for t in range(T)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in out:
+        assert not isinstance(r, BaseException), r
+    assert len({r[0] for r in out}) == 1 and len({r[1] for r in out}) == 1
+    assert len({r[2] for r in out}) == 1
+    for r in out:
+        assert torch.equal(r[3][0], want[0]) and torch.equal(r[3][1], want[1])
+        assert torch.allclose(r[3][2], want[2], rtol=1e-2, atol=1e-2)
+
+
 def test_validation_errors(sk):
     with pytest.raises(sk.ValidationError):
         sk.CoordSet.create(np.array([[0, 70000, 0, 0]], np.int32))  # outside packable range
