@@ -38,6 +38,7 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "sk_internal.hpp"
 
@@ -1317,6 +1318,68 @@ __global__ void k_scatter_add(const float* __restrict__ buf, int c, const int* _
 // wgrad SIMT: one block per (offset, ci-tile 32, co-tile 32, pair-chunk);
 // dW_k[ci][co] += sum_p x[in[p]][ci] * dy[out[p]][co], fp32 atomics across
 // pair chunks (deterministic: one chunk).
+// wgrad for tiny C_in (the 4-channel stem): dW[k][ci][co] = sum over offset
+// k's pairs of x[in][ci] * dy[out][co]. Lane = output channel (coalesced dy
+// row loads), warps stride over the pairs with the CI input values broadcast,
+// CI fp32 accumulators per lane; the block's 8 warps reduce in smem and flush
+// one red.add per (ci, co). The 32x32-tile SIMT kernel wasted 28 of 32 rows
+// of every tile on C_in = 4 (337 us -> tens of us per MinkUNet scan).
+template <typename T, int CI>
+__global__ void __launch_bounds__(256) k_wgrad_small_cin(const T* __restrict__ x,
+                                                         const T* __restrict__ dy, int c_out,
+                                                         const long long* __restrict__ ptr,
+                                                         const int* __restrict__ ws_in,
+                                                         const int* __restrict__ ws_out, int chunk,
+                                                         float* __restrict__ dw) {
+    const int k = blockIdx.z;
+    const long long b = ptr[k], e = ptr[k + 1];
+    const long long p0 = b + (long long)blockIdx.x * chunk;
+    const long long p1 = p0 + chunk < e ? p0 + chunk : e;
+    if (p0 >= p1) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int co = blockIdx.y * 32 + lane;
+    const bool live = co < c_out;
+    float acc[CI];
+#pragma unroll
+    for (int c = 0; c < CI; ++c) acc[c] = 0.f;
+    long long p = p0 + warp;
+    for (; p + 24 < p1; p += 32) {  // four pairs per trip: loads in flight together
+        int ii[4], oo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            ii[u] = __ldg(ws_in + p + 8 * u);
+            oo[u] = __ldg(ws_out + p + 8 * u);
+        }
+        float g[4], xv[4][CI];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            g[u] = live ? to_f(dy[(size_t)oo[u] * c_out + co]) : 0.f;
+#pragma unroll
+            for (int c = 0; c < CI; ++c) xv[u][c] = to_f(x[(size_t)ii[u] * CI + c]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < CI; ++c) acc[c] = fmaf(xv[u][c], g[u], acc[c]);
+    }
+    for (; p < p1; p += 8) {
+        const int i = __ldg(ws_in + p), o = __ldg(ws_out + p);
+        const float g = live ? to_f(dy[(size_t)o * c_out + co]) : 0.f;
+#pragma unroll
+        for (int c = 0; c < CI; ++c) acc[c] = fmaf(to_f(x[(size_t)i * CI + c]), g, acc[c]);
+    }
+    __shared__ float red[8][CI][32];
+#pragma unroll
+    for (int c = 0; c < CI; ++c) red[warp][c][lane] = acc[c];
+    __syncthreads();
+    if (warp < CI && live) {  // warp c flushes input channel c
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sum += red[w][warp][lane];
+        atomicAdd(dw + ((size_t)k * CI + warp) * c_out + co, sum);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
                                                     const T* __restrict__ dy, int c_in, int c_out,
@@ -2127,6 +2190,37 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
         auto kern = dt == SK_F16 ? k_wgrad_tc<__half> : k_wgrad_tc<__nv_bfloat16>;
         ensure_smem(reinterpret_cast<const void*>(kern), smem);
         kern<<<ctx->num_sms, kWgThreads, smem, st>>>(a, stages);
+        SK_LAUNCH_CHECK();
+        return;
+    }
+    if (dt != SK_F32 && !ctx->deterministic && c_in <= 8 && !m->graph) {
+        // tiny C_in (the stem): lane-per-output-channel kernel; conv maps hold
+        // at most n_out pairs per offset
+        const int chunk = 1024;
+        const dim3 grid((unsigned)ceil_div(std::max(m->n_out, 1), chunk),
+                        (unsigned)ceil_div(c_out, 32), (unsigned)m->kd);
+        const long long* ptr = m->ws_ptr.as<long long>();
+        auto launch = [&](auto tag, auto ci) {
+            using T = decltype(tag);
+            constexpr int CI = decltype(ci)::value;
+            k_wgrad_small_cin<T, CI><<<grid, 256, 0, st>>>(
+                static_cast<const T*>(x), static_cast<const T*>(dy), c_out, ptr,
+                m->ws_in.as<int>(), m->ws_out.as<int>(), chunk, dw);
+        };
+        auto by_ci = [&](auto tag) {
+            switch (c_in) {
+                case 1: launch(tag, std::integral_constant<int, 1>{}); break;
+                case 2: launch(tag, std::integral_constant<int, 2>{}); break;
+                case 3: launch(tag, std::integral_constant<int, 3>{}); break;
+                case 4: launch(tag, std::integral_constant<int, 4>{}); break;
+                case 5: launch(tag, std::integral_constant<int, 5>{}); break;
+                case 6: launch(tag, std::integral_constant<int, 6>{}); break;
+                case 7: launch(tag, std::integral_constant<int, 7>{}); break;
+                default: launch(tag, std::integral_constant<int, 8>{}); break;
+            }
+        };
+        if (dt == SK_F16) by_ci(__half{});
+        else by_ci(__nv_bfloat16{});
         SK_LAUNCH_CHECK();
         return;
     }

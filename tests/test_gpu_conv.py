@@ -74,7 +74,7 @@ def test_forward_all_dataflows(env, restatement, dtype, cin, cout):
 
 @pytest.mark.parametrize("dtype", ["float16", "float32"])
 @pytest.mark.parametrize("cin,cout", [(32, 64), (64, 64), (128, 96), (4, 16), (256, 128),
-                                      (96, 256), (16, 8)])
+                                      (96, 256), (16, 8), (4, 32), (3, 48), (1, 32), (8, 40)])
 @pytest.mark.parametrize("stride", [1, 2])
 def test_dgrad_wgrad(env, restatement, dtype, cin, cout, stride):
     torch, sk = env
