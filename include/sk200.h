@@ -256,6 +256,13 @@ sk_status sk_net_forward_profiled(sk_net* net, sk_coords* in, const void* d_feat
 sk_status sk_net_measure(sk_net* net, sk_coords* in, const void* d_feats, int channels,
                          int forward, int dgrad, int wgrad, void* stream, double* ms);
 int64_t sk_net_map_builds(const sk_net* net);
+/* Overlapped map build (default on): a forward on a new coordinate set builds
+ * each layer's maps on a runner-owned stream from a helper host thread while
+ * the convs run on the caller's stream (kernel-map readback syncs stall only
+ * the helper). Turn off when several runners are already in flight on one GPU
+ * (they fill each other's sync bubbles). No reference counterpart (sk200
+ * runtime). */
+sk_status sk_net_set_overlap(sk_net* net, int on);
 /* modeled_group_traffic (network.cpp:453-471) */
 sk_status sk_net_group_traffic(sk_net* net, int group, const sk_dataflow_cfg* cfg, void* stream,
                                double* bytes);

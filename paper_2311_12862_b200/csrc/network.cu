@@ -19,8 +19,11 @@
 //    with a CUDA-event RunnerProbe (warmup 2, median of 5, tuner.cpp:50-60);
 //    ties break on the traffic model (cost.cpp:47-93) then space order.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <exception>
 #include <functional>
+#include <thread>
 #include <sstream>
 #include <unordered_map>
 
@@ -258,8 +261,17 @@ struct sk_net {
     size_t wgrad_total = 0;
     std::vector<DevBuf> gout;  // fp32 output grads (backward)
     int64_t map_builds = 0;
+    bool overlap = true;                      // overlapped map builds (sk_net_set_overlap)
+    cudaStream_t map_stream = nullptr;        // overlapped map builds (run_forward)
+    cudaStream_t cmp_stream = nullptr;        // overlapped forward's convs for legacy-stream callers
+    std::vector<cudaEvent_t> map_ready;       // per layer: its maps are built on map_stream
 
-    ~sk_net() { clear_state(); }
+    ~sk_net() {
+        clear_state();
+        for (auto e : map_ready) cudaEventDestroy(e);
+        if (map_stream) cudaStreamDestroy(map_stream);
+        if (cmp_stream) cudaStreamDestroy(cmp_stream);
+    }
     void clear_state() {
         for (auto* c : in_set) if (c) sk_coords_release(c);
         for (auto* c : out_set) if (c) sk_coords_release(c);
@@ -310,46 +322,77 @@ struct Timer {
     }
 };
 
-// Per-layer maps for the network input `root`; reuses the sk_coords caches
-// (one build per (coordinate set, K, stride, orientation) = per group).
-void ensure_maps(sk_net* n, sk_coords* root, cudaStream_t st, std::vector<double>* map_ms) {
-    if (n->root_id == root->id && !n->exec_map.empty()) return;
+// Maps of layer i for the network input `root` (layers before i done);
+// reuses the sk_coords caches (one build per (coordinate set, K, stride,
+// orientation) = per group).
+void build_layer_maps(sk_net* n, sk_coords* root, size_t i, cudaStream_t st) {
+    const LayerSpec& l = n->spec.layers[i];
+    sk_coords* in = l.inputs.empty() ? root : n->out_set[n->spec.index(l.inputs[0])];
+    sk_coords_retain(in);
+    n->in_set[i] = in;
+    int32_t s3[3] = {l.stride, l.stride, n->spec.dims == 3 ? l.stride : 1};
+    if (l.kind == 0) {
+        sk_coords* out = nullptr;
+        sk_status rc0 = sk_out_coords(n->ctx, in, s3, st, &out);
+        if (rc0) fail(rc0, sk_last_error());
+        n->out_set[i] = out;
+        sk_kmap* m = nullptr;
+        sk_status rc = sk_kmap_build(n->ctx, in, out, l.kernel, s3, 0, st, &m);
+        if (rc) fail(rc, sk_last_error());
+        n->exec_map[i] = m;
+    } else {
+        const int j = n->spec.index(l.transpose_of);
+        sk_coords* out = n->in_set[j];
+        sk_coords_retain(out);
+        n->out_set[i] = out;
+        sk_kmap* t2 = nullptr;
+        sk_status rc = sk_kmap_transpose(n->ctx, n->exec_map[j], st, &t2);
+        if (rc) fail(rc, sk_last_error());
+        n->exec_map[i] = t2;
+    }
+}
+
+void reset_maps(sk_net* n) {
     n->clear_state();
     const size_t L = n->spec.layers.size();
     n->in_set.assign(L, nullptr);
     n->out_set.assign(L, nullptr);
     n->exec_map.assign(L, nullptr);
-    for (size_t i = 0; i < L; ++i) {
-        const LayerSpec& l = n->spec.layers[i];
+}
+
+void ensure_maps(sk_net* n, sk_coords* root, cudaStream_t st, std::vector<double>* map_ms) {
+    if (n->root_id == root->id && !n->exec_map.empty()) return;
+    reset_maps(n);
+    for (size_t i = 0; i < n->spec.layers.size(); ++i) {
         std::unique_ptr<Timer> t;
         if (map_ms) t = std::make_unique<Timer>(st);
-        sk_coords* in = l.inputs.empty() ? root : n->out_set[n->spec.index(l.inputs[0])];
-        sk_coords_retain(in);
-        n->in_set[i] = in;
-        int32_t s3[3] = {l.stride, l.stride, n->spec.dims == 3 ? l.stride : 1};
-        if (l.kind == 0) {
-            sk_coords* out = nullptr;
-            sk_status rc0 = sk_out_coords(n->ctx, in, s3, st, &out);
-            if (rc0) fail(rc0, sk_last_error());
-            n->out_set[i] = out;
-            sk_kmap* m = nullptr;
-            sk_status rc = sk_kmap_build(n->ctx, in, out, l.kernel, s3, 0, st, &m);
-            if (rc) fail(rc, sk_last_error());
-            n->exec_map[i] = m;
-        } else {
-            const int j = n->spec.index(l.transpose_of);
-            sk_coords* out = n->in_set[j];
-            sk_coords_retain(out);
-            n->out_set[i] = out;
-            sk_kmap* t2 = nullptr;
-            sk_status rc = sk_kmap_transpose(n->ctx, n->exec_map[j], st, &t2);
-            if (rc) fail(rc, sk_last_error());
-            n->exec_map[i] = t2;
-        }
+        build_layer_maps(n, root, i, st);
         if (map_ms) (*map_ms)[n->group_of[i]] += t->stop();
     }
     n->root_id = root->id;
     ++n->map_builds;
+}
+
+// xsum[c] (the summed input of two-input layer c) sized from its first input's set
+void ensure_xsum(sk_net* n, int c, cudaStream_t st) {
+    const LayerSpec& l = n->spec.layers[c];
+    const sk_coords* src = n->out_set[n->spec.index(l.inputs[0])];
+    const size_t xb = (size_t)std::max(src->n, 1) * l.c_in * n->es();
+    if (n->xsum[c].bytes != xb) n->xsum[c].alloc(xb, st);
+}
+
+// output buffer of layer i (or its alias into the fused consumer's xsum)
+void alloc_layer_output(sk_net* n, size_t i, cudaStream_t st) {
+    const LayerSpec& l = n->spec.layers[i];
+    if (l.inputs.size() == 2 && !n->fused_input[i]) ensure_xsum(n, (int)i, st);
+    if (n->fuse_into[i] >= 0) {
+        ensure_xsum(n, n->fuse_into[i], st);
+        n->out_ptr[i] = n->xsum[n->fuse_into[i]].p;
+        return;
+    }
+    const size_t bytes = (size_t)std::max(n->out_set[i]->n, 1) * l.c_out * n->es();
+    if (n->out[i].bytes != bytes) n->out[i].alloc(bytes, st);
+    n->out_ptr[i] = n->out[i].p;
 }
 
 void alloc_outputs(sk_net* n, cudaStream_t st) {
@@ -429,19 +472,15 @@ struct LayerEvents {
     }
 };
 
-void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cudaStream_t st,
-                 std::vector<double>* map_ms, std::vector<double>* ker_ms,
-                 std::vector<double>* layer_ms = nullptr) {
-    validate(channels == n->spec.layers[0].c_in || !n->spec.layers[0].inputs.empty(),
-             "network input channel count does not match the first layer");
-    ensure_maps(n, root, st, map_ms);
-    alloc_outputs(n, st);
-    refresh_wt(n, st);
+void run_layers(sk_net* n, const void* feats, int channels, cudaStream_t st,
+                std::vector<double>* ker_ms, std::vector<double>* layer_ms,
+                const std::function<void(size_t)>& before) {
     const size_t L = n->spec.layers.size();
     std::unique_ptr<LayerEvents> evs;
     if (ker_ms || layer_ms) evs = std::make_unique<LayerEvents>(L);
     for (size_t i = 0; i < L; ++i) {
         const LayerSpec& l = n->spec.layers[i];
+        if (before) before(i);
         if (evs) SK_CUDA(cudaEventRecord(evs->ev[2 * i], st));
         const void* x;
         if (l.inputs.empty()) {
@@ -478,6 +517,108 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
             if (layer_ms) (*layer_ms)[i] = v;
         }
     }
+}
+
+bool overlap_maps() {
+    static const bool v = [] {
+        const char* e = getenv("SK_NET_OVERLAP");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
+}
+
+void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cudaStream_t st,
+                 std::vector<double>* map_ms, std::vector<double>* ker_ms,
+                 std::vector<double>* layer_ms = nullptr) {
+    validate(channels == n->spec.layers[0].c_in || !n->spec.layers[0].inputs.empty(),
+             "network input channel count does not match the first layer");
+    const size_t L = n->spec.layers.size();
+    const bool cached = n->root_id == root->id && !n->exec_map.empty();
+    if (cached || map_ms || !overlap_maps() || !n->overlap) {
+        ensure_maps(n, root, st, map_ms);
+        alloc_outputs(n, st);
+        refresh_wt(n, st);
+        run_layers(n, feats, channels, st, ker_ms, layer_ms, nullptr);
+        return;
+    }
+    // Overlapped map build: a host thread builds layer i's maps (down-sampled
+    // sets with their count readbacks, queries, transposes, the prepared map
+    // or pair lists the layer's dataflow reads) on the runner's map stream
+    // and records map_ready[i]; this thread enqueues layer i's conv on st
+    // behind that event. The readback syncs then stall only the builder, and
+    // the device runs level l's convs while level l+1's maps are built.
+    reset_maps(n);
+    if (!n->map_stream) SK_CUDA(cudaStreamCreateWithFlags(&n->map_stream, cudaStreamNonBlocking));
+    // a caller on the legacy default stream gets the convs on a runner-owned
+    // stream (measured: the overlap bought nothing with the convs on the
+    // legacy stream), bracketed by events so the caller's order is unchanged
+    const cudaStream_t caller = st;
+    const bool legacy = st == nullptr || st == cudaStreamLegacy;
+    if (legacy) {
+        if (!n->cmp_stream) SK_CUDA(cudaStreamCreateWithFlags(&n->cmp_stream, cudaStreamNonBlocking));
+        st = n->cmp_stream;
+    }
+    while (n->map_ready.size() < L + 2) {
+        cudaEvent_t e;
+        SK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        n->map_ready.push_back(e);
+    }
+    cudaStream_t ms = n->map_stream;
+    SK_CUDA(cudaEventRecord(n->map_ready[L], caller));  // the caller's prior work (root, feats)
+    SK_CUDA(cudaStreamWaitEvent(ms, n->map_ready[L], 0));
+    if (legacy) SK_CUDA(cudaStreamWaitEvent(st, n->map_ready[L], 0));
+    // layer i's maps are ready once done > i; this thread spins (yielding) on
+    // it: a condition-variable wake per layer added tens of microseconds
+    std::atomic<size_t> done{0};
+    std::atomic<bool> failed{false};
+    std::exception_ptr err;
+    const int dev = n->ctx->device;
+    std::thread builder([&] {
+        try {
+            SK_CUDA(cudaSetDevice(dev));
+            for (size_t i = 0; i < L; ++i) {
+                build_layer_maps(n, root, i, ms);
+                const LayerSpec& l = n->spec.layers[i];
+                conv_forward_prepare(n->ctx, n->exec_map[i], layer_cfg(n, 0, (int)i), n->dt,
+                                     l.c_in, l.c_out, ms);
+                SK_CUDA(cudaEventRecord(n->map_ready[i], ms));
+                done.store(i + 1, std::memory_order_release);
+            }
+        } catch (...) {
+            err = std::current_exception();
+            failed.store(true, std::memory_order_release);
+        }
+    });
+    struct Join {
+        std::thread& t;
+        ~Join() {
+            if (t.joinable()) t.join();
+        }
+    } join{builder};
+    refresh_wt(n, st);
+    n->out.resize(L);
+    n->xsum.resize(L);
+    n->x_ptr.assign(L, nullptr);
+    n->out_ptr.assign(L, nullptr);
+    run_layers(n, feats, channels, st, ker_ms, layer_ms, [&](size_t i) {
+        while (done.load(std::memory_order_acquire) <= i) {
+            if (failed.load(std::memory_order_acquire)) {
+                builder.join();
+                std::rethrow_exception(err);
+            }
+            std::this_thread::yield();
+        }
+        SK_CUDA(cudaStreamWaitEvent(st, n->map_ready[i], 0));
+        alloc_layer_output(n, i, st);
+    });
+    builder.join();
+    if (err) std::rethrow_exception(err);
+    if (legacy) {  // the caller's stream continues after the convs
+        SK_CUDA(cudaEventRecord(n->map_ready[L + 1], st));
+        SK_CUDA(cudaStreamWaitEvent(caller, n->map_ready[L + 1], 0));
+    }
+    n->root_id = root->id;
+    ++n->map_builds;
 }
 
 // measure_ms (network.cpp:398-438): forward always runs; dgrad / wgrad sweeps
@@ -781,6 +922,13 @@ sk_status sk_net_measure(sk_net* n, sk_coords* in, const void* d_feats, int chan
 }
 
 int64_t sk_net_map_builds(const sk_net* n) { return n ? n->map_builds : -1; }
+
+sk_status sk_net_set_overlap(sk_net* n, int on) {
+    return nguard([&] {
+        sk::validate(n != nullptr, "null network");
+        n->overlap = on != 0;
+    });
+}
 
 sk_status sk_net_group_traffic(sk_net* n, int group, const sk_dataflow_cfg* cfg, void* stream,
                                double* bytes) {

@@ -129,6 +129,11 @@ int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st);
 // conv.cu
 // w_kmajor (optional, forward only): W already transposed to [kd][c_out][c_in]
 // residual (optional): y = conv(x) + residual, same shape as y (fused skip add)
+// Builds, on st, the prepared OS map or the WS pair lists a forward
+// conv_forward(m, cfg, dt, c_in, c_out) will read (nothing for the paths that
+// read the raw map): lets the network runner build them ahead on its map stream.
+void conv_forward_prepare(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt,
+                          int c_in, int c_out, cudaStream_t st);
 void conv_forward(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
                   const void* w_kmajor = nullptr, const void* residual = nullptr,

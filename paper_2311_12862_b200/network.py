@@ -180,6 +180,10 @@ class NetworkRunner:
                                    int(forward), int(dgrad), int(wgrad), _stream(), C.byref(ms)))
         return ms.value
 
+    def set_overlap(self, on: bool) -> None:
+        """Overlapped map build (sk_net_set_overlap; default on)."""
+        check(lib().sk_net_set_overlap(self.ptr, int(bool(on))))
+
     def map_build_count(self) -> int:
         return lib().sk_net_map_builds(self.ptr)
 

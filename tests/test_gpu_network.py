@@ -210,7 +210,9 @@ def test_tune_result_and_tspw_weights_roundtrip(env, tmp_path):
     y1, _ = net.forward(cs, x)
     y2, _ = net2.forward(cs, x)
     torch.cuda.synchronize()
-    assert torch.equal(y1, y2)
+    # tuned split-K dataflows flush partials with fp32 atomics (order-dependent
+    # last bits), so the two runners agree to fp16 rounding, not bitwise
+    assert torch.allclose(y1.float(), y2.float(), rtol=2e-3, atol=2e-3)
 
 
 def test_scan_pipeline_matches_serial_forward(env):
@@ -245,3 +247,31 @@ def test_scan_pipeline_matches_serial_forward(env):
         assert pipe.d2h_bytes == sum(w.nbytes for w in want)
     with pytest.raises(sk.ValidationError):
         ScanPipeline(net, 10, 4).run(scans[:1])
+
+
+def test_overlapped_map_build_matches_serial(env):
+    """The overlapped map build (helper thread + map stream, sk_net_set_overlap)
+    returns exactly the serial build's outputs, scan after scan, and its maps
+    serve the chained backward (SGD on the same runner)."""
+    torch, sk, N, M = env
+    net = N.NetworkRunner(M.minkunet18(), dtype=torch.float16, weight_seed=4)
+    net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large()))  # no red.add: bitwise
+    rng = np.random.default_rng(3)
+    for s, n_pts in enumerate([20000, 9000, 20000]):
+        c = scan(n_pts, seed=40 + s)
+        f = torch.from_numpy(rng.standard_normal((len(c), 4)).astype(np.float16)).cuda()
+        builds = net.map_build_count()
+        net.set_overlap(True)
+        y_on, _ = net.forward(sk.CoordSet.create(c), f)
+        assert net.map_build_count() == builds + 1
+        g_on = torch.zeros(net.num_params, device="cuda")
+        net.backward(torch.ones_like(y_on), g_on)
+        net.set_overlap(False)
+        y_off, _ = net.forward(sk.CoordSet.create(c), f)
+        g_off = torch.zeros(net.num_params, device="cuda")
+        net.backward(torch.ones_like(y_off), g_off)
+        torch.cuda.synchronize()
+        assert torch.equal(y_on, y_off), s
+        # wgrad flushes with fp32 atomics (order-dependent): compare to the scale
+        err = float((g_on - g_off).abs().max() / g_off.abs().max().clamp_min(1.0))
+        assert err <= 1e-4, (s, err)
