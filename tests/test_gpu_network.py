@@ -275,3 +275,26 @@ def test_overlapped_map_build_matches_serial(env):
         # wgrad flushes with fp32 atomics (order-dependent): compare to the scale
         err = float((g_on - g_off).abs().max() / g_off.abs().max().clamp_min(1.0))
         assert err <= 1e-4, (s, err)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_forward_error_inside_map_build_propagates(env, overlap):
+    """A map-build failure (here an unsupported kernel volume, K=7 -> 343
+    offsets, at the third layer) surfaces from forward as the reference's
+    ValidationError with both the overlapped (helper thread) and the serial
+    map build, and the runner keeps working on a valid network afterwards."""
+    torch, sk, N, M = env
+    from paper_2311_12862_b200.models import Layer
+    layers = M.toy_unet()
+    bad = [Layer(l.name, l.kind, l.c_in, l.c_out, 7 if l.name == "mid" else l.kernel, l.stride,
+                 list(l.inputs), l.transpose_of) for l in layers]
+    c = scan(3000, seed=21)
+    x = torch.randn(len(c), 1, device="cuda").half()
+    net = N.NetworkRunner(bad, dtype=torch.float16, weight_seed=1)
+    net.set_overlap(overlap)
+    with pytest.raises(sk.ValidationError):
+        net.forward(sk.CoordSet.create(c), x)
+    good = N.NetworkRunner(layers, dtype=torch.float16, weight_seed=1)
+    good.set_overlap(overlap)
+    y, _ = good.forward(sk.CoordSet.create(c), x)
+    assert y.shape == (len(c), 2) and bool(torch.isfinite(y.float()).all())

@@ -45,6 +45,9 @@ def main():
     dev_f = [torch.from_numpy(f).cuda() for f in feats]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     nets = replicate(net, max(a.workers))
+    if os.environ.get("OVERLAP") == "1":
+        for r in nets:
+            r.set_overlap(True)
     streams = [torch.cuda.Stream() for _ in range(max(a.workers))]
     if os.environ.get("GC_FREEZE"):
         import gc
