@@ -1968,6 +1968,14 @@ void conv_forward_prepare(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, s
     else kmap_ensure_ws(m, st);
 }
 
+bool dense_gemm_enabled() {  // SK_DENSE_CUBLAS=0: identity layers stay on k_gconv_tc
+    static const bool v = [] {
+        const char* e = getenv("SK_DENSE_CUBLAS");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
+}
+
 // Forward (dgrad = false) or dgrad (dgrad = true; m_fwd is the FORWARD map).
 void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
@@ -2041,6 +2049,9 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     pick_n_tiling(n_total, cfg.tile.cta_n, tc, a.bn, a.n_ntiles);
     const bool det = ctx->deterministic;
 
+    if (m->identity && tc && !det && !residual && k_eff == k_total && dense_gemm_enabled() &&
+        dense_identity_gemm(dt, m->n_out, c_in, c_out, x, w, y, y_accum, dgrad, st))
+        return;  // plain dense GEMM -> cuBLAS (dense.cu)
     if (m->identity && tc && !det) {
         // K=1 stride-1 layer on one coordinate set: y = x W_0 for every
         // dataflow (the map is the identity), so run it as a dense GEMM

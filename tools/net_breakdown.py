@@ -1,4 +1,8 @@
-"""Per-group / per-layer time breakdown of the MinkUNet bench workload."""
+"""Per-group time breakdown of the MinkUNet bench workload: algorithmic FLOPs,
+kernel ms (CUDA events per layer), TFLOP/s and the fraction of the measured
+bf16 peak, map-build ms. TUNE=1 (default) tunes per group like bench.py.
+
+  python tools/net_breakdown.py [--out profiles/r01_group_roofline.md]"""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -14,6 +18,11 @@ c = torch.from_numpy(scan).cuda()
 f = torch.randn(len(scan), 4, device="cuda").half()
 net = NetworkRunner(minkunet18(), dtype=torch.float16)
 net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, splits, sk.tile_large()))
+if os.environ.get("TUNE", "1") == "1":
+    tc = torch.from_numpy(lidar_scan(200_000, seed=900_000)).cuda()
+    net.tune(sk.CoordSet.create(tc), torch.randn(len(tc), 4, device="cuda").half(), training=0,
+             warmup=1, runs=3)
+peak = bench.peaks().get("bf16_tflops", 1652.8)
 cs = sk.CoordSet.create(c)
 for _ in range(3):
     net.forward(cs, f)
@@ -21,11 +30,25 @@ _, st = net.forward(cs, f, stats=True)
 pairs = bench.layer_pairs(sk, net, cs)
 groups = net.groups()
 tot = 0
+lines = ["# MinkUNet-18 per map group: algorithmic FLOPs vs kernel time (one B200)", "",
+         f"tools/net_breakdown.py; lidar scan {len(scan)} voxels, fp16 in / fp32 acc, tuned per "
+         f"group; kernel ms from CUDA events per layer (warm maps); peak = {peak} TFLOP/s "
+         "(MEASURED_PEAKS bf16). FLOPs = 2*pairs*C_in*C_out (padding not credited).", "",
+         "| group | layers | K | s | first layer | (C_in, C_out) | pairs (first layer) | GFLOP | "
+         "dataflow | kernel ms | TFLOP/s | frac | map ms |", "|" + "---|" * 13]
 for g, ls in enumerate(groups):
     fl = sum(2.0 * pairs[i] * net.layers[i].c_in * net.layers[i].c_out for i in ls)
     k = st["kernel_ms"][g]
     tot += k
     L = net.layers[ls[0]]
-    print(f"g{g:2d} n_layers={len(ls):2d} K={L.kernel} s={L.stride} {L.name:8s} ch={sorted(set((net.layers[i].c_in, net.layers[i].c_out) for i in ls))} "
-          f"pairs={pairs[ls[0]]:8d} GFLOP={fl/1e9:7.2f} kernel_ms={k:6.3f} TF/s={fl/k/1e9:6.1f} map_ms={st['mapping_ms'][g]:.3f}")
-print("kernel total ms", tot, "map total", st["mapping_ms"].sum())
+    chans = sorted(set((net.layers[i].c_in, net.layers[i].c_out) for i in ls))
+    lines.append(f"| {g} | {len(ls)} | {L.kernel} | {L.stride} | {L.name} | {chans} | {pairs[ls[0]]} | "
+                 f"{fl / 1e9:.2f} | {net.config(g).name()} | {k:.3f} | {fl / k / 1e9:.1f} | "
+                 f"{fl / k / 1e9 / peak:.3f} | {st['mapping_ms'][g]:.3f} |")
+allfl = sum(2.0 * pairs[i] * l.c_in * l.c_out for i, l in enumerate(net.layers))
+lines += ["", f"kernels {tot:.3f} ms, {allfl / tot / 1e9:.1f} TFLOP/s over the network "
+          f"({allfl / tot / 1e9 / peak:.3f} of peak); map build {st['mapping_ms'].sum():.3f} ms"]
+txt = "\n".join(lines) + "\n"
+print(txt)
+if "--out" in sys.argv:
+    open(sys.argv[sys.argv.index("--out") + 1], "w").write(txt)
