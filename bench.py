@@ -13,7 +13,7 @@ Prints ONE JSON line (rank 0). Under torchrun each rank runs its own scans
 region is bracketed by barrier + synchronize and the max over ranks is taken.
 
   value       scans/s over all ranks, inputs already in HBM, --concurrency
-              (default 4) scans in flight per GPU; config.latency_ms_per_scan
+              (default 6) scans in flight per GPU; config.latency_ms_per_scan
               is the one-scan-at-a-time latency
   e2e         scans/s through the public API (pipeline.ScanPipeline) from
               pinned HOST coords+feats to the output features in pinned host
@@ -172,7 +172,7 @@ def main():
                     help="infer: configs[1] MinkUNet inference (default); second: configs[2] "
                          "SECOND encoder inference; train: configs[3] mixed-precision DP "
                          "training step, global batch 8 scans")
-    ap.add_argument("--concurrency", type=int, default=4,
+    ap.add_argument("--concurrency", type=int, default=6,
                     help="scans in flight (host threads x CUDA streams x NetworkRunners); "
                          "1 = one scan at a time")
     ap.add_argument("--no-tune", action="store_true",
@@ -219,9 +219,12 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
 
+    yout = torch.empty(max(len(c) for c in scans), net.layer_shapes[-1][2], dtype=torch.float16,
+                       device="cuda")
+
     def step(i):
         cs = sk.CoordSet.create(dev_coords[i])
-        y, _ = net.forward(cs, dev_feats[i])
+        y, _ = net.forward(cs, dev_feats[i], out=yout)
         return y
 
     def timed(fn, idxs):
@@ -238,7 +241,7 @@ def main():
 
     # per-scan latency: one scan at a time, CUDA events around each scan, L2
     # flushed outside the events
-    for i in range(args.warmup):
+    for i in range(n_scans):  # every scan once: all buffer size classes seen
         step(i)
     torch.cuda.synchronize()
     lat_ms = timed(step, range(args.warmup, n_scans)) / args.steps
@@ -462,7 +465,10 @@ def run_train(args, rank, world, local):
         scenes = [(sk.CoordSet.create(c), x, t) for c, x, t in prepared[i]]
         return tr.train_step(scenes, B)
 
-    for i in range(args.warmup):
+    # warm pass over every batch: the torch allocator (loss temporaries, per
+    # replica stream) and the block cache see every size class before the
+    # timed steps (a cudaMalloc mid-window stalls the whole device)
+    for i in range(args.warmup + args.steps):
         step(i)
     torch.cuda.synchronize()
     if world > 1:

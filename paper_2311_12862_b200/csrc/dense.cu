@@ -11,33 +11,30 @@
 namespace sk {
 
 namespace {
-// Process-wide pool of cuBLAS handles, created once and never destroyed: a
-// handle serves one host thread at a time, and creating one per (short-lived)
-// worker thread cost a cudaMalloc of its workspace, which stalls the device.
-struct HandlePool {
+// One cuBLAS handle per CUDA stream, created on first use, bound to that
+// stream once and never destroyed. Re-binding a handle to another stream
+// resets its workspace (cuBLAS then re-allocates it: a device-wide stall each
+// time the runners' streams alternate), and a handle is not safe for
+// concurrent host threads, hence the per-handle mutex around the (short) call.
+struct StreamHandle {
     std::mutex mu;
-    std::vector<cublasHandle_t> free;
-};
-HandlePool& pool() {
-    static HandlePool* p = new HandlePool();
-    return *p;
-}
-cublasHandle_t acquire() {
-    {
-        std::lock_guard<std::mutex> g(pool().mu);
-        if (!pool().free.empty()) {
-            cublasHandle_t h = pool().free.back();
-            pool().free.pop_back();
-            return h;
-        }
-    }
     cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    return h;
-}
-void release(cublasHandle_t h) {
-    std::lock_guard<std::mutex> g(pool().mu);
-    pool().free.push_back(h);
+};
+StreamHandle* handle_for(cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, StreamHandle*>* table = new std::map<cudaStream_t, StreamHandle*>();
+    std::lock_guard<std::mutex> g(mu);
+    StreamHandle*& e = (*table)[st];
+    if (!e) {
+        auto* n = new StreamHandle();
+        if (cublasCreate(&n->h) != CUBLAS_STATUS_SUCCESS ||
+            cublasSetStream(n->h, st) != CUBLAS_STATUS_SUCCESS) {
+            delete n;
+            return nullptr;
+        }
+        e = n;
+    }
+    return e;
 }
 }  // namespace
 
@@ -48,13 +45,10 @@ bool dense_identity_gemm(sk_dtype dt, long long rows, int c_in, int c_out, const
                          const void* w, void* y, float* y_accum, bool dgrad, cudaStream_t st) {
     if (dt != SK_F16 && dt != SK_BF16) return false;
     if (rows <= 0 || rows > INT32_MAX) return false;
-    cublasHandle_t h = acquire();
-    if (!h) return false;
-    struct Back {
-        cublasHandle_t h;
-        ~Back() { release(h); }
-    } back{h};
-    if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return false;
+    StreamHandle* sh = handle_for(st);
+    if (!sh) return false;
+    std::lock_guard<std::mutex> g(sh->mu);
+    cublasHandle_t h = sh->h;
     const cudaDataType_t ab = dt == SK_F16 ? CUDA_R_16F : CUDA_R_16BF;
     const int m = dgrad ? c_in : c_out;   // rows of the col-major result
     const int k = dgrad ? c_out : c_in;
