@@ -547,7 +547,6 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     // and records map_ready[i]; this thread enqueues layer i's conv on st
     // behind that event. The readback syncs then stall only the builder, and
     // the device runs level l's convs while level l+1's maps are built.
-    reset_maps(n);
     if (!n->map_stream) SK_CUDA(cudaStreamCreateWithFlags(&n->map_stream, cudaStreamNonBlocking));
     // a caller on the legacy default stream gets the convs on a runner-owned
     // stream (measured: the overlap bought nothing with the convs on the
@@ -567,6 +566,10 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     SK_CUDA(cudaEventRecord(n->map_ready[L], caller));  // the caller's prior work (root, feats)
     SK_CUDA(cudaStreamWaitEvent(ms, n->map_ready[L], 0));
     if (legacy) SK_CUDA(cudaStreamWaitEvent(st, n->map_ready[L], 0));
+    // release the previous scan's maps only now: their buffers go back to the
+    // map stream's cache / pool behind the wait above, i.e. after every conv
+    // of the previous scan that read them
+    reset_maps(n);
     // layer i's maps are ready once done > i; this thread spins (yielding) on
     // it: a condition-variable wake per layer added tens of microseconds
     std::atomic<size_t> done{0};
