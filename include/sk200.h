@@ -109,6 +109,10 @@ sk_status sk_coords_create(sk_ctx* ctx, int dims, int n, const int32_t* d_coords
 sk_status sk_coords_create_host(sk_ctx* ctx, int dims, int n, const int32_t* h_coords,
                                 const int32_t stride_tag[3], void* stream, sk_coords** out);
 sk_status sk_coords_retain(sk_coords* c);
+/* Release (refcounted). Device buffers return to the stream-ordered pool on
+ * the stream that built them; a set or map also used from OTHER streams must
+ * be released after that work completes (the usual stream-ordered lifetime
+ * rule; readers on other streams are ordered after the build automatically). */
 sk_status sk_coords_release(sk_coords* c);
 int sk_coords_n(const sk_coords* c);
 int sk_coords_dims(const sk_coords* c);
