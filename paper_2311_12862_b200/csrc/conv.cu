@@ -28,7 +28,7 @@
 //              tile (2D TMA). Stages are 128B/64B/32B-swizzled K-major and
 //              complete on one mbarrier (expect_tx). Row indices arrive by
 //              128B cp.async.bulk into a per-warp 16-slot smem ring,
-//              prefetched 12 column steps ahead.
+//              prefetched up to 8 column steps ahead.
 //   warp 4     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
 //              N=BN, K=16 per instruction); tcgen05.commit frees stages
 //   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
@@ -65,7 +65,7 @@ constexpr uint32_t kRowBits = 6, kRowMask = 63;
 constexpr int kTmaWarps = 4;          // warps 0-3: TMA gather4 producers (TMA variant)
 constexpr int kZeroWarps = 2;
 constexpr int kMaxStages = 10;       // launch_tc_kc caps the stage count
-constexpr int kCompactLag = 3;       // index warp compacts slot s-3 after publishing s
+constexpr int kCompactLag = 1;       // index warp compacts slot s-1 after publishing s (3: -1..2% slower)
 constexpr int kIdxRing = 8;           // column steps in flight in the index ring (1 KB each)
 
 struct ConvArgs {
