@@ -1729,7 +1729,11 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStr
     if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
     else memset(&ta, 0, sizeof(ta));
     tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
-    const bool slab3 = !tma && KC == 32 && nchunks == 3;  // C = 96: three-slab path wins
+    static const bool slab3_ok = [] {  // SK_SLAB3=0: C = 96 takes the 2-CTA single-slab path
+        const char* e = getenv("SK_SLAB3");
+        return !e || atoi(e) != 0;
+    }();
+    const bool slab3 = slab3_ok && !tma && KC == 32 && nchunks == 3;  // C = 96: three-slab path wins
     if (!tma && two_cta && bn <= 128 && !slab3) {
         // TMEM per CTA <= 256 columns: double-buffer only up to BN = 64
         const int acc_bufs = 4 * bn <= 256 ? 2 : 1;
@@ -1744,7 +1748,7 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStr
     // C_in = 96 (three 32-channel slabs) is the one width where fusing the
     // chunks pays (measured: C = 64/128 gain nothing, and SLABS stays a
     // compile-time constant so the single-slab kernel keeps its lean loops)
-    const int slabs = (!tma && KC == 32 && nchunks == 3 && ((size_t)bn * KC * 2) % 1024 == 0 &&
+    const int slabs = (slab3 && ((size_t)bn * KC * 2) % 1024 == 0 &&
                        (size_t)min_stages * 3 * slab_bytes <= 200 * 1024) ? 3 : 1;
     const size_t stage_bytes = slabs * slab_bytes;
     int stages = (int)std::min<size_t>(kMaxStages, (200 * 1024) / stage_bytes);
