@@ -265,7 +265,7 @@ sk_status sk_ctx_create(int device, sk_ctx** out) {
             // memory: growing it mid-run blocked the whole device for
             // 10-100 ms per cudaMallocAsync (several runners in flight)
             const char* pg = getenv("SK_POOL_MB");
-            const size_t grow = (size_t)(pg ? atol(pg) : 16384) << 20;
+            const size_t grow = (size_t)(pg ? atol(pg) : 24576) << 20;
             void* p = nullptr;
             if (grow && cudaMallocAsync(&p, grow, nullptr) == cudaSuccess)
                 cudaFreeAsync(p, nullptr);

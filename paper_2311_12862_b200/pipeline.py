@@ -54,12 +54,12 @@ def replicate(net, count: int):
 
 
 class _Worker:
-    def __init__(self, net, max_voxels, c_in, depth):
+    def __init__(self, net, max_voxels, c_in, depth, stream=None):
         self.net = net
         self.depth = depth
         dt = net.dtype
         c_out = net.layer_shapes[-1][2]
-        self.s_cmp = torch.cuda.Stream()
+        self.s_cmp = stream if stream is not None else torch.cuda.Stream()
         self.s_in = torch.cuda.Stream()
         self.s_out = torch.cuda.Stream()
         self.d_c = [torch.empty((max_voxels, 4), dtype=torch.int32, device="cuda")
@@ -133,13 +133,15 @@ class _Worker:
 
 
 class ScanPipeline:
-    def __init__(self, nets, max_voxels: int, c_in: int, depth: int = 2):
+    def __init__(self, nets, max_voxels: int, c_in: int, depth: int = 2, streams=None):
         """nets: one NetworkRunner or a list (one worker thread per runner;
-        see replicate())."""
+        see replicate()). streams: optional compute stream per runner (reusing
+        the streams a runner already ran on reuses its cached device blocks)."""
         if not isinstance(nets, (list, tuple)):
             nets = [nets]
         self.max_voxels = max_voxels
-        self.workers = [_Worker(n, max_voxels, c_in, depth) for n in nets]
+        streams = streams or [None] * len(nets)
+        self.workers = [_Worker(n, max_voxels, c_in, depth, s) for n, s in zip(nets, streams)]
 
     @property
     def d2h_bytes(self) -> int:
