@@ -164,8 +164,9 @@ def test_contract_errors(env):
         sk.conv_forward(m, x, w, sk.DataflowConfig(sk.IMPLICIT_GEMM, 99))
 
 
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
 @pytest.mark.parametrize("cin,cout", [(32, 96), (96, 96), (128, 256), (256, 256), (4, 32)])
-def test_identity_k1_dense_path(env, restatement, cin, cout):
+def test_identity_k1_dense_path(env, restatement, cin, cout, dtype):
     """K=1 stride-1 layers on one coordinate set run as a dense GEMM (the map
     is the identity); every dataflow config must agree with the oracle."""
     torch, sk = env
@@ -175,10 +176,11 @@ def test_identity_k1_dense_path(env, restatement, cin, cout):
     m = sk.build_kmap(c, c, 1, 1)
     ent, _ = m.os()
     assert (ent[:, 0] == np.arange(len(c_np))).all()
-    x = torch.randn(m.n_in, cin).half()
-    w = (torch.randn(1, cin, cout) / np.sqrt(cin)).half()
+    dt = getattr(torch, dtype)
+    x = torch.randn(m.n_in, cin).to(dt)
+    w = (torch.randn(1, cin, cout) / np.sqrt(cin)).to(dt)
     y_ref = restatement.conv(ent, x.double().numpy(), w.double().numpy())
-    dy = torch.randn(m.n_out, cout).half()
+    dy = torch.randn(m.n_out, cout).to(dt)
     dx_ref = restatement.dgrad(restatement.transpose_os(ent, m.n_in), dy.double().numpy(),
                                w.double().numpy())
     for cfg in configs(sk)[:4]:
