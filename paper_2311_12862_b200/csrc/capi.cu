@@ -264,12 +264,19 @@ sk_status sk_ctx_create(int device, sk_ctx** out) {
             // pre-grow the pool once so steady-state scans never map new
             // memory: growing it mid-run blocked the whole device for
             // 10-100 ms per cudaMallocAsync (several runners in flight)
+            // (capped at a third of the free memory, so a shared GPU or a
+            // second process still has room; a failed grow is harmless and
+            // must not leave the runtime's sticky last error set)
             const char* pg = getenv("SK_POOL_MB");
-            const size_t grow = (size_t)(pg ? atol(pg) : 24576) << 20;
+            size_t grow = (size_t)(pg ? atol(pg) : 24576) << 20;
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) grow = std::min(grow, free_b / 3);
+            else (void)cudaGetLastError();
             void* p = nullptr;
-            if (grow && cudaMallocAsync(&p, grow, nullptr) == cudaSuccess)
-                cudaFreeAsync(p, nullptr);
+            if (grow && cudaMallocAsync(&p, grow, nullptr) == cudaSuccess) cudaFreeAsync(p, nullptr);
+            else (void)cudaGetLastError();
             cudaStreamSynchronize(nullptr);
+            (void)cudaGetLastError();
         }
         *out = c;
     });

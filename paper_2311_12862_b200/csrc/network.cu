@@ -20,6 +20,7 @@
 //    ties break on the traffic model (cost.cpp:47-93) then space order.
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -173,6 +174,44 @@ std::vector<std::vector<int>> partition_groups(const NetSpec& net) {
     return groups;
 }
 
+// Runner-owned streams live for the process: objects built on them (cached
+// maps and coordinate sets, block-cache entries) can outlive the runner, and a
+// destroyed handle could be reused by an unrelated stream.
+namespace {
+std::mutex g_stream_mu;
+std::vector<std::pair<int, cudaStream_t>>& stream_pool() {
+    static auto* v = new std::vector<std::pair<int, cudaStream_t>>();
+    return *v;
+}
+}  // namespace
+cudaStream_t acquire_runner_stream(int dev) {
+    {
+        std::lock_guard<std::mutex> g(g_stream_mu);
+        auto& v = stream_pool();
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i].first == dev) {
+                cudaStream_t s = v[i].second;
+                v.erase(v.begin() + (long)i);
+                return s;
+            }
+    }
+    int cur = 0;
+    SK_CUDA(cudaGetDevice(&cur));
+    SK_CUDA(cudaSetDevice(dev));
+    cudaStream_t s = nullptr;
+    SK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SK_CUDA(cudaSetDevice(cur));
+    return s;
+}
+void release_runner_stream(int dev, cudaStream_t s) {
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return;  // leaked, never reused
+    }
+    std::lock_guard<std::mutex> g(g_stream_mu);
+    stream_pool().push_back({dev, s});
+}
+
 namespace {
 
 template <typename T>
@@ -269,8 +308,11 @@ struct sk_net {
     ~sk_net() {
         clear_state();
         for (auto e : map_ready) cudaEventDestroy(e);
-        if (map_stream) cudaStreamDestroy(map_stream);
-        if (cmp_stream) cudaStreamDestroy(cmp_stream);
+        // cached maps / sets built here still name these streams (BuiltOn
+        // marks, block-cache keys): they go back to a process-lifetime pool
+        // instead of being destroyed
+        if (map_stream) sk::release_runner_stream(ctx->device, map_stream);
+        if (cmp_stream) sk::release_runner_stream(ctx->device, cmp_stream);
     }
     void clear_state() {
         for (auto* c : in_set) if (c) sk_coords_release(c);
@@ -352,7 +394,10 @@ void build_layer_maps(sk_net* n, sk_coords* root, size_t i, cudaStream_t st) {
     }
 }
 
+// a failed build leaves partial maps: root_id is cleared here and set only
+// after every layer's maps are built, so a retry never takes them as cached
 void reset_maps(sk_net* n) {
+    n->root_id = 0;
     n->clear_state();
     const size_t L = n->spec.layers.size();
     n->in_set.assign(L, nullptr);
@@ -360,8 +405,13 @@ void reset_maps(sk_net* n) {
     n->exec_map.assign(L, nullptr);
 }
 
+bool maps_complete(const sk_net* n, const sk_coords* root) {
+    return n->root_id != 0 && n->root_id == root->id && !n->exec_map.empty() &&
+           n->exec_map.back() != nullptr;
+}
+
 void ensure_maps(sk_net* n, sk_coords* root, cudaStream_t st, std::vector<double>* map_ms) {
-    if (n->root_id == root->id && !n->exec_map.empty()) return;
+    if (maps_complete(n, root)) return;
     reset_maps(n);
     for (size_t i = 0; i < n->spec.layers.size(); ++i) {
         std::unique_ptr<Timer> t;
@@ -533,7 +583,7 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     validate(channels == n->spec.layers[0].c_in || !n->spec.layers[0].inputs.empty(),
              "network input channel count does not match the first layer");
     const size_t L = n->spec.layers.size();
-    const bool cached = n->root_id == root->id && !n->exec_map.empty();
+    const bool cached = maps_complete(n, root);
     if (cached || map_ms || !overlap_maps() || !n->overlap) {
         ensure_maps(n, root, st, map_ms);
         alloc_outputs(n, st);
@@ -547,14 +597,14 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     // and records map_ready[i]; this thread enqueues layer i's conv on st
     // behind that event. The readback syncs then stall only the builder, and
     // the device runs level l's convs while level l+1's maps are built.
-    if (!n->map_stream) SK_CUDA(cudaStreamCreateWithFlags(&n->map_stream, cudaStreamNonBlocking));
+    if (!n->map_stream) n->map_stream = acquire_runner_stream(n->ctx->device);
     // a caller on the legacy default stream gets the convs on a runner-owned
     // stream (measured: the overlap bought nothing with the convs on the
     // legacy stream), bracketed by events so the caller's order is unchanged
     const cudaStream_t caller = st;
     const bool legacy = st == nullptr || st == cudaStreamLegacy;
     if (legacy) {
-        if (!n->cmp_stream) SK_CUDA(cudaStreamCreateWithFlags(&n->cmp_stream, cudaStreamNonBlocking));
+        if (!n->cmp_stream) n->cmp_stream = acquire_runner_stream(n->ctx->device);
         st = n->cmp_stream;
     }
     while (n->map_ready.size() < L + 2) {
@@ -951,7 +1001,8 @@ sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, 
     return nguard([&] {
         const int L = (int)n->spec.layers.size();
         validate(layer_hi < L && layer_lo >= 0 && layer_lo <= layer_hi, "bad layer range");
-        validate(!n->exec_map.empty(), "backward before forward");
+        validate(n->root_id != 0 && !n->exec_map.empty() && n->exec_map.back() != nullptr,
+                 "backward before a successful forward");
         cudaStream_t st = S(stream);
         if (layer_hi == L - 1) {
             n->gout.resize(L);

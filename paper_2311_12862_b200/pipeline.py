@@ -137,6 +137,10 @@ class ScanPipeline:
         """nets: one NetworkRunner or a list (one worker thread per runner;
         see replicate()). streams: optional compute stream per runner (reusing
         the streams a runner already ran on reuses its cached device blocks)."""
+        if depth < 2:
+            # scan k+1 is staged while scan k's forward is still to be enqueued:
+            # one slot would overwrite scan k's inputs
+            raise _sk.ValidationError("ScanPipeline depth must be >= 2")
         if not isinstance(nets, (list, tuple)):
             nets = [nets]
         self.max_voxels = max_voxels
