@@ -43,14 +43,14 @@ import numpy as np  # noqa: E402
 METRIC = "MinkUNet ms/scan & scans/s (1–8 B200); spconv TFLOP/s, kmap GB/s vs roofline"
 WORKLOAD = ("MinkUNet-18 inference (SURVEY App. B skeleton: 77 convs, 14 map groups) on a "
             "SemanticKITTI-shaped synthetic LiDAR scan (planar_patches n=200k, extent 4, "
-            "5 cm voxels, ~125k voxels), 4 input channels, fp16 in / fp32 accumulate, cold "
+            "5 cm voxels, 124,756 voxels at seed 1: exact gen_cloud restatement), 4 input channels, fp16 in / fp32 accumulate, cold "
             "maps per scan")
 
 
 WORKLOAD_SECOND = ("SECOND/CenterPoint sparse 3D encoder (SURVEY App. A: subm 4->16, 16->16, three "
                    "[s2 conv + 2 subm] stages at 32/64/64, s2 conv 64->128; kernel maps reused "
                    "across each stride level) on a Waymo-shaped synthetic scan (planar_patches "
-                   "n=275k, extent 8, voxel 0.1x0.1x0.15 m, ~150k voxels), fp16 in / fp32 "
+                   "n=275k, extent 8, voxel 0.1x0.1x0.15 m, 149,357 voxels at seed 1), fp16 in / fp32 "
                    "accumulate, cold maps per scan")
 
 
@@ -127,15 +127,27 @@ def cpu_reference_time(coords, feats, threads, max_steps=1, workload="infer"):
     return times
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the compiled reference on the box's host cores."""
+    """--impl reference: the compiled reference on the box's host cores, on
+    the very scans the sk200 arm times (rank 0's seeds warmup+1 ...)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     wl = args.workload if args.workload == "second" else "infer"
-    scans = make_scans(max(1, min(args.steps, 4)), 1000, workload=wl)
-    feats = [np.random.default_rng(i).standard_normal((len(c), 4)).astype(np.float32)
-             for i, c in enumerate(scans)]
+    k = max(1, min(args.steps, 4))
+    scans = make_scans(args.warmup + k, 1, workload=wl)[args.warmup:]
+    feats = bench_feats(scans, args.warmup, 0)
+    feats = [f.astype(np.float32) for f in feats]
     # bounded sample: full cold scans, as many as fit ~120 s (at least 1)
     t_one = cpu_reference_time(scans, feats, threads, 1, wl)[0]
     n = max(1, min(args.steps, int(120.0 / max(t_one, 1e-3))))
@@ -150,14 +162,24 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD_SECOND if wl == "second" else WORKLOAD,
                    "voxels_per_scan": int(np.mean([len(c) for c in scans])),
+                   "scans": f"the sk200 arm's timed scans {args.warmup}..{args.warmup + k - 1} "
+                            "(gen_cloud seeds warmup+1..)",
                    "impl_detail": "compiled reference NetworkRunner::forward, default GGS "
                                   "assignment, f32, cold maps"},
         "cpu_baseline": {"value": value, "unit": "scans/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{len(times)} cold {'SECOND encoder' if wl == 'second' else 'MinkUNet-18'} scans (median)"},
         "e2e": {"value": value, "unit": "scans/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_feats(scans, first_index, rank):
+    """4-channel N(0,1) fp16 features of scan i, seeded by (rank, global scan
+    index) so both arms read identical inputs."""
+    return [np.random.default_rng([rank, first_index + i]).standard_normal((len(c), 4))
+            .astype(np.float16) for i, c in enumerate(scans)]
 
 
 def main():
@@ -200,7 +222,7 @@ def main():
     wl = args.workload
     scans = make_scans(n_scans, 1 + rank * 10000, workload=wl)
     rng = np.random.default_rng(rank)
-    feats = [rng.standard_normal((len(c), 4)).astype(np.float16) for c in scans]
+    feats = bench_feats(scans, 0, rank)
     net = NetworkRunner(model_for(wl), dtype=torch.float16, weight_seed=3)
     net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, args.splits, sk.tile_large()))
     dev_coords = [torch.from_numpy(c).cuda() for c in scans]
@@ -366,9 +388,11 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            t = cpu_reference_time(scans[:1], [f.astype(np.float32) for f in feats[:1]], threads,
-                                   1, wl)
+            t = cpu_reference_time(scans[args.warmup:args.warmup + 1],
+                                   [f.astype(np.float32) for f in feats[args.warmup:args.warmup + 1]],
+                                   threads, 1, wl)
             cpu = {"value": 1.0 / t[0], "unit": "scans/s", "cores": threads, "kind": "reference",
+                   "cpu_model": cpu_model(),
                    "sample": f"1 cold {'SECOND encoder' if wl == 'second' else 'MinkUNet-18'} "
                              "forward on the first timed scan, f32, compiled reference "
                              "NetworkRunner (default GGS assignment)"}
@@ -518,13 +542,8 @@ def kmap_roofline(sk, pk):
     survey's contract with the actual table size (cap x 12 B, charged once for
     the insert and once for the query)."""
     import torch
-    from paper_2311_12862_b200.synth import planar_patches, quantize
-    tiles = []
-    for t in range(10):
-        c = quantize(planar_patches(160_000, 1 + t, 2.0), [0.025] * 3)
-        c[:, 1] += 200 * t
-        tiles.append(c)
-    coords = torch.from_numpy(np.concatenate(tiles)).cuda()
+    from paper_2311_12862_b200.synth import sweep_cloud
+    coords = torch.from_numpy(sweep_cloud(160_000, seed=1, tiles=10)).cuda()
     n = coords.shape[0]
     cap = 64
     while cap < 4 * n:  # load factor <= 1/4 (kmap.cu pow2_cap)
