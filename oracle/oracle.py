@@ -337,6 +337,8 @@ class Reference:
                                       C.POINTER(C.c_double)]
         L.ref_net_output.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                      C.POINTER(C.c_int)]
+        L.ref_net_group_traffic.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.POINTER(C.c_double)]
         self.has_io = hasattr(L, "ref_tspw_write")  # io.cpp compiled in (json.hpp found)
         if self.has_io:
             L.ref_tspw_write.argtypes = [C.c_char_p, C.c_int, _i32p, _f64p]
@@ -532,6 +534,13 @@ class RefNet:
         self.ref._check(self.ref.lib.ref_net_measure(self.ptr, int(fwd), int(dgrad), int(wgrad),
                                                      C.byref(t)))
         return t.value
+
+    def group_traffic(self, group, kind, splits=0, tile_large=False):
+        """modeled_group_traffic (network.cpp:453-471) after forward()/output()."""
+        b = C.c_double()
+        self.ref._check(self.ref.lib.ref_net_group_traffic(self.ptr, group, kind, splits,
+                                                           int(tile_large), C.byref(b)))
+        return b.value
 
     def output(self):
         n, c = C.c_int(), C.c_int()

@@ -462,6 +462,16 @@ int ref_net_output(RefNet* n, double* y, int* n_rows, int* c_out) {
 }
 
 
+// NetworkRunner::modeled_group_traffic (network.cpp:453-471) after a forward:
+// traffic_model (cost.cpp:47-93) bytes of every layer of `group` under a
+// default_space-style config (kind, splits, small/large preset).
+int ref_net_group_traffic(RefNet* n, int group, int kind, int splits, int tile_large,
+                          double* bytes) {
+    return guard([&] {
+        *bytes = n->runner->modeled_group_traffic(group, make_cfg(kind, splits, tile_large, 0));
+    });
+}
+
 #ifdef SK_REF_IO
 // ---- io.cpp (TSPW weights, DataflowConfig / TuneResult JSON) ----------------
 int ref_tspw_write(const char* path, int n_layers, const int32_t* shapes, const double* vals) {

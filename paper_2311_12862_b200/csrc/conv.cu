@@ -1183,11 +1183,14 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
         const int item = iter >> 1, h = iter & 1;  // 128-row half h of a 256-row item
         Item it = decode(p, item);
         const int n0 = it.nt * kSimtN;
-        float acc[8][4];
+        // fp64 accumulators: this is the 1e-5 parity path, so a row's
+        // K^D * C_in products must not carry fp32 summation error (the result
+        // is rounded once, at the store)
+        double acc[8][4];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
         unsigned long long m0 = it.m0, m1 = it.m1;
         for (int j = next_col(m0, m1, it.biw0, it.bw1); j >= 0;
              j = next_col(m0, m1, it.biw0, it.bw1)) {
@@ -1220,7 +1223,8 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(a[i], b[jj], acc[i][jj]);
+                        for (int jj = 0; jj < 4; ++jj)
+                            acc[i][jj] = fma((double)a[i], (double)b[jj], acc[i][jj]);
                 }
                 __syncthreads();
             }
@@ -1234,11 +1238,14 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
                 const int col = n0 + tc * 4 + jj;
                 if (col >= p.n_total) continue;
                 const size_t o = (size_t)orow * p.ld_y + col;
-                const float res = p.residual ? to_f(static_cast<const T*>(p.residual)[o]) : 0.f;
-                if (p.out_mode == 0) static_cast<T*>(p.y)[o] = from_f<T>(acc[i][jj] + res);
-                else if (p.out_mode == 1) static_cast<float*>(p.y)[o] = acc[i][jj] + res;
-                else if (p.out_mode == 2) atomicAdd(static_cast<float*>(p.y) + o, acc[i][jj]);
-                else static_cast<float*>(p.y)[o] += acc[i][jj];
+                const double res = p.residual ? (double)to_f(static_cast<const T*>(p.residual)[o]) : 0.0;
+                if (p.out_mode == 0) static_cast<T*>(p.y)[o] = from_f<T>((float)(acc[i][jj] + res));
+                else if (p.out_mode == 1) static_cast<float*>(p.y)[o] = (float)(acc[i][jj] + res);
+                else if (p.out_mode == 2) atomicAdd(static_cast<float*>(p.y) + o, (float)acc[i][jj]);
+                else {
+                    float* d = static_cast<float*>(p.y) + o;
+                    *d = (float)((double)*d + acc[i][jj]);
+                }
             }
         }
     }
@@ -1380,13 +1387,16 @@ __global__ void __launch_bounds__(256) k_wgrad_small_cin(const T* __restrict__ x
     }
 }
 
+// fp64 accumulation (per thread over its chunk, fp64 atomics across chunks
+// into dw64): the fp32 path's dW sums tens of thousands of pairs per cell and
+// must stay within 1e-5 of the f64 reference; dw64 is rounded once.
 template <typename T>
 __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
                                                     const T* __restrict__ dy, int c_in, int c_out,
                                                     const long long* __restrict__ ptr,
                                                     const int* __restrict__ ws_in,
                                                     const int* __restrict__ ws_out, int chunk,
-                                                    float* __restrict__ dw) {
+                                                    double* __restrict__ dw) {
     __shared__ float xs[32][33];
     __shared__ float ds[32][33];
     const int k = blockIdx.z;
@@ -1397,7 +1407,7 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
     if (p0 >= hi) return;
     const long long p1 = min(hi, p0 + chunk);
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
-    float acc[4] = {0, 0, 0, 0};
+    double acc[4] = {0, 0, 0, 0};
     for (long long pb = p0; pb < p1; pb += 32) {
         for (int i = threadIdx.x; i < 32 * 32; i += 256) {
             int pp = i / 32, cc = i % 32;
@@ -1411,7 +1421,7 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
         for (int pp = 0; pp < 32; ++pp) {
             float d = ds[pp][tx];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = fmaf(xs[pp][ty * 4 + u], d, acc[u]);
+            for (int u = 0; u < 4; ++u) acc[u] = fma((double)xs[pp][ty * 4 + u], (double)d, acc[u]);
         }
         __syncthreads();
     }
@@ -1419,6 +1429,14 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
         int ci = ci0 + ty * 4 + u, co = co0 + tx;
         if (ci < c_in && co < c_out) atomicAdd(&dw[((size_t)k * c_in + ci) * c_out + co], acc[u]);
     }
+}
+
+// dw (fp32) = [dw +] dw64, rounded once
+__global__ void k_round_f64(const double* __restrict__ src, long long n, float* __restrict__ dw,
+                            int accumulate) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        dw[i] = accumulate ? (float)((double)dw[i] + src[i]) : (float)src[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -2262,18 +2280,26 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
     const int chunks = (int)ceil_div(std::max<int64_t>(per_off, 1), chunk);
     dim3 grid(chunks, (unsigned)(ceil_div(c_in, 32) * ceil_div(c_out, 32)), m->kd);
     const long long* ptr = m->ws_ptr.as<long long>();
+    const long long cells = (long long)m->kd * c_in * c_out;
+    DevBuf dw64;
+    dw64.alloc((size_t)cells * 8, st);
+    SK_CUDA(cudaMemsetAsync(dw64.p, 0, (size_t)cells * 8, st));
+    double* d64 = dw64.as<double>();
     if (dt == SK_F32)
         k_wgrad_simt<float><<<grid, 256, 0, st>>>((const float*)x, (const float*)dy, c_in, c_out,
                                                   ptr, m->ws_in.as<int>(), m->ws_out.as<int>(),
-                                                  chunk, dw);
+                                                  chunk, d64);
     else if (dt == SK_F16)
         k_wgrad_simt<__half><<<grid, 256, 0, st>>>((const __half*)x, (const __half*)dy, c_in,
                                                    c_out, ptr, m->ws_in.as<int>(),
-                                                   m->ws_out.as<int>(), chunk, dw);
+                                                   m->ws_out.as<int>(), chunk, d64);
     else
         k_wgrad_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(
             (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, c_in, c_out, ptr,
-            m->ws_in.as<int>(), m->ws_out.as<int>(), chunk, dw);
+            m->ws_in.as<int>(), m->ws_out.as<int>(), chunk, d64);
+    SK_LAUNCH_CHECK();
+    k_round_f64<<<(int)std::min<long long>(ceil_div(cells, 256), 148 * 16), 256, 0, st>>>(
+        d64, cells, dw, accumulate ? 1 : 0);
     SK_LAUNCH_CHECK();
 }
 

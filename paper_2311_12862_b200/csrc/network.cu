@@ -744,11 +744,14 @@ double modeled_group_traffic(sk_net* n, int g, const sk_dataflow_cfg& cfg, cudaS
             wr = pairs * l.c_out;
             rd = pairs * l.c_in + kdv * unit + pairs * l.c_out;
         } else {
-            Prepared* p = kmap_prepare(m, std::min(cfg.splits, m->kd), kTileM, st);
-            const double s_eff = std::max(1, p->num_splits), red = s_eff > 1 ? 1 : 0;
-            double a_loads = 0;
-            for (int s = 0; s < p->num_splits; ++s)
-                a_loads += (double)p->rows_pad * (p->begin[s + 1] - p->begin[s]) * l.c_in;
+            // prepare_os_map = pad_map(split_and_sort(raw, s), cta_m)
+            // (exec.cpp:342-344): every split keeps all n_out rows padded to
+            // the preset's cta_m and the split widths sum to K^D, so the A
+            // loads are rows_padded * K^D * C_in whatever the split count
+            const int pad = cfg.tile.cta_m > 0 ? cfg.tile.cta_m : kTileM;
+            const double rows = (double)ceil_div((int64_t)m->n_out, pad) * pad;
+            const double s_eff = std::max(1, std::min(cfg.splits, m->kd)), red = s_eff > 1 ? 1 : 0;
+            const double a_loads = rows * kdv * l.c_in;
             wr = (s_eff * n_out + red * n_out) * l.c_out;
             rd = a_loads + kdv * unit + red * s_eff * n_out * l.c_out;
         }
