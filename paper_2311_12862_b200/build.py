@@ -64,7 +64,7 @@ def build(verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if jobs or _stale(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas",
+        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart",
              "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     return LIB
 

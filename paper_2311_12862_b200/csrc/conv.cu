@@ -41,6 +41,7 @@
 #include <type_traits>
 
 #include "sk_internal.hpp"
+#include "sk_tc.cuh"
 
 namespace sk {
 
@@ -295,126 +296,6 @@ struct Cursor {
     }
 };
 
-template <typename T>
-struct Fmt;
-template <>
-struct Fmt<__half> {
-    static constexpr uint32_t v = 0;
-};
-template <>
-struct Fmt<__nv_bfloat16> {
-    static constexpr uint32_t v = 1;
-};
-
-__device__ __forceinline__ uint32_t pack2(float a, float b, __half*) {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ uint32_t pack2(float a, float b, __nv_bfloat16*) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ float2 unpack2(uint32_t u, __half*) {
-    return __half22float2(*reinterpret_cast<__half2*>(&u));
-}
-__device__ __forceinline__ float2 unpack2(uint32_t u, __nv_bfloat16*) {
-    return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm, int col, int r0,
-                                            int r1, int r2, int r3, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_tile2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
-                                           uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-// whole-warp (uniform) callers: one elected lane issues
-__device__ __forceinline__ void tma_gather4_elect(uint32_t dst, const CUtensorMap* tm, int col,
-                                                  int r0, int r1, int r2, int r3, uint64_t* bar) {
-    asm volatile(
-        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n"
-        "@P cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n}" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_tile2d_elect(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
-                                                 uint64_t* bar) {
-    asm volatile(
-        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n"
-        "@P cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];\n}" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(dst),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s_elect(uint32_t dst, const void* src, uint32_t bytes,
-                                               uint64_t* bar) {
-    asm volatile(
-        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n"
-        "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}" ::
-            "r"(dst),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// K-major smem descriptor; row = KC*2 bytes, 8-row swizzle atoms (SBO).
-template <int KC>
-__device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr) {
-    constexpr uint32_t RB = KC * 2;                                  // 32 / 64 / 128
-    constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);  // SW128/SW64/SW32
-    constexpr uint64_t sbo = (8 * RB) >> 4;
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | (sbo << 32) | (1ull << 46) | (layout << 61);
-}
-
-// byte offset of 16B chunk q of row r inside a K-major swizzled tile whose
-// base is aligned to the swizzle repeat (Swizzle<B,4,3>: bits[4,4+B) ^= bits[7,7+B))
-template <int KC>
-__device__ __forceinline__ uint32_t swz(int r, int q) {
-    constexpr uint32_t RB = KC * 2;
-    constexpr uint32_t B = RB == 128 ? 7 : (RB == 64 ? 3 : 1);
-    const uint32_t off = (uint32_t)r * RB + (uint32_t)q * 16;
-    return off ^ (((off >> 7) & B) << 4);
-}
-
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
 
 // epilogue store of 16 fp32 accumulators (row orow, columns col..col+15)
 template <typename T>
@@ -466,41 +347,6 @@ __device__ __forceinline__ void store16(const ConvArgs& p, long long orow, int c
     }
 }
 
-// One K step of both 128-row halves (KC/16 MMAs each, interleaved so they
-// share the B stage), then commit -> bar. Called by the whole warp with
-// uniform operands; elect.sync picks the issuing lane.
-template <int KC>
-__device__ __forceinline__ void tc_mma_step_f16(uint32_t d0, uint32_t d1, uint64_t a0, uint64_t a1,
-                                                uint64_t b, uint32_t idesc, uint32_t accumulate,
-                                                uint64_t* bar) {
-#pragma unroll
-    for (int kk = 0; kk < KC / 16; ++kk) {
-        const uint32_t acc = (kk > 0 || accumulate) ? 1u : 0u;
-        asm volatile(
-            "{\n.reg .pred E, p;\n"
-            "elect.sync _|E, 0xffffffff;\n"
-            "setp.ne.b32 p, %6, 0;\n"
-            "@E tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, p;\n"
-            "@E tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %5, p;\n"
-            "}\n" ::"r"(d0),
-            "r"(d1), "l"(a0 + (uint64_t)(kk * 2)), "l"(a1 + (uint64_t)(kk * 2)),
-            "l"(b + (uint64_t)(kk * 2)), "r"(idesc), "r"(acc)
-            : "memory");
-    }
-    if (bar)
-        asm volatile(
-            "{\n.reg .pred E;\nelect.sync _|E, 0xffffffff;\n"
-            "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
-                smem_u32(bar))
-            : "memory");
-}
-__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
-    asm volatile(
-        "{\n.reg .pred E;\nelect.sync _|E, 0xffffffff;\n"
-        "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
 
 // Per ring slot, built by the index warp from the slot's 256 row indices:
 // for each producer warp's 16-row group the list of its real rows
@@ -1671,6 +1517,8 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int 
 
 size_t elem_size(sk_dtype dt) { return dt == SK_F32 ? 4 : 2; }
 
+}  // namespace
+
 // ---- tensor maps (driver entry point resolved once through cudart) ----
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1687,6 +1535,25 @@ EncodeTiledFn encode_fn() {
         return reinterpret_cast<EncodeTiledFn>(f);
     }();
     return fn;
+}
+
+// 2D row-major tensor [rows][cols] with row pitch ld (elements), any element
+// type, box {box_cols, box_rows}, swizzle = box_cols * elem bytes (32/64/128)
+CUtensorMap make_tmap_rows(const void* base, CUtensorMapDataType ty, int elem_bytes, long long cols,
+                           long long rows, long long ld, int box_cols, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)std::max<long long>(rows, 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * elem_bytes)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    const int rb = box_cols * elem_bytes;
+    CUtensorMapSwizzle sw = rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = encode_fn()(&m, ty, 2, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
 }
 
 // 2D row-major [rows][cols] half tensor, box {kc, box_rows}, swizzle = kc*2 bytes
@@ -1707,6 +1574,8 @@ CUtensorMap make_tmap(const void* base, sk_dtype dt, int cols, long long rows, i
     if (r != CUDA_SUCCESS) fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
 }
+
+namespace {
 
 template <typename T, int KC, bool TMA, int SLABS, int PW>
 void launch_tc_variant(const ConvArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
@@ -1990,14 +1859,6 @@ void conv_forward_prepare(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, s
     else kmap_ensure_ws(m, st);
 }
 
-bool dense_gemm_enabled() {  // SK_DENSE_CUBLAS=0: identity layers stay on k_gconv_tc
-    static const bool v = [] {
-        const char* e = getenv("SK_DENSE_CUBLAS");
-        return !e || atoi(e) != 0;
-    }();
-    return v;
-}
-
 // Forward (dgrad = false) or dgrad (dgrad = true; m_fwd is the FORWARD map).
 void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
@@ -2071,9 +1932,10 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     pick_n_tiling(n_total, cfg.tile.cta_n, tc, a.bn, a.n_ntiles);
     const bool det = ctx->deterministic;
 
-    if (m->identity && tc && !det && !residual && k_eff == k_total && dense_gemm_enabled() &&
-        dense_identity_gemm(dt, m->n_out, c_in, c_out, x, w, y, y_accum, dgrad, st))
-        return;  // plain dense GEMM -> cuBLAS (dense.cu)
+    if (m->identity && tc && !det &&
+        dense_identity_tc(ctx, dt, m->n_out, k_eff, n_total, x, b, y, residual, y_accum,
+                          cfg.tile.cta_n, st))
+        return;  // plain dense GEMM (dense.cu: k_dense_tc)
     if (m->identity && tc && !det) {
         // K=1 stride-1 layer on one coordinate set: y = x W_0 for every
         // dataflow (the map is the identity), so run it as a dense GEMM

@@ -134,9 +134,11 @@ int64_t kmap_total_pairs(sk_kmap* m, cudaStream_t st);
 // read the raw map): lets the network runner build them ahead on its map stream.
 void conv_forward_prepare(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt,
                           int c_in, int c_out, cudaStream_t st);
-// identity-map (K=1, stride 1) layers as a cuBLAS GEMM (dense.cu); false = not handled
-bool dense_identity_gemm(sk_dtype dt, long long rows, int c_in, int c_out, const void* x,
-                         const void* w, void* y, float* y_accum, bool dgrad, cudaStream_t st);
+// identity-map (K=1, stride 1) layers as a dense tcgen05 GEMM (dense.cu);
+// b = [n_total][k_total] K-major; false = shape not handled
+bool dense_identity_tc(sk_ctx* ctx, sk_dtype dt, long long rows, int k_total, int n_total,
+                       const void* x, const void* b, void* y, const void* residual,
+                       float* y_accum, int cta_n, cudaStream_t st);
 void conv_forward(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
                   int c_out, const void* x, const void* w, void* y, bool dgrad, cudaStream_t st,
                   const void* w_kmajor = nullptr, const void* residual = nullptr,

@@ -299,43 +299,6 @@ def test_forward_error_inside_map_build_propagates(env, overlap):
     assert y.shape == (len(c), 2) and bool(torch.isfinite(y.float()).all())
 
 
-def test_identity_layers_cublas_matches_gathered_kernel(env, tmp_path):
-    """The K=1 identity-map layers run as cuBLAS GEMMs (dense.cu), including
-    the backward's fp32 accumulate into the producer gradient (C operand).
-    Forward output and the chained backward's weight gradient equal the
-    all-hand-written path (SK_DENSE_CUBLAS=0, a subprocess) within tolerance."""
-    import subprocess
-    import sys
-    torch, sk, N, M = env
-    script = tmp_path / "run.py"
-    script.write_text(f"""
-import sys, numpy as np, torch
-sys.path.insert(0, {repr(str(__import__("pathlib").Path(__file__).resolve().parents[1]))})
-from paper_2311_12862_b200 import sparse as sk, models as M, network as N
-from paper_2311_12862_b200.synth import planar_patches, quantize
-c = quantize(planar_patches(20000, 7, 1.0), [0.05] * 3)
-net = N.NetworkRunner(M.minkunet18(), dtype=torch.float16, weight_seed=6)
-net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large()))
-f = torch.from_numpy(np.random.default_rng(1).standard_normal((len(c), 4)).astype(np.float16)).cuda()
-y, _ = net.forward(sk.CoordSet.create(c), f)
-g = torch.zeros(net.num_params, device="cuda")
-net.backward(torch.ones_like(y), g)
-torch.save({{"y": y.float().cpu(), "g": g.cpu()}}, sys.argv[1])
-""")
-    out = {}
-    for flag in ("0", "1"):
-        env_ = dict(__import__("os").environ, SK_DENSE_CUBLAS=flag)
-        path = tmp_path / f"r{flag}.pt"
-        r = subprocess.run([sys.executable, str(script), str(path)], env=env_, capture_output=True,
-                           text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        out[flag] = torch.load(path)
-    y0, y1 = out["0"]["y"], out["1"]["y"]
-    assert float((y0 - y1).abs().max() / y0.abs().max().clamp_min(1.0)) <= 1e-2
-    g0, g1 = out["0"]["g"], out["1"]["g"]
-    assert float((g0 - g1).abs().max() / g0.abs().max().clamp_min(1.0)) <= 1e-2
-
-
 @pytest.mark.parametrize("which", ["toy", "minkunet"])
 def test_traffic_model_matches_reference(env, reference, which):
     """modeled_group_traffic (network.cpp:453-471) = traffic_model

@@ -1,4 +1,4 @@
-"""K=1 stride-1 (identity map) layers: sk200's dense path vs a torch (cuBLAS)
+"""K=1 stride-1 (identity map) layers: sk200 k_dense_tc vs a torch (cuBLAS)
 GEMM of the same shape, device time per call (GPU sleep ahead of the start
 event hides host launch overhead)."""
 import os, sys
@@ -26,7 +26,7 @@ c = torch.from_numpy(lidar_scan(200_000, seed=1)).cuda()
 cs = sk.CoordSet.create(c)
 m = sk.build_kmap(cs, cs, 1, 1)
 n = cs.n
-for ci, co in [(32, 96), (96, 96), (32, 32), (64, 128), (128, 128)]:
+for ci, co in [(32, 96), (96, 96), (32, 32), (64, 128), (128, 128), (128, 256), (256, 256)]:
     x = torch.randn(n, ci, device="cuda").half()
     w = (torch.randn(1, ci, co, device="cuda") / 10).half()
     y = torch.empty(n, co, device="cuda").half()
