@@ -27,7 +27,6 @@
 //   k_split_keys/...   split_and_sort + pad_map (kmap.cpp:211-288): split-local
 //                      masks -> stable radix sort on (split, ~mask) -> reorder
 #include <cstdlib>
-#include <cub/cub.cuh>
 
 #include "sk_internal.hpp"
 
@@ -735,23 +734,59 @@ __global__ void k_split_keys(const int* __restrict__ os, int n, int kd, int ns,
     vals[i] = r;
 }
 
-// 32-bit sort keys straight from the query's full-width masks (kd <= 64,
-// W + split bits <= 32): split s's local big-endian mask is the bit field
-// [kd-e, kd-b) of the row mask -- 8 B per row instead of re-reading the
-// kd-wide OS row, and half the radix-sort key traffic.
-__global__ void k_split_keys32(const unsigned long long* __restrict__ masks, int n, int kd, int ns,
-                               const int* __restrict__ begin, int W,
-                               unsigned* __restrict__ keys, int* __restrict__ vals) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long long)n * ns) return;
-    const int s = (int)(i / n), r = (int)(i % n);
-    const int b = begin[s], e = begin[s + 1], w = e - b;
-    const unsigned long long m = masks[r];  // words == 1: column j <-> bit kd-1-j
-    const unsigned local = (unsigned)((m >> (kd - e)) & ((1ull << w) - 1));
-    unsigned key = ~local & ((1u << w) - 1);
-    if (ns > 1) key |= (unsigned)s << W;
-    keys[i] = key;
-    vals[i] = r;
+constexpr int kMaxSplitDesc = 128;  // splits <= K^D <= 125
+// split bounds for the prepare kernels, passed by value (no host->device copy)
+struct SplitDesc {
+    int ns, kd, W, n;
+    int begin[kMaxSplitDesc + 1];
+    int woff[kMaxSplitDesc + 1];
+};
+
+// k_split_keys32 + the radix sort's digit histograms for every pass (warp-
+// aggregated smem counters, one global atomic per nonzero bin per block) +
+// the split bounds on the device: one launch ahead of the sort passes
+__global__ void __launch_bounds__(256) k_split_keygen32(
+    const unsigned long long* __restrict__ masks, const SplitDesc sd, int dbits, int passes,
+    unsigned* __restrict__ keys, int* __restrict__ vals, uint32_t* __restrict__ ghist,
+    int* __restrict__ d_begin, int* __restrict__ d_woff) {
+    extern __shared__ uint32_t hsh[];  // [passes][1 << dbits]
+    const int D = 1 << dbits;
+    for (int i = threadIdx.x; i < passes * D; i += blockDim.x) hsh[i] = 0;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= sd.ns; i += blockDim.x) {
+            d_begin[i] = sd.begin[i];
+            d_woff[i] = sd.woff[i];
+        }
+    __syncthreads();
+    const long long tot = (long long)sd.n * sd.ns;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long lim = (tot + stride - 1) / stride * stride;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += stride) {
+        unsigned key = 0;
+        const bool ok = i < tot;
+        if (ok) {
+            const int s = (int)(i / sd.n), r = (int)(i % sd.n);
+            const int b = sd.begin[s], e = sd.begin[s + 1], w = e - b;
+            const unsigned long long m = masks[r];  // column j <-> bit kd-1-j
+            const unsigned local = (unsigned)((m >> (sd.kd - e)) & ((1ull << w) - 1));
+            key = ~local & ((1u << w) - 1);
+            if (sd.ns > 1) key |= (unsigned)s << sd.W;
+            keys[i] = key;
+            vals[i] = r;
+        }
+        for (int p = 0; p < passes; ++p)
+            hist_add(hsh + p * D, ok ? (int)((key >> (p * dbits)) & (unsigned)(D - 1)) : -1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * D; i += blockDim.x)
+        if (hsh[i]) atomicAdd(&ghist[i], hsh[i]);
+}
+
+__global__ void k_split_desc(const SplitDesc sd, int* __restrict__ d_begin, int* __restrict__ d_woff) {
+    for (int i = threadIdx.x; i <= sd.ns; i += blockDim.x) {
+        d_begin[i] = sd.begin[i];
+        d_woff[i] = sd.woff[i];
+    }
 }
 
 __device__ void row_reorder(const int* __restrict__ os, int n, int kd, int rows_pad,
@@ -996,16 +1031,10 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     SK_LAUNCH_CHECK();
     k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), n, flag.as<int>());
     SK_LAUNCH_CHECK();
-    size_t tbytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tbytes, flag.as<int>(), pos.as<int>(), n + 1, st);
-    tmp.alloc(tbytes, st);
-    // scan n+1 items: the last (flag past the end reads pos[n] slot) -> total
-    // count lands in pos[n] via an inclusive trick: exclusive over n then add
-    cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, flag.as<int>(), pos.as<int>(), n, st);
-    SK_LAUNCH_CHECK();
-    int h_last[2] = {0, 0};
-    read_back(st, {{pos.as<int>() + n - 1, 4}, {flag.as<int>() + n - 1, 4}}, h_last);
-    out->n = h_last[0] + h_last[1];
+    scan_exclusive_i32(flag.as<int>(), pos.as<int>(), n, pos.as<int>() + n, st);
+    int h_count = 0;
+    read_back(st, {{pos.as<int>() + n, 4}}, &h_count);
+    out->n = h_count;
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
     k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(),
                                       q.as<int4>(), n, out->table.as<ulonglong2>(),
@@ -1058,14 +1087,10 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
     }
     k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), m, flag.as<int>());
     SK_LAUNCH_CHECK();
-    size_t tbytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tbytes, flag.as<int>(), pos.as<int>(), m, st);
-    tmp.alloc(tbytes, st);
-    cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, flag.as<int>(), pos.as<int>(), m, st);
-    SK_LAUNCH_CHECK();
-    int h_last[2] = {0, 0};
-    read_back(st, {{pos.as<int>() + m - 1, 4}, {flag.as<int>() + m - 1, 4}}, h_last);
-    out->n = h_last[0] + h_last[1];
+    scan_exclusive_i32(flag.as<int>(), pos.as<int>(), m, pos.as<int>() + m, st);
+    int h_count = 0;
+    read_back(st, {{pos.as<int>() + m, 4}}, &h_count);
+    out->n = h_count;
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
     k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(), q.as<int4>(),
                                       m, out->table.as<ulonglong2>(), out->coords.as<int4>());
@@ -1168,16 +1193,14 @@ sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int 
         }
         int rbits = 1;
         while ((1 << rbits) < R) ++rbits;
-        size_t tb = 0;
         // LSD radix sort is stable: equal (relation, dst) keep the edge order
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<unsigned long long>(),
-                                        keys2.as<unsigned long long>(), vals.as<int>(),
-                                        order.as<int>(), E, 0, 32 + rbits, st);
-        tmp.alloc(tb, st);
-        cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<unsigned long long>(),
-                                        keys2.as<unsigned long long>(), vals.as<int>(),
-                                        order.as<int>(), E, 0, 32 + rbits, st);
-        SK_LAUNCH_CHECK();
+        unsigned long long* kb[2] = {keys.as<unsigned long long>(), keys2.as<unsigned long long>()};
+        int* vb[2] = {vals.as<int>(), order.as<int>()};
+        const int res = radix_sort_pairs<unsigned long long>(kb, vb, E, 0, 32 + rbits, st);
+        if (res == 0) {  // k_edge_scatter reads keys2 / order
+            SK_CUDA(cudaMemcpyAsync(keys2.p, keys.p, (size_t)E * 8, cudaMemcpyDeviceToDevice, st));
+            SK_CUDA(cudaMemcpyAsync(order.p, vals.p, (size_t)E * 4, cudaMemcpyDeviceToDevice, st));
+        }
         k_edge_scan<<<1, 1, 0, st>>>(counts.as<int>(), R, m->ws_ptr.as<long long>(),
                                      m->ws_tile_ptr.as<int>());
         SK_LAUNCH_CHECK();
@@ -1410,8 +1433,25 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
     DevBuf d_woff;
     d_begin.alloc((ns + 1) * 4, st);
     d_woff.alloc((ns + 1) * 4, st);
-    SK_CUDA(cudaMemcpyAsync(d_begin.p, p->begin.data(), (ns + 1) * 4, cudaMemcpyHostToDevice, st));
-    SK_CUDA(cudaMemcpyAsync(d_woff.p, p->word_off.data(), (ns + 1) * 4, cudaMemcpyHostToDevice, st));
+    validate(ns <= kMaxSplitDesc, "split count exceeds 128");
+    SplitDesc sd;
+    sd.ns = ns;
+    sd.kd = kd;
+    sd.W = W;
+    sd.n = n;
+    for (int i = 0; i <= ns; ++i) {
+        sd.begin[i] = p->begin[i];
+        sd.woff[i] = p->word_off[i];
+    }
+    int sbits = 0;
+    while ((1 << sbits) < ns) ++sbits;
+    // the fused key-generation path (32-bit keys from the query's masks) writes
+    // the split bounds itself; every other path gets them from k_split_desc
+    const bool fused32 = splits != 0 && n != 0 && kd <= 64 && W + (ns > 1 ? sbits : 0) <= 32;
+    if (!fused32) {
+        k_split_desc<<<1, 128, 0, st>>>(sd, d_begin.as<int>(), d_woff.as<int>());
+        SK_LAUNCH_CHECK();
+    }
 
     DevBuf order;
     order.alloc((size_t)std::max(n * ns, 1) * 4, st);
@@ -1423,44 +1463,49 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
         }
     } else {
         const long long tot = (long long)n * ns;
-        int sbits = 0;
-        while ((1 << sbits) < ns) ++sbits;
-        DevBuf k_in, k_out, v_in, tmp;
-        k_in.alloc(tot * 8, st);
-        k_out.alloc(tot * 8, st);
+        DevBuf k_in, k_out, v_in, v_out, order1;
+        k_in.alloc(tot * (fused32 ? 4 : 8), st);
+        k_out.alloc(tot * (fused32 ? 4 : 8), st);
         v_in.alloc(tot * 4, st);
+        if (!fused32) v_out.alloc(tot * 4, st);
+        if (!fused32 && W > 64) order1.alloc(tot * 4, st);
         const int g = (int)ceil_div(tot, 256);
-        DevBuf order1;
-        order1.alloc(tot * 4, st);
+        // stable sort of (key, row) -> dst (hand-written radix sort, sort.cu)
+        auto sort_to = [&](auto* kdummy, int end_bit, int* dst) {
+            using KT = std::remove_pointer_t<decltype(kdummy)>;
+            KT* kb[2] = {k_in.as<KT>(), k_out.as<KT>()};
+            int* vb[2] = {v_in.as<int>(), v_out.as<int>()};
+            const int r = radix_sort_pairs<KT>(kb, vb, (int)tot, 0, end_bit, st);
+            SK_CUDA(cudaMemcpyAsync(dst, vb[r], (size_t)tot * 4, cudaMemcpyDeviceToDevice, st));
+        };
         auto sort_pass = [&](int word, int end_bit, const int* perm, int* dst) {
             k_split_keys<<<g, 256, 0, st>>>(m->os.as<int>(), n, kd, ns, d_begin.as<int>(), W, word,
                                             perm, k_in.as<unsigned long long>(), v_in.as<int>());
             SK_LAUNCH_CHECK();
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in.as<unsigned long long>(),
-                                            k_out.as<unsigned long long>(), v_in.as<int>(), dst,
-                                            (int)tot, 0, end_bit, st);
-            tmp.alloc(tb, st);
-            cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.as<unsigned long long>(),
-                                            k_out.as<unsigned long long>(), v_in.as<int>(), dst,
-                                            (int)tot, 0, end_bit, st);
-            SK_LAUNCH_CHECK();
+            sort_to((unsigned long long*)nullptr, end_bit, dst);
         };
-        if (kd <= 64 && W + (ns > 1 ? sbits : 0) <= 32) {
+        if (fused32) {
             const int end_bit = W + (ns > 1 ? sbits : 0);
-            k_split_keys32<<<g, 256, 0, st>>>(m->masks.as<unsigned long long>(), n, kd, ns,
-                                              d_begin.as<int>(), W, k_in.as<unsigned>(),
-                                              v_in.as<int>());
+            const RadixPlan pl = radix_plan((int)tot, end_bit);
+            DevBuf scratch;
+            scratch.alloc(pl.scratch_words * 4, st);
+            SK_CUDA(cudaMemsetAsync(scratch.p, 0, scratch.bytes, st));
+            // values start in the buffer that makes the last pass land in order
+            int* vb[2];
+            vb[pl.passes % 2] = order.as<int>();
+            vb[(pl.passes + 1) % 2] = v_in.as<int>();
+            unsigned* kb[2] = {k_in.as<unsigned>(), k_out.as<unsigned>()};
+            const size_t hsm = pl.hist_words * 4;
+            ensure_smem(reinterpret_cast<const void*>(k_split_keygen32), hsm);
+            const int kg = (int)std::min<long long>(ceil_div(tot, 256), 2 * 148);
+            k_split_keygen32<<<kg, 256, hsm, st>>>(m->masks.as<unsigned long long>(), sd, pl.dbits,
+                                                   pl.passes, kb[0], vb[0], scratch.as<uint32_t>(),
+                                                   d_begin.as<int>(), d_woff.as<int>());
             SK_LAUNCH_CHECK();
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in.as<unsigned>(), k_out.as<unsigned>(),
-                                            v_in.as<int>(), order.as<int>(), (int)tot, 0, end_bit,
-                                            st);
-            tmp.alloc(tb, st);
-            cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.as<unsigned>(), k_out.as<unsigned>(),
-                                            v_in.as<int>(), order.as<int>(), (int)tot, 0, end_bit,
-                                            st);
-            SK_LAUNCH_CHECK();
+            const int r = radix_sort_run<unsigned>(kb, vb, (int)tot, 0, pl, scratch.as<uint32_t>(),
+                                                   true, st);
+            if (vb[r] != order.as<int>())  // fewer passes ran (n <= 1)
+                SK_CUDA(cudaMemcpyAsync(order.p, vb[r], (size_t)tot * 4, cudaMemcpyDeviceToDevice, st));
         } else if (W <= 64) {
             sort_pass(0, std::min(64, W + (ns > 1 ? sbits : 0)), nullptr, order.as<int>());
         } else {

@@ -289,6 +289,13 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                  "f"(c), "f"(d)
                  : "memory");
 }
+// warp-aggregated shared-memory histogram increment: the whole warp calls it
+// (d < 0: no-op lane); one atomic per distinct digit in the warp, so skewed
+// digit distributions do not serialise on one bank
+__device__ __forceinline__ void hist_add(uint32_t* h, int d) {
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[d], (uint32_t)__popc(peers));
+}
 #endif
 
 }  // namespace sk

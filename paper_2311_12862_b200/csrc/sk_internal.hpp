@@ -153,6 +153,26 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
                 int c_out, const void* x, const void* dy, float* dw, cudaStream_t st,
                 bool accumulate = false);
 
+// sort.cu: hand-written scan / stable radix sort (no CUB)
+// out[i] = sum in[0..i); *total_dev (optional, device) = sum of all n
+void scan_exclusive_i32(const int* in, int* out, int n, int* total_dev, cudaStream_t st);
+// stable LSD sort of (key, value) pairs on bits [begin_bit, end_bit); keys[0]
+// / vals[0] hold the input, keys[1] / vals[1] scratch of the same size;
+// returns the index (0 / 1) of the buffers holding the sorted result
+template <typename KT>
+int radix_sort_pairs(KT* keys[2], int* vals[2], int n, int begin_bit, int end_bit, cudaStream_t st);
+// the same in steps, for callers that fuse the digit histogram into their key
+// generation: plan, a zeroed scratch of scratch_words u32 (digit histograms
+// [passes][digits] first, then the look-back status), run
+struct RadixPlan {
+    int bits = 0, passes = 0, dbits = 0, digits = 1, tiles = 0;
+    size_t hist_words = 0, scratch_words = 0;
+};
+RadixPlan radix_plan(int n, int bits);
+template <typename KT>
+int radix_sort_run(KT* keys[2], int* vals[2], int n, int begin_bit, const RadixPlan& pl,
+                   uint32_t* scratch, bool have_hist, cudaStream_t st);
+
 uint64_t next_coord_set_id();
 void set_last_error(const std::string& m);
 
