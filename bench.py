@@ -536,25 +536,23 @@ def run_train(args, rank, world, local):
 
 
 def kmap_roofline(sk, pk):
-    """Kernel-map build (hash insert + K=3 submanifold query: OS matrix, masks,
-    per-offset counts) on the C5 1M-voxel sweep point (10 disjoint tiles of the
-    planar n=160k / 2.5 cm recipe); algorithmic bytes per the
-    survey's contract with the actual table size (cap x 12 B, charged once for
-    the insert and once for the query)."""
+    """Kernel-map build on the C5 1M-voxel sweep point (10 disjoint tiles of
+    the planar n=160k / 2.5 cm recipe): coordinate set creation
+    (copy + hash insert) and the K=3 submanifold map (block-index query at
+    this size: k_block_insert + k_kmap_query_blk; OS, masks). Algorithmic bytes are SURVEY §8(d)'s contract: 100 + 4*K^D =
+    208 B per voxel (coords, the table charged at 2N x 16 B for the insert and
+    again for the query, out coords, OS and masks)."""
     import torch
     from paper_2311_12862_b200.synth import sweep_cloud
     coords = torch.from_numpy(sweep_cloud(160_000, seed=1, tiles=10)).cuda()
     n = coords.shape[0]
-    cap = 64
-    while cap < 4 * n:  # load factor <= 1/4 (kmap.cu pow2_cap)
-        cap *= 2
     ins, qry = [], []
-    for _ in range(4):
+    for _ in range(5):
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record()
         cs = sk.CoordSet.create(coords)  # copy + hash insert (+ range check read)
         b.record()
-        m = sk.build_kmap(cs, cs, 3, 1)  # query kernel: OS, masks, counts
+        m = sk.build_kmap(cs, cs, 3, 1)  # block index + query: OS, masks
         c.record()
         torch.cuda.synchronize()
         ins.append(a.elapsed_time(b))
@@ -562,15 +560,19 @@ def kmap_roofline(sk, pk):
         del m, cs
     t_ins, t_q = statistics.median(ins[1:]), statistics.median(qry[1:])
     kd = 27
-    b_ins = 16 * n + 16 * cap + 16 * n       # coords copy (r+w) + table write (16 B slots)
-    b_q = 16 * n + 16 * cap + 4 * kd * n + 8 * n  # out coords, table read, OS, masks
-    achieved = (b_ins + b_q) / ((t_ins + t_q) * 1e-3) / 1e9
+    algo = (100 + 4 * kd) * n
+    achieved = algo / ((t_ins + t_q) * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("kmap_dram_bytes_per_build")
     return {"bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs", 6650.0),
-            "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs", 6650.0), "traffic": None,
+            "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs", 6650.0), "traffic": traffic,
             "voxels": int(n), "insert_ms": t_ins, "query_ms": t_q,
-            "query_gbs": b_q / (t_q * 1e-3) / 1e9,
-            "algorithmic_bytes": int(b_ins + b_q),
-            "kernel": "k_hash_insert + k_kmap_query<27,4> (1M-voxel C5 sweep point)"}
+            "algorithmic_bytes": int(algo),
+            "bytes_contract": "SURVEY 8(d): 208 B/voxel at K=3 (table at 2N x 16 B)",
+            "kernel": "k_hash_insert + k_block_insert + k_kmap_query_blk<3> "
+                      "(1M-voxel C5 sweep point)"}
 
 
 def layer_pairs(sk, net, cs):

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("SK200_LIB") or os.path.join(PKG, "libsk200.so")
 # exported symbols, in header order (include/sk200.h); tests check the .so
 # exports exactly these
 SYMBOLS = [
-    "sk_last_error", "sk_version", "sk_kernel_launches", "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_deterministic",
+    "sk_last_error", "sk_version", "sk_kernel_launches", "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_deterministic", "sk_ctx_set_kmap_block_rows",
     "sk_coords_create", "sk_coords_create_host", "sk_coords_retain", "sk_coords_release",
     "sk_quantize", "sk_quantize_features", "sk_kmap_from_edges", "sk_kmap_build_ex",
     "sk_coords_n", "sk_coords_dims", "sk_coords_id", "sk_coords_device_ptr",
@@ -85,6 +85,7 @@ def lib():
         "sk_ctx_create": ([C.c_int, pp], C.c_int),
         "sk_ctx_destroy": ([vp], C.c_int),
         "sk_ctx_set_deterministic": ([vp, C.c_int], C.c_int),
+        "sk_ctx_set_kmap_block_rows": ([vp, C.c_int], C.c_int),
         "sk_coords_create": ([vp, C.c_int, C.c_int, vp, i32p, vp, pp], C.c_int),
         "sk_coords_create_host": ([vp, C.c_int, C.c_int, vp, i32p, vp, pp], C.c_int),
         "sk_coords_retain": ([vp], C.c_int),

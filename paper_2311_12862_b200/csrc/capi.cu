@@ -293,6 +293,14 @@ sk_status sk_ctx_set_deterministic(sk_ctx* ctx, int on) {
     });
 }
 
+sk_status sk_ctx_set_kmap_block_rows(sk_ctx* ctx, int min_rows) {
+    return guard([&] {
+        sk::validate(ctx != nullptr, "null context");
+        sk::validate(min_rows >= 0, "min_rows must be >= 0");
+        ctx->kmap_block_rows = min_rows;
+    });
+}
+
 sk_status sk_coords_create(sk_ctx* ctx, int dims, int n, const int32_t* d_coords,
                            const int32_t stride_tag[3], void* stream, sk_coords** out) {
     return guard([&] { *out = make_coords(ctx, dims, n, d_coords, false, stride_tag, S(stream)); });

@@ -913,20 +913,16 @@ void coords_build_blocks(sk_coords* c, cudaStream_t st) {
 // stride-1, non-transposed, 3-D, K in {3, 5}, large input sets: the block-
 // index query. Measured: its extra build pass costs more than it saves below
 // ~0.5M input voxels (MinkUNet scan: maps 0.72 -> 0.82 ms), above it the query
-// is ~12% faster (1M-voxel sweep point). SK_KMAP_BLOCKS=0/1 forces off/on.
-bool use_block_query(const sk_kmap* m) {
-    static const int mode = [] {
-        const char* e = getenv("SK_KMAP_BLOCKS");
-        return e ? atoi(e) : -1;
-    }();
+// is ~12% faster (1M-voxel sweep point). The threshold is a context setting
+// (sk_ctx_set_kmap_block_rows, default 1 << 19).
+bool use_block_query(const sk_kmap* m, const sk_coords* in) {
     const bool shape = !m->transposed && m->dims == 3 && (m->kernel == 3 || m->kernel == 5) &&
                        m->stride[0] == 1 && m->stride[1] == 1 && m->stride[2] == 1;
-    if (!shape || mode == 0) return false;
-    return mode == 1 || m->n_in >= (1 << 19);
+    return shape && in->n > 0 && m->n_in >= in->ctx->kmap_block_rows;
 }
 
 void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_t st) {
-    if (use_block_query(m)) {
+    if (use_block_query(m, in)) {
         coords_build_blocks(in, st);
         const int grid = m->rows_pad / kQB;
         const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;

@@ -7,6 +7,7 @@ struct sk_ctx {
     int device = 0;
     int num_sms = 148;
     bool deterministic = false;
+    int kmap_block_rows = 1 << 19;  // sk_ctx_set_kmap_block_rows
     size_t smem_optin = 227 * 1024;
 };
 

@@ -77,6 +77,12 @@ class Context:
         check(lib().sk_ctx_set_deterministic(self.ptr, int(bool(on))))
         self._deterministic = bool(on)
 
+    def set_kmap_block_rows(self, min_rows: int) -> None:
+        """Stride-1 3-D K=3/5 maps over input sets of >= min_rows voxels are
+        queried through a 4x4x4 block index (default 1 << 19; identical
+        results)."""
+        check(lib().sk_ctx_set_kmap_block_rows(self.ptr, int(min_rows)))
+
 
 class CoordSet:
     """Device coordinate set with a stable id (coord_set_id, tensor.cpp:26-29)."""

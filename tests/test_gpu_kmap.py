@@ -222,6 +222,7 @@ from oracle.oracle import Reference
 from paper_2311_12862_b200 import sparse as sk
 from paper_2311_12862_b200.synth import random_instance_coords, lidar_scan
 ref = Reference()
+sk.Context.get().set_kmap_block_rows(int(sys.argv[2]))
 cases = [(1, 300, 3, 1, 12), (4, 200, 5, 1, 12), (8, 20000, 3, 1, 60), (11, 6000, 5, 3, 25),
          (12, 3000, 3, 2, 400)]
 for seed, n, k, batches, rng in cases:
@@ -239,6 +240,18 @@ for seed, n, k, batches, rng in cases:
             ri, ro = rm.pairs(kk)
             assert np.array_equal(inn[ptr[kk]:ptr[kk + 1]], ri)
             assert np.array_equal(outs[ptr[kk]:ptr[kk + 1]], ro)
+    for k in (3, 5):  # strided / transposed maps on the same sets (hash query)
+        m = sk.build_kmap(c, o, k, 2)
+        rm = ref.kmap(3, k, c_np, o_np, [2, 2, 2])
+        assert np.array_equal(m.os()[0], rm.os()[0]) and np.array_equal(m.os()[1], rm.os()[1])
+        mt = sk.build_kmap(o, c, k, 2, transposed=True)
+        rmt = ref.kmap(3, k, o_np, c_np, [2, 2, 2], transposed=True)
+        assert np.array_equal(mt.os()[0], rmt.os()[0]), (seed, k, "transposed")
+for dims, k in ((2, 3), (2, 5)):  # 2-D sets: z == 0, one block layer
+    c_np = random_instance_coords(21, 3000, -40, 40, 2, dims=2)
+    c = sk.CoordSet.create(c_np, dims=2)
+    m, rm = sk.build_kmap(c, c, k, 1), ref.kmap(2, k, c_np, c_np, [1, 1, 1])
+    assert np.array_equal(m.os()[0], rm.os()[0]) and np.array_equal(m.os()[1], rm.os()[1])
 s_np = lidar_scan(60_000, seed=5)
 s = sk.CoordSet.create(s_np)
 m, rm = sk.build_kmap(s, s, 3, 1), ref.kmap(3, 3, s_np, s_np, [1, 1, 1])
@@ -247,13 +260,16 @@ print("blocks ok")
 '''
 
 
-def test_block_index_query_matches_reference(reference):
-    """The 4x4x4 block-index query (used for stride-1 maps on >= 0.5M-voxel
-    sets) forced on small instances: K=3/5, batches, negative coordinates,
-    output set != input set, a LiDAR-shaped scan."""
+@pytest.mark.parametrize("min_rows", [1, 100])
+def test_block_query_matches_reference(reference, min_rows):
+    """The 4x4x4 block-index query (stride-1 3-D maps on >= 2^19-voxel input
+    sets) forced on small instances (every set, or sets >= 100 voxels): K=3/5,
+    batches, negative coordinates, output set != input set, a LiDAR scan, and
+    the hash-query maps (strided, transposed, 2-D sets) next to it; OS, masks
+    and the WS lists bit-exact vs the reference."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", BLOCK_CHECK, root], capture_output=True, text=True,
-                       env={**os.environ, "SK_KMAP_BLOCKS": "1"}, timeout=600)
+    r = subprocess.run([sys.executable, "-c", BLOCK_CHECK, root, str(min_rows)],
+                       capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "blocks ok" in r.stdout, r.stdout + r.stderr
