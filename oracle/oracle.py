@@ -37,6 +37,11 @@ def build(reference: bool = True) -> None:
     targets = ["restatement"]
     if reference and os.path.isdir("/root/reference/proj/src"):
         targets.append("reference")
+        # the INTEGRATION.md shim against the reference headers (needs the
+        # product library, which build() compiles first)
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2311_12862_b200",
+                                       "libsk200.so")):
+            targets.append("shim")
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
