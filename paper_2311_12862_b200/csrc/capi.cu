@@ -256,6 +256,8 @@ sk_status sk_ctx_create(int device, sk_ctx** out) {
         SK_CUDA(cudaGetDeviceProperties(&prop, device));
         c->num_sms = prop.multiProcessorCount;
         c->smem_optin = prop.sharedMemPerBlockOptin;
+        SK_CUDA(cudaMalloc(&c->sched, sk_ctx::kSchedSlots * 2 * sizeof(int)));
+        SK_CUDA(cudaMemset(c->sched, 0, sk_ctx::kSchedSlots * 2 * sizeof(int)));
         // keep freed blocks in the stream-ordered pool (no cudaFree syncs)
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -283,7 +285,13 @@ sk_status sk_ctx_create(int device, sk_ctx** out) {
 }
 
 sk_status sk_ctx_destroy(sk_ctx* ctx) {
-    return guard([&] { delete ctx; });
+    return guard([&] {
+        if (ctx && ctx->sched) {
+            cudaDeviceSynchronize();
+            cudaFree(ctx->sched);
+        }
+        delete ctx;
+    });
 }
 
 sk_status sk_ctx_set_deterministic(sk_ctx* ctx, int on) {

@@ -98,6 +98,7 @@ struct ConvArgs {
     long long* trace; // SK_CONV_TRACE builds: per-step clock64 timeline of CTA 0
     int exp;          // SK_CONV_TRACE builds: SK_EXP bits 1 no A gathers, 2 no zeroing, 4 no MMA, 8 no B TMA
     int offset_only;  // >= 0: WS mode only tiles of this offset
+    int* sched;       // dynamic item queue {next item, CTAs done} (self-resetting), or null
 };
 
 // one work item = 256 rows (OS: 128-row tiles 2*t2 and 2*t2+1 of split s;
@@ -119,6 +120,21 @@ struct ConvArgs {
     } while (0)
 #else
 #define SK_TZ(k) do {} while (0)
+#endif
+
+#ifdef SK_CONV_TRACE
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SK_CTA_REC(k, v)                                                               \
+    do {                                                                               \
+        if (p.trace && lane == 0 && blockIdx.x < 1024)                                 \
+            p.trace[4096 * 16 + blockIdx.x * 4 + (k)] = (v);                           \
+    } while (0)
+#else
+#define SK_CTA_REC(k, v) do {} while (0)
 #endif
 
 struct Item {
@@ -263,14 +279,86 @@ __device__ __forceinline__ int item_of(int i, int n_items) {
     return it < n_items ? (int)it : -1;
 }
 
+// Work-item source of one warp (all lanes call next() together).
+// Static (p.sched == null): the boustrophedon schedule of item_of. Dynamic:
+// the CTA's scheduler warp takes the next item with one global atomic
+// (descending-cost order -> greedy LPT balance across CTAs; a static
+// schedule left the slowest CTA ~1.4x the mean, tools/trace2.py) and
+// publishes it through a kItemRing smem ring that every other item-walking
+// warp of the CTA reads in order.
+constexpr int kItemRing = 4;  // smem-bound: two CTAs per SM must still fit
+struct ItemSrc {
+    int kind;  // 0 static, 1 publisher, 2 consumer
+    int local, n_items, slot;
+    uint32_t ph;
+    int* ids;
+    uint64_t* full;
+    uint64_t* empty;
+    int* sched;
+    __device__ void init(const ConvArgs& p, int dyn_kind, int n, int* ids_, uint64_t* full_,
+                         uint64_t* empty_) {
+        kind = p.sched ? dyn_kind : 0;
+        local = 0;
+        n_items = n;
+        slot = 0;
+        ph = 0;
+        ids = ids_;
+        full = full_;
+        empty = empty_;
+        sched = p.sched;
+    }
+    __device__ int next() {
+        const int lane = threadIdx.x & 31;
+        int v;
+        if (kind == 0) {
+            v = item_of(local, n_items);
+        } else if (kind == 1) {
+            mbar_wait(&empty[slot], ph ^ 1);
+            if (lane == 0) {
+                // first item static (no atomic round trip before the CTA's
+                // first gather), the rest from the queue
+                v = local == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(sched, 1);
+                if (v >= n_items) v = -1;
+                ids[slot] = v;
+                mbar_arrive(&full[slot]);
+            }
+            v = __shfl_sync(0xffffffffu, v, 0);
+        } else {
+            mbar_wait(&full[slot], ph);
+            v = ids[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+        if (kind != 0 && ++slot == kItemRing) {
+            slot = 0;
+            ph ^= 1;
+        }
+        ++local;
+        return v;
+    }
+};
+// end of a dynamically scheduled launch: the last CTA out re-zeroes the
+// queue so the context can hand the slot to a later launch
+__device__ __forceinline__ void sched_finish(const ConvArgs& p) {
+    if (p.sched && threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+            p.sched[0] = 0;
+            p.sched[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // iterator over the column steps (item, active column) of this CTA
 struct Cursor {
     int local, n_items, j;
     Item it;
     unsigned long long m0, m1;
     bool done;
+    ItemSrc* src;
     __device__ void load(const ConvArgs& p) {
-        for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
+        for (int item; (item = src->next()) >= 0; ++local) {
             it = decode(p, item);
             m0 = it.m0;
             m1 = it.m1;
@@ -282,9 +370,10 @@ struct Cursor {
         }
         done = true;
     }
-    __device__ void init(const ConvArgs& p, int n) {
+    __device__ void init(const ConvArgs& p, int n, ItemSrc* s) {
         n_items = n;
         local = 0;
+        src = s;
         load(p);
     }
     __device__ void advance(const ConvArgs& p) {
@@ -434,8 +523,11 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
     uint64_t* ifull = tempty + 2;         // [R] ring slot landed (bulk copy / fill)
     uint64_t* iempty = ifull + kIdxRing;  // [R] all gathering warps done with the slot
     uint64_t* cfull = iempty + kIdxRing;  // [R] compacted row lists of the slot ready
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + kIdxRing);
-    CSlot<PW>* cslots = reinterpret_cast<CSlot<PW>*>(tmem_slot + 4);  // [R] compacted row lists
+    uint64_t* itfull = cfull + kIdxRing;  // [kItemRing] dynamic item queue
+    uint64_t* itempty = itfull + kItemRing;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(itempty + kItemRing);
+    int* item_ids = reinterpret_cast<int*>(tmem_slot + 4);
+    CSlot<PW>* cslots = reinterpret_cast<CSlot<PW>*>(item_ids + kItemRing);  // [R] compacted row lists
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint32_t ncols = 32;
@@ -467,6 +559,10 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             const int zw_n = kZeroWarps;
 #endif
             mbar_init(&iempty[i], USE_TMA ? kTmaWarps : kProducerWarps + zw_n);
+        }
+        for (int i = 0; i < kItemRing; ++i) {
+            mbar_init(&itfull[i], 1);
+            mbar_init(&itempty[i], 5);  // MMA warp + 4 epilogue warps
         }
         fence_mbar_init();
         if (USE_TMA)
@@ -504,7 +600,16 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
 #ifdef SK_CONV_TRACE
         int tr_n = 0;
 #endif
-        for (int local = 0, item; (item = item_of(local, n_items)) >= 0; ++local) {
+        ItemSrc src;
+        src.init(p, 1, n_items, item_ids, itfull, itempty);
+        // The item queue may block this warp until the MMA / epilogue warps
+        // consume earlier items, and they wait on steps this warp has
+        // published but not yet compacted: flush before every take.
+        auto take = [&]() {
+            while (cmp < pub) compact_one();
+            return src.next();
+        };
+        for (int item; (item = take()) >= 0;) {
             const Item it = decode(p, item);
             const uint64_t r0 = it.biw0 > 0 ? (__brevll(it.m0) >> (64 - it.biw0)) : 0ull;
             const uint64_t r1 = it.bw1 > 0 ? (__brevll(it.m1) >> (64 - it.bw1)) : 0ull;
@@ -563,7 +668,9 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
 #ifdef SK_CONV_TRACE
         int tr_n = 0;
 #endif
-        cur.init(p, n_items);
+        ItemSrc src;
+        src.init(p, 1, n_items, item_ids, itfull, itempty);
+        cur.init(p, n_items, &src);
         const bool ident = (p.mode == 1 && p.a_identity) || p.mode == 2;
         int slot = 0;
         uint32_t ph = 0;
@@ -632,8 +739,14 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
 #ifdef SK_CONV_TRACE
             ++tr_n;
 #endif
+            ++pub;
+            // last column of the item: the advance takes the next item from
+            // the queue (may block on the MMA / epilogue warps), so flush the
+            // compactions they depend on first
+            if (!USE_TMA && (cur.m0 | cur.m1) == 0)
+                while (cmp < pub) compact_one();
             cur.advance(p);
-            if (!USE_TMA && ++pub - cmp > kCompactLag) compact_one();
+            if (!USE_TMA && pub - cmp > kCompactLag) compact_one();
             if (++slot == kIdxRing) {
                 slot = 0;
                 ph ^= 1;
@@ -902,9 +1015,17 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
         const uint64_t desc0 = kmajor_desc<KC>(smem_u32(stage_base));
 #ifdef SK_CONV_TRACE
         int tr_n = 0;
+        SK_CTA_REC(0, gtimer());
+        {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            SK_CTA_REC(3, (long long)smid);
+        }
 #endif
         int local = 0;
-        for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
+        ItemSrc src;
+        src.init(p, 2, n_items, item_ids, itfull, itempty);
+        for (int item; (item = src.next()) >= 0; ++local) {
             Item it = decode(p, item);
             const int acc = acc_bufs == 2 ? (local & 1) : 0;
             const uint32_t aph = acc_bufs == 2 ? (uint32_t)((local >> 1) & 1) : (uint32_t)(local & 1);
@@ -950,12 +1071,18 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             tc_commit_elect(&tfull[acc]);
             __syncwarp();
         }
+#ifdef SK_CONV_TRACE
+        SK_CTA_REC(1, gtimer());
+        SK_CTA_REC(2, (long long)tr_n);
+#endif
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ====== epilogue: thread owns TMEM lane (quad*32+lane) = rows r, 128+r ======
         const int quad = warp & 3;
         const int lr = quad * 32 + lane;
         int local = 0;
-        for (int item; (item = item_of(local, n_items)) >= 0; ++local) {
+        ItemSrc src;
+        src.init(p, 2, n_items, item_ids, itfull, itempty);
+        for (int item; (item = src.next()) >= 0; ++local) {
             Item it = decode(p, item);
             long long orow[2];
             orow[0] = out_index(p, it, lr);  // issued before the wait
@@ -992,6 +1119,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
     __syncthreads();
     tc_fence_after();
     if (warp == kMmaWarp) tmem_dealloc(tmem, ncols);
+    sched_finish(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -1582,7 +1710,8 @@ void launch_tc_variant(const ConvArgs& a, const CUtensorMap& ta, const CUtensorM
                        int grid, int stages, int acc_bufs, size_t stage_bytes,
                        cudaStream_t st) {
     const size_t smem = stages * stage_bytes + kIdxRing * (kItemM * 4 + 16) +
-                        (2 * stages + 4 + 3 * kIdxRing) * 8 + 16 + kIdxRing * sizeof(CSlot<PW>);
+                        (2 * stages + 4 + 3 * kIdxRing + 2 * kItemRing) * 8 + 16 + kItemRing * 4 +
+                        kIdxRing * sizeof(CSlot<PW>);
     auto kern = k_gconv_tc<T, KC, TMA, SLABS, PW>;
     ensure_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, Roles<PW>::kThreads, smem, st>>>(ta, tb, a, stages, acc_bufs);
@@ -1677,7 +1806,7 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
     DevBuf tbuf;
     const char* tpath = getenv("SK_TRACE");
     if (tpath) {
-        tbuf.alloc(4096 * 16 * 8, st);
+        tbuf.alloc((4096 * 16 + 4 * 1024) * 8, st);
         SK_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, st));
         a.trace = tbuf.as<long long>();
     }
@@ -1686,7 +1815,7 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
         DevBuf& b; const char* path; cudaStream_t st; const ConvArgs& a;
         ~Dump() {
             if (!path) return;
-            std::vector<long long> h(4096 * 16);
+            std::vector<long long> h(4096 * 16 + 4 * 1024);
             cudaMemcpyAsync(h.data(), b.p, b.bytes, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             if (FILE* f = fopen(path, "a")) {
@@ -1698,12 +1827,17 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
                     for (int j = 0; j < 2; ++j) fprintf(f, "%lld ", h[4096 * 14 + i * 2 + j]);
                     fprintf(f, "\n");
                 }
+                fprintf(f, "# cta start end stages smid\n");
+                for (int c = 0; c < 1024 && h[4096 * 16 + c * 4 + 1]; ++c)
+                    fprintf(f, "C %d %lld %lld %lld %lld\n", c, h[4096 * 16 + c * 4], h[4096 * 16 + c * 4 + 1],
+                            h[4096 * 16 + c * 4 + 2], h[4096 * 16 + c * 4 + 3]);
                 fclose(f);
             }
         }
     } dump{tbuf, tpath, st, a};
 #endif
     const bool tc = tc_ok(dt, a.k_total, a.n_total);
+    if (tc) a.sched = ctx->sched_slot();  // dynamic item queue (ItemSrc)
     int grid;
     if (a.mode != 1) grid = std::max(1, std::min(a.items, ctx->num_sms * (tc ? 1 : 8)));
     else grid = ctx->num_sms * (tc ? 1 : 8);

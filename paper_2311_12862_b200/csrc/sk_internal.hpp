@@ -1,5 +1,6 @@
 // sk200 internal object model behind the C ABI (include/sk200.h).
 #pragma once
+#include <atomic>
 
 #include "sk_common.cuh"
 
@@ -9,6 +10,13 @@ struct sk_ctx {
     bool deterministic = false;
     int kmap_block_rows = 1 << 19;  // sk_ctx_set_kmap_block_rows
     size_t smem_optin = 227 * 1024;
+    // dynamic work queues of the persistent conv kernels: kSchedSlots pairs
+    // {next item, CTAs done}, zeroed once; a launch takes the next slot and
+    // its last CTA re-zeroes it
+    static constexpr uint32_t kSchedSlots = 16384;
+    int* sched = nullptr;
+    std::atomic<uint32_t> sched_seq{0};
+    int* sched_slot() { return sched ? sched + 2 * (sched_seq.fetch_add(1) % kSchedSlots) : nullptr; }
 };
 
 namespace sk {
