@@ -58,11 +58,19 @@ typedef enum {
 /* ReorderMode (exec.hpp:60) */
 typedef enum { SK_REORDER_OFFLINE = 0, SK_REORDER_ONLINE = 1 } sk_reorder;
 
-/* TilePreset (exec.hpp:46-54) re-read for tcgen05:
- * cta_m = MMA M rows per tile (= pad multiple, 128), cta_n = C_out tile
- * (multiple of 16, <= 256; 0 = whole C_out), cta_k = channel step per
- * pipeline stage (16/32/64; 0 = auto), warp_rows = lockstep rows of the cost
- * model (= cta_m), load_width = rows per gather instruction. */
+/* TilePreset (exec.hpp:46-54) re-read for the tcgen05 gathered GEMM
+ * (SURVEY App. A.8); the tuner's space (sk_tune_space_entry) holds the
+ * reference's two presets plus the B200 variants below:
+ *   cta_m      128: 128-row MMA tiles in 256-row items, two CTAs per SM
+ *              (8 gather warps each) when C_out <= 128 and stages fit;
+ *              256: one CTA per SM (16 gather warps, ~200 KB of stages)
+ *   cta_n      C_out tile (multiple of 16, <= 256; 0 = whole C_out)
+ *   cta_k      channels per pipeline stage: 0 = auto (64/32/16 dividing
+ *              C_in; C_in = 96 as three 32-channel slabs), 16 / 32 / 64 =
+ *              that single-slab step when it divides C_in
+ *   warp_rows  lockstep rows of the cost model (traffic_model)
+ *   load_width 4 = cp.async row gathers (16 B per lane); 1 = TMA
+ *              tile::gather4 (one tensor-map gather per 4 rows) */
 typedef struct {
     int cta_m, cta_n, cta_k, warp_rows, load_width;
 } sk_tile;

@@ -99,6 +99,10 @@ struct ConvArgs {
     int exp;          // SK_CONV_TRACE builds: SK_EXP bits 1 no A gathers, 2 no zeroing, 4 no MMA, 8 no B TMA
     int offset_only;  // >= 0: WS mode only tiles of this offset
     int* sched;       // dynamic item queue {next item, CTAs done} (self-resetting), or null
+    // tile preferences from the layer's TilePreset (include/sk200.h):
+    int cta_m;        // 256: one CTA per SM; otherwise two per SM when C_out <= 128 fits
+    int cta_k;        // channels per pipeline stage: 0 auto, 16 / 32 / 64, 96 = 3 x 32 slabs
+    int tma_gather;   // load_width == 1: TMA tile::gather4 producers instead of cp.async
 };
 
 // one work item = 256 rows (OS: 128-row tiles 2*t2 and 2*t2+1 of split s;
@@ -1720,36 +1724,25 @@ void launch_tc_variant(const ConvArgs& a, const CUtensorMap& ta, const CUtensorM
 
 template <typename T, int KC>
 void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStream_t st) {
-    // cp.async measured faster than TMA gather4 for C <= 128 on B200
-    // (tools/layer_bench.py, profiles/r01_gather_paths.md); SK_GATHER=tma selects TMA
-    static const bool use_tma = [] {
-        const char* e = getenv("SK_GATHER");
-        return e && std::string(e) == "tma";
-    }();
-    // two CTAs per SM (8 producer warps, half the smem each) for C_out <= 128:
-    // the pipeline is paced by single-warp latency, so a second independent
-    // pipeline per SM overlaps it (SK_CONV_2CTA=0 disables)
-    static const bool two_cta = [] {
-        const char* e = getenv("SK_CONV_2CTA");
-        return !e || atoi(e) != 0;
-    }();
+    // Variant choice follows the layer's TilePreset (tuned per group; the
+    // defaults are the measured winners, profiles/r01_gather_paths.md,
+    // r01_gather_pipeline.md, r02_gather_redesign.md):
+    //  * gather: cp.async (default) or TMA tile::gather4 (load_width 1);
+    //  * two CTAs per SM (8 gather warps, ~100 KB of stages each) for
+    //    C_out <= 128 unless cta_m = 256 asks for one CTA (16 gather warps);
+    //  * C_in = 96 runs three 32-channel K-slabs per stage (one CTA per SM)
+    //    unless cta_k = 32 asks for single-slab stages.
+    constexpr int kMinSlabStages = 3;
     const int bn = a.bn;
-    const bool tma = use_tma || a.mode == 2;  // dense A always streams 2D TMA tiles
-    static const int min_stages = [] {
-        const char* e = getenv("SK_SLAB_MIN_STAGES");
-        return e ? std::max(1, atoi(e)) : 3;
-    }();
+    const bool tma = a.tma_gather || a.mode == 2;  // dense A always streams 2D TMA tiles
+    const bool two_cta = a.cta_m != 256;
     const int nchunks = (int)ceil_div(a.k_total, KC);
     const size_t slab_bytes = (size_t)kItemM * KC * 2 + (size_t)bn * KC * 2;
     CUtensorMap ta, tb;
     if (tma) ta = make_tmap(a.a, dt, a.k_total, a.n_rows_a, KC, a.mode == 2 ? kTileM : 1);
     else memset(&ta, 0, sizeof(ta));
     tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
-    static const bool slab3_ok = [] {  // SK_SLAB3=0: C = 96 takes the 2-CTA single-slab path
-        const char* e = getenv("SK_SLAB3");
-        return !e || atoi(e) != 0;
-    }();
-    const bool slab3 = slab3_ok && !tma && KC == 32 && nchunks == 3;  // C = 96: three-slab path wins
+    const bool slab3 = a.cta_k != 32 && !tma && KC == 32 && nchunks == 3;
     if (!tma && two_cta && bn <= 128 && !slab3) {
         // TMEM per CTA <= 256 columns: double-buffer only up to BN = 64
         const int acc_bufs = 4 * bn <= 256 ? 2 : 1;
@@ -1765,7 +1758,7 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStr
     // chunks pays (measured: C = 64/128 gain nothing, and SLABS stays a
     // compile-time constant so the single-slab kernel keeps its lean loops)
     const int slabs = (slab3 && ((size_t)bn * KC * 2) % 1024 == 0 &&
-                       (size_t)min_stages * 3 * slab_bytes <= 200 * 1024) ? 3 : 1;
+                       (size_t)kMinSlabStages * 3 * slab_bytes <= 200 * 1024) ? 3 : 1;
     const size_t stage_bytes = slabs * slab_bytes;
     int stages = (int)std::min<size_t>(kMaxStages, (200 * 1024) / stage_bytes);
     stages = std::max(stages, 2);
@@ -1778,8 +1771,13 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStr
 
 template <typename T>
 void launch_tc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStream_t st) {
-    if (a.k_total % 64 == 0) launch_tc_kc<T, 64>(a, dt, grid, num_sms, st);
-    else if (a.k_total % 32 == 0) launch_tc_kc<T, 32>(a, dt, grid, num_sms, st);
+    // channel step: the widest of 64 / 32 / 16 dividing C_in, or the
+    // preset's cta_k when it divides C_in
+    const int k = a.k_total;
+    const int pref = (a.cta_k == 16 || a.cta_k == 32 || a.cta_k == 64) && k % a.cta_k == 0 ? a.cta_k : 0;
+    const int kc = pref ? pref : (k % 64 == 0 ? 64 : (k % 32 == 0 ? 32 : 16));
+    if (kc == 64) launch_tc_kc<T, 64>(a, dt, grid, num_sms, st);
+    else if (kc == 32) launch_tc_kc<T, 32>(a, dt, grid, num_sms, st);
     else launch_tc_kc<T, 16>(a, dt, grid, num_sms, st);
 }
 
@@ -2064,6 +2062,9 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     a.mirror = dgrad ? 1 : 0;
     a.ld_y = n_total;
     pick_n_tiling(n_total, cfg.tile.cta_n, tc, a.bn, a.n_ntiles);
+    a.cta_m = cfg.tile.cta_m;
+    a.cta_k = cfg.tile.cta_k;
+    a.tma_gather = cfg.tile.load_width == 1 ? 1 : 0;
     const bool det = ctx->deterministic;
 
     if (m->identity && tc && !det &&

@@ -876,11 +876,7 @@ __global__ void k_iota(int* __restrict__ v, int n) {
 // load factor <= 1/4: short linear-probing chains keep warps convergent (a
 // warp waits for its longest chain); 16 B slots -> 64 n..128 n bytes, L2-resident
 int64_t pow2_cap(int64_t n) {
-    // slots per key (load factor 1/m); SK_HASH_SLOTS overrides for experiments
-    static const int64_t m = [] {
-        const char* e = getenv("SK_HASH_SLOTS");
-        return e ? std::max<int64_t>(2, atoll(e)) : 4;
-    }();
+    constexpr int64_t m = 4;  // slots per key (load factor 1/4; 1/2 measured 1.6x slower, r02_kmap.md)
     int64_t c = 64;
     while (c < m * n) c <<= 1;
     return c;

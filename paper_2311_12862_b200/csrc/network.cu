@@ -569,14 +569,6 @@ void run_layers(sk_net* n, const void* feats, int channels, cudaStream_t st,
     }
 }
 
-bool overlap_maps() {
-    static const bool v = [] {
-        const char* e = getenv("SK_NET_OVERLAP");
-        return !e || atoi(e) != 0;
-    }();
-    return v;
-}
-
 void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cudaStream_t st,
                  std::vector<double>* map_ms, std::vector<double>* ker_ms,
                  std::vector<double>* layer_ms = nullptr) {
@@ -584,7 +576,7 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
              "network input channel count does not match the first layer");
     const size_t L = n->spec.layers.size();
     const bool cached = maps_complete(n, root);
-    if (cached || map_ms || !overlap_maps() || !n->overlap) {
+    if (cached || map_ms || !n->overlap) {
         ensure_maps(n, root, st, map_ms);
         alloc_outputs(n, st);
         refresh_wt(n, st);
@@ -807,7 +799,11 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
 }
 
 // ---- tuner (tuner.cpp) ----
-std::vector<sk_dataflow_cfg> default_space() {  // tuner.cpp:9-26 (12 entries)
+// tuner.cpp:9-26's 12 entries, then the B200 kernel variants the reference's
+// presets cannot name (include/sk200.h sk_tile): one CTA per SM (cta_m 256),
+// TMA tile::gather4 producers (load_width 1) and single-slab 32-channel
+// stages (cta_k 32) for the sorted implicit GEMM at 1-2 splits
+std::vector<sk_dataflow_cfg> default_space() {
     std::vector<sk_dataflow_cfg> sp;
     sk_dataflow_cfg c = default_cfg();
     sp.push_back(c);
@@ -821,6 +817,20 @@ std::vector<sk_dataflow_cfg> default_space() {  // tuner.cpp:9-26 (12 entries)
             ig.tile.cta_n = large ? 0 : 64;  // tile_large = whole C_out per tile
             sp.push_back(ig);
         }
+    for (int s = 1; s <= 2; ++s) {
+        sk_dataflow_cfg ig = default_cfg();
+        ig.kind = SK_IMPLICIT_GEMM;
+        ig.splits = s;
+        ig.tile.cta_n = 0;
+        ig.tile.cta_m = 256;  // one CTA per SM, 16 gather warps
+        sp.push_back(ig);
+        ig.tile.cta_m = 128;
+        ig.tile.load_width = 1;  // TMA tile::gather4
+        sp.push_back(ig);
+        ig.tile.load_width = 4;
+        ig.tile.cta_k = 32;  // single-slab 32-channel stages
+        sp.push_back(ig);
+    }
     return sp;
 }
 

@@ -353,7 +353,15 @@ class DataflowConfig:
     def name(self) -> str:  # DataflowConfig::name (exec.cpp:61-69)
         s = _KIND_NAMES[self.kind]
         if self.kind == IMPLICIT_GEMM:
-            s += f"_s{self.splits}" + ("_large" if self.tile == tile_large() else "_small")
+            t = self.tile
+            if t == tile_large():
+                tn = "_large"
+            elif t == tile_small():
+                tn = "_small"
+            else:  # B200 kernel variants (include/sk200.h sk_tile)
+                tn = (f"_m{t.cta_m}" + (f"n{t.cta_n}" if t.cta_n else "") +
+                      (f"k{t.cta_k}" if t.cta_k else "") + ("_tma" if t.load_width == 1 else ""))
+            s += f"_s{self.splits}" + tn
             s += "_online" if self.reorder else "_offline"
         return s
 

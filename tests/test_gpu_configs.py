@@ -59,11 +59,9 @@ def env():
 
 
 def all_configs(sk):
-    out = [sk.DataflowConfig(sk.GATHER_GEMM_SCATTER), sk.DataflowConfig(sk.FETCH_ON_DEMAND)]
-    for s in range(5):
-        for t in (sk.tile_small(), sk.tile_large()):
-            out.append(sk.DataflowConfig(sk.IMPLICIT_GEMM, s, t))
-    return out
+    """The tuner's space: the 12 default_space entries plus the B200 variants."""
+    from paper_2311_12862_b200.network import default_space
+    return default_space()
 
 
 def assert_map_equal(gpu_map, ref_map, what):

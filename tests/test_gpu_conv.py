@@ -42,10 +42,17 @@ def make(sk, torch, seed, n, stride, k=3, rng=20):
 
 
 def configs(sk):
-    out = [sk.DataflowConfig(sk.GATHER_GEMM_SCATTER), sk.DataflowConfig(sk.FETCH_ON_DEMAND)]
+    """The tuner's whole space: the reference's 12 entries (tuner.cpp:9-26)
+    plus the B200 kernel variants (one CTA per SM, TMA gather4 producers,
+    single-slab 32-channel stages), so every variant the tuner may pick is
+    checked against the oracle."""
+    from paper_2311_12862_b200.network import default_space
+    out = default_space()
+    ref = [sk.DataflowConfig(sk.GATHER_GEMM_SCATTER), sk.DataflowConfig(sk.FETCH_ON_DEMAND)]
     for s in range(5):
         for t in (sk.tile_small(), sk.tile_large()):
-            out.append(sk.DataflowConfig(sk.IMPLICIT_GEMM, s, t))
+            ref.append(sk.DataflowConfig(sk.IMPLICIT_GEMM, s, t))
+    assert out[:12] == ref and len(out) > 12
     return out
 
 
