@@ -19,6 +19,8 @@
 //    with a CUDA-event RunnerProbe (warmup 2, median of 5, tuner.cpp:50-60);
 //    ties break on the traffic model (cost.cpp:47-93) then space order.
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <atomic>
 #include <mutex>
 #include <cstring>
@@ -274,6 +276,65 @@ void by_dtype(sk_dtype dt, F&& f) {
 
 using namespace sk;
 
+namespace sk {
+// The runner's map-builder thread (overlapped forward), created on first use
+// and kept for the runner's lifetime: one job per forward. After a job it
+// polls for the next one for a short while (back-to-back scans hand over in
+// microseconds), then sleeps on a condition variable; spawning a thread per
+// forward cost ~40 us of host latency before the first map kernel.
+struct MapWorker {
+    std::thread t;
+    std::mutex mu;
+    std::condition_variable cv, cv_done;
+    std::function<void()> job;
+    std::atomic<bool> pending{false};
+    bool stop = false;
+    void post(std::function<void()> j) {
+        if (!t.joinable()) t = std::thread([this] { loop(); });
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            job = std::move(j);
+            pending.store(true, std::memory_order_release);
+        }
+        cv.notify_one();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_done.wait(lk, [&] { return !pending.load(std::memory_order_acquire); });
+    }
+    void loop() {
+        for (;;) {
+            const auto until = std::chrono::steady_clock::now() + std::chrono::microseconds(500);
+            while (!pending.load(std::memory_order_acquire) &&
+                   std::chrono::steady_clock::now() < until)
+                std::this_thread::yield();
+            std::function<void()> j;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return stop || pending.load(std::memory_order_acquire); });
+                if (!pending.load(std::memory_order_acquire)) return;  // stop
+                j = std::move(job);
+            }
+            j();
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                pending.store(false, std::memory_order_release);
+            }
+            cv_done.notify_all();
+        }
+    }
+    ~MapWorker() {
+        if (!t.joinable()) return;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_one();
+        t.join();
+    }
+};
+}  // namespace sk
+
 struct sk_net {
     sk_ctx* ctx = nullptr;
     NetSpec spec;
@@ -304,8 +365,10 @@ struct sk_net {
     cudaStream_t map_stream = nullptr;        // overlapped map builds (run_forward)
     cudaStream_t cmp_stream = nullptr;        // overlapped forward's convs for legacy-stream callers
     std::vector<cudaEvent_t> map_ready;       // per layer: its maps are built on map_stream
+    std::unique_ptr<sk::MapWorker> worker;    // overlapped map builder (run_forward)
 
     ~sk_net() {
+        worker.reset();  // no job can be running: run_forward waits for its job
         clear_state();
         for (auto e : map_ready) cudaEventDestroy(e);
         // cached maps / sets built here still name these streams (BuiltOn
@@ -618,7 +681,9 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     std::atomic<bool> failed{false};
     std::exception_ptr err;
     const int dev = n->ctx->device;
-    std::thread builder([&] {
+    if (!n->worker) n->worker = std::make_unique<MapWorker>();
+    MapWorker* builder = n->worker.get();
+    builder->post([&] {
         try {
             SK_CUDA(cudaSetDevice(dev));
             for (size_t i = 0; i < L; ++i) {
@@ -634,11 +699,9 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
             failed.store(true, std::memory_order_release);
         }
     });
-    struct Join {
-        std::thread& t;
-        ~Join() {
-            if (t.joinable()) t.join();
-        }
+    struct Join {  // the job references this frame: wait for it on every exit path
+        MapWorker* w;
+        ~Join() { w->wait(); }
     } join{builder};
     refresh_wt(n, st);
     n->out.resize(L);
@@ -648,7 +711,7 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     run_layers(n, feats, channels, st, ker_ms, layer_ms, [&](size_t i) {
         while (done.load(std::memory_order_acquire) <= i) {
             if (failed.load(std::memory_order_acquire)) {
-                builder.join();
+                builder->wait();
                 std::rethrow_exception(err);
             }
             std::this_thread::yield();
@@ -656,7 +719,7 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
         SK_CUDA(cudaStreamWaitEvent(st, n->map_ready[i], 0));
         alloc_layer_output(n, i, st);
     });
-    builder.join();
+    builder->wait();
     if (err) std::rethrow_exception(err);
     if (legacy) {  // the caller's stream continues after the convs
         SK_CUDA(cudaEventRecord(n->map_ready[L + 1], st));

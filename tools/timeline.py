@@ -69,6 +69,14 @@ def main():
             else:
                 cur_e = max(cur_e, e)
         busy += cur_e - cur_s
+        # gaps > 3 us with the kernels around them
+        gl, end_max, prev = [], None, None
+        for s_, e_, n in iv:
+            if end_max is not None and s_ - end_max > 3:
+                short = lambda x: x.replace("void ", "").replace("sk::(anonymous namespace)::", "").split("<")[0].split("(")[0][:24]
+                gl.append((round(s_ - end_max, 1), short(prev), short(n), round(end_max - t0, 1)))
+            if end_max is None or e_ > end_max:
+                end_max, prev = e_, n
         cls = {}
         for s, e, n in iv:
             c = classify(n)
@@ -78,8 +86,9 @@ def main():
             k = n.replace("void ", "").replace("sk::(anonymous namespace)::", "").replace("sk::", "")
             k = k.split("<")[0].split("(")[0][-40:]
             names[k] = names.get(k, 0.0) + (e_ - s_)
+        ms = sorted(round(e_ - s_, 1) for s_, e_, n in iv if "Memset" in n)
         gaps = np.array(gaps) if gaps else np.zeros(1)
-        r = {"span_us": t1 - t0, "busy_us": busy, "idle_us": (t1 - t0) - busy,
+        r = {"gap_list": gl, "memsets_us": ms, "span_us": t1 - t0, "busy_us": busy, "idle_us": (t1 - t0) - busy,
              "kernels": len(iv), "gaps_over_5us": int((gaps > 5).sum()),
              "largest_gaps_us": sorted(gaps.tolist())[-8:], "by_class_us": cls,
              "by_kernel_us": dict(sorted(((k, round(v, 1)) for k, v in names.items()),
