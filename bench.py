@@ -490,6 +490,27 @@ def run_train(args, rank, world, local):
         scenes = [(sk.CoordSet.create(c), x, t) for c, x, t in prepared[i]]
         return tr.train_step(scenes, B)
 
+    # e2e: the same steps from pinned HOST scans (coords, feats, targets) copied
+    # in every step and the loss read back every step
+    host = [[(c.cpu().pin_memory(), x.cpu().pin_memory(), t.cpu().pin_memory()) for c, x, t in pb]
+            for pb in prepared]
+    dev_slots = [[(torch.empty_like(c, device="cuda"), torch.empty_like(x, device="cuda"),
+                   torch.empty_like(t, device="cuda")) for c, x, t in pb] for pb in host]
+    h2d_bytes = [sum(c.numel() * c.element_size() + x.numel() * x.element_size() +
+                     t.numel() * t.element_size() for c, x, t in pb) for pb in host]
+    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
+
+    def step_e2e(i):
+        scenes = []
+        for (hc, hx, ht), (dc_, dx_, dt_) in zip(host[i], dev_slots[i]):
+            dc_.copy_(hc, non_blocking=True)
+            dx_.copy_(hx, non_blocking=True)
+            dt_.copy_(ht, non_blocking=True)
+            scenes.append((sk.CoordSet.create(dc_), dx_, dt_))
+        loss = tr.train_step(scenes, B)
+        loss_host.copy_(loss.float(), non_blocking=True)
+        return loss
+
     # warm pass over every batch: the torch allocator (loss temporaries, per
     # replica stream) and the block cache see every size class before the
     # timed steps (a cudaMalloc mid-window stalls the whole device)
@@ -507,13 +528,55 @@ def run_train(args, rank, world, local):
         step(i)
     b.record()
     torch.cuda.synchronize()
+    launches1 = _lib.lib().sk_kernel_launches()
     clk = clocks.stop()
     t_ms = a.elapsed_time(b)
+    # e2e window (host data in, loss out, every step)
+    for i in range(min(2, args.warmup)):
+        step_e2e(i)
+    torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([t_ms], device="cuda")
+        dist.barrier()
+    torch.cuda.synchronize()
+    a.record()
+    for i in range(args.warmup, args.warmup + args.steps):
+        step_e2e(i)
+    b.record()
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([t_ms, e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
+        t_ms, e2e_ms = float(t[0].item()), float(t[1].item())
     value = B * args.steps / (t_ms / 1e3)
+    # roofline: every conv's algorithmic fwd + dgrad + wgrad FLOPs
+    # (3 x 2 * pairs * C_in * C_out per scan) over the whole step, against the
+    # sustained bf16 peak (a step is seconds-long at the power cap)
+    pk = peaks()
+    step_flops = 0.0
+    for c, _x, _t in prepared[args.warmup]:
+        cs = sk.CoordSet.create(c)
+        pr = layer_pairs(sk, net, cs)
+        step_flops += sum(3 * 2.0 * pr[i] * l.c_in * l.c_out for i, l in enumerate(net.layers))
+    step_flops *= world  # every rank's scenes of the global batch (weak: B fixed)
+    peak_s = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    ach = step_flops / (t_ms / args.steps * 1e-3) / 1e12
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        c0, x0, _ = prepared[args.warmup][0]
+        from oracle.oracle import Reference
+        from paper_2311_12862_b200.models import spec_text
+        ref = Reference()
+        rn = ref.network(3, spec_text(minkunet18()), prec=0, threads=threads, weight_seed=3)
+        rn.set_input(c0.cpu().numpy(), x0.float().cpu().numpy().astype(np.float64), prec=0)
+        t0 = time.perf_counter()
+        rn.measure(fwd=True, dgrad=True, wgrad=True)
+        sec = time.perf_counter() - t0
+        cpu = {"value": 1.0 / sec, "unit": "scans/s", "cores": threads, "kind": "reference",
+               "cpu_model": cpu_model(),
+               "sample": "1 scan: compiled reference NetworkRunner::measure_ms (forward + dgrad "
+                         "+ wgrad sweeps, f32, default GGS) on the first timed batch's first scan"}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "scans/s", "n_gpus": world,
@@ -528,7 +591,17 @@ def run_train(args, rank, world, local):
                                       "CUDA streams), gradients folded before the last scene",
                        "params": int(net.num_params),
                        "dataflow": tuned if tuned else "implicit_gemm s1 (all groups, untuned)"},
-            "gpu_launches": int(_lib.lib().sk_kernel_launches() - launches0),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_s, "unit": "TFLOP/s",
+                         "frac": ach / peak_s, "traffic": None,
+                         "kernel": "whole training step: every conv's fwd + dgrad + wgrad "
+                                   "(3 x 2*pairs*C_in*C_out per scan), all kernels in the step",
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": B * args.steps / (e2e_ms / 1e3), "unit": "scans/s",
+                    "h2d_bytes_per_step": int(h2d_bytes[args.warmup]), "d2h_bytes_per_step": 4,
+                    "path": "pinned host coords / feats / targets -> device every step, "
+                            "CoordSet.create + DataParallelTrainer.train_step, loss -> pinned host"},
+            "gpu_launches": int(launches1 - launches0),
             "clocks": clk}), flush=True)
     if world > 1:
         dist.barrier()
