@@ -20,20 +20,33 @@
 //    mirrored offset and B = W[k'] read as [c_in][c_out] (already K-major);
 //    forward uses B = W^T (a tiny per-call transpose to [k][c_out][c_in]).
 //
-// fp16/bf16 -> k_gconv_tc: warp-specialised, persistent tcgen05 kernel
-//   warps 0-3  producers: warp w owns rows [32w, 32w+32) of the 128-row A
-//              tile and issues its 8 TMA tile::gather4 (4 rows each) from a
-//              single thread (uniform operands); sentinel rows -> out-of-
-//              bounds coordinate -> TMA zero fill. Warp 0 also loads the B
-//              tile (2D TMA). Stages are 128B/64B/32B-swizzled K-major and
-//              complete on one mbarrier (expect_tx). Row indices arrive by
-//              128B cp.async.bulk into a per-warp 16-slot smem ring,
-//              prefetched up to 8 column steps ahead.
-//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer (M=128,
-//              N=BN, K=16 per instruction); tcgen05.commit frees stages
-//   warps 5-8  epilogue: tcgen05.ld 32x32b -> registers -> global, double-
-//              buffered TMEM accumulators so tile i's epilogue overlaps tile
-//              i+1's MMAs
+// fp16/bf16 -> k_gconv_tc: warp-specialised, persistent tcgen05 kernel over
+// 256-row work items (two 128-row MMA halves sharing each B stage). Default
+// (cp.async) roles, PW = 16 gather warps at one CTA per SM or 8 at two:
+//   warps 0..PW-1  producers: warp w gathers only the REAL rows of its
+//                  256/PW rows (compacted lists), 16 B cp.async into
+//                  128/64/32 B-swizzled K-major stages, completion via
+//                  cp.async.mbarrier.arrive.noinc; warp 0 also loads the B
+//                  tile (2D TMA, expect_tx)
+//   warp PW        TMEM allocator + tcgen05.mma issuer (M=128 x 2 halves,
+//                  N = C_out tile <= 256, K=16; elect.sync inside the asm),
+//                  tcgen05.commit frees stages
+//   warp PW+1      index warp: takes work items from the dynamic item queue
+//                  (ItemSrc), walks their active columns (tile OR-masks),
+//                  streams each column step's 256 row indices into an 8-slot
+//                  smem ring (cp.async.bulk) and compacts them into the
+//                  producers' real-row lists one step behind
+//   warps PW+2..3  zero warps: st.shared zeros only for sentinel rows that
+//                  still hold data from the stage's previous use
+//   warps PW+4..7  epilogue: tcgen05.ld 32x32b -> registers -> fp16 store /
+//                  fp32 red.add / RMW (+ fused skip add); double-buffered TMEM
+//                  accumulators so item i's epilogue overlaps item i+1's MMAs
+// The TilePreset picks the variant (launch_tc_kc): cta_m 256 = one CTA per
+// SM, cta_k = channels per stage (C_in = 96: three 32-channel slabs),
+// load_width 1 = TMA tile::gather4 producers (4 warps, one gather per 4 rows,
+// sentinel rows -> out-of-bounds coordinate -> zero fill).
+// Measured limits and rejected designs: profiles/r01_gather_pipeline.md,
+// r01_gather_paths.md, r02_gather_redesign.md.
 // fp32 -> k_gconv_simt: the 1e-5 parity path (FFMA, fp32 accumulate).
 #include <cuda.h>
 #include <cstdio>
