@@ -8,7 +8,7 @@
 //    quantize; kmap.cpp:80-88, tensor.cpp:87-142).
 //
 //  * radix_sort_pairs: stable LSD radix sort of (key, int value) pairs with
-//    up-to-11-bit digits (split_and_sort's stable mask sort, kmap.cpp:252-256;
+//    up-to-10-bit digits (split_and_sort's stable mask sort, kmap.cpp:252-256;
 //    the graph maps' stable (relation, dst) order, kmap.cpp:317-336). One
 //    histogram launch computes every pass's global digit counts; then ONE
 //    launch per pass ("onesweep"): each 2048-key tile ranks its keys stably
@@ -16,7 +16,7 @@
 //    publishes its per-digit counts and looks back over the earlier tiles'
 //    counts (decoupled look-back) to find its output offsets. A 27-bit split
 //    mask key sorts in 3 passes (CUB's 8-bit onesweep: 4), a split-local key
-//    of <= 11 bits (3+ splits at K=3) in one.
+//    of <= 11 bits (3+ splits at K=3) in two of <= 6 bits.
 #include "sk_internal.hpp"
 
 namespace sk {
@@ -126,8 +126,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int* __res
 
 // ---- radix sort ------------------------------------------------------------
 constexpr int kRsThreads = 256, kRsWarps = 8, kRsIpt = 8, kRsTile = kRsThreads * kRsIpt;
-constexpr int kRsMaxBits = 11, kRsMaxPasses = 6;
-constexpr int kLookBatch = 16;
+// 10-bit digits: 27-bit masks in 3 passes, 3-4 split keys (<= 11 bits) in 2
+// passes of <= 6 bits rather than one of 11 (measured, tools/prep_bench.py:
+// 1024+-digit look-backs made the single pass the slowest: s=3 prepare 70.6
+// -> 52.2 us, s=1 65.5 -> 64.5 us)
+constexpr int kRsMaxBits = 10, kRsMaxPasses = 8;
+constexpr int kLookBatch = 16;  // 32 / 64 measured slower (register pressure)
 
 template <typename KT>
 __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const KT* __restrict__ keys, int n,
@@ -276,7 +280,7 @@ RadixPlan radix_plan(int n, int bits) {
     RadixPlan r;
     r.bits = bits;
     r.passes = bits > 0 ? (int)ceil_div(bits, kRsMaxBits) : 0;
-    if (r.passes > kRsMaxPasses) fail(SK_ERR_VALIDATION, "radix sort key wider than 66 bits");
+    if (r.passes > kRsMaxPasses) fail(SK_ERR_VALIDATION, "radix sort key wider than 80 bits");
     if ((long long)n >= (1ll << 30)) fail(SK_ERR_VALIDATION, "radix sort: too many keys");
     r.dbits = r.passes ? (int)ceil_div(bits, r.passes) : 0;
     r.digits = 1 << r.dbits;
