@@ -279,6 +279,14 @@ int64_t sk_net_map_builds(const sk_net* net);
  * (they fill each other's sync bubbles). No reference counterpart (sk200
  * runtime). */
 sk_status sk_net_set_overlap(sk_net* net, int on);
+/* Programmatic dependent launch (default on): every kernel of the runner's
+ * calls is launched with programmatic stream serialization, so its launch
+ * and prologue overlap the previous kernel's tail (griddepcontrol.wait
+ * before it touches memory): -5 % single-scan latency on MinkUNet. Turn off
+ * when several runners share the GPU: early-resident CTAs waiting on their
+ * predecessor hold shared memory other streams' kernels could use (-7 %
+ * scans/s at 6 in flight). No reference counterpart (sk200 runtime). */
+sk_status sk_net_set_pdl(sk_net* net, int on);
 /* modeled_group_traffic (network.cpp:453-471) */
 sk_status sk_net_group_traffic(sk_net* net, int group, const sk_dataflow_cfg* cfg, void* stream,
                                double* bytes);

@@ -35,6 +35,10 @@ std::atomic<unsigned long long>& launch_counter() {
     static std::atomic<unsigned long long> c{0};
     return c;
 }
+bool& pdl_enabled() {
+    thread_local bool on = true;
+    return on;
+}
 
 void stream_after(const BuiltOn& on, cudaStream_t st) {
     if (!on.set || on.s == st) return;
@@ -132,6 +136,8 @@ struct RbArgs {
     int n;
 };
 __global__ void k_read_back(RbArgs a, volatile uint8_t* dst) {
+    pdl_wait();
+    pdl_trigger();
     int o = 0;
     for (int k = 0; k < a.n; ++k) {
         for (int i = threadIdx.x; i < a.bytes[k]; i += blockDim.x) dst[o + i] = a.src[k][i];
@@ -168,8 +174,7 @@ void read_back(cudaStream_t st, std::initializer_list<RbSeg> segs, void* dst) {
     validate(total <= (size_t)kRbSlotBytes, "read_back: too many bytes");
     Mapped& m = mapped();
     const unsigned slot = m.next.fetch_add(1) % kRbSlots;
-    k_read_back<<<1, 32, 0, st>>>(a, m.d + slot * kRbSlotBytes);
-    SK_LAUNCH_CHECK();
+    launch_pdl(k_read_back, 1, 32, 0, st, a, m.d + slot * kRbSlotBytes);
     SK_CUDA(cudaStreamSynchronize(st));
     memcpy(dst, m.h + slot * kRbSlotBytes, total);
 }

@@ -510,6 +510,8 @@ template <typename T, int KC, bool USE_TMA, int SLABS, int PW>
 __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
     k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const ConvArgs p, int stages, int acc_bufs) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int kProducerWarps = Roles<PW>::kProducerWarps;
     constexpr int kGroupRows = Roles<PW>::kGroupRows;
     constexpr int kMmaWarp = Roles<PW>::kMmaWarp;
@@ -1162,6 +1164,8 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float As[kSimtK][kTileM + 4];
     __shared__ float Bs[kSimtK][kSimtN + 4];
     __shared__ int aidx[kTileM];
@@ -1248,6 +1252,8 @@ __global__ void __launch_bounds__(256) k_gconv_simt(const ConvArgs p) {
 template <typename T>
 __global__ void k_transpose_w(const T* __restrict__ w, int kd, int c_in, int c_out,
                               T* __restrict__ wt) {
+    pdl_wait();
+    pdl_trigger();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long tot = (long long)kd * c_in * c_out;
     if (i >= tot) return;
@@ -1260,6 +1266,8 @@ __global__ void k_transpose_w(const T* __restrict__ w, int kd, int c_in, int c_o
 template <typename T>
 __global__ void k_convert_out(const float* __restrict__ src, long long n, T* __restrict__ dst,
                               const T* __restrict__ res) {
+    pdl_wait();
+    pdl_trigger();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = from_f<T>(src[i] + (res ? to_f(res[i]) : 0.f));
 }
@@ -1269,6 +1277,8 @@ __global__ void k_convert_out(const float* __restrict__ src, long long n, T* __r
 template <typename T>
 __global__ void k_pad_cols(const T* __restrict__ src, long long rows, int k, int k_pad,
                            T* __restrict__ dst) {
+    pdl_wait();
+    pdl_trigger();
     const long long n = rows * k_pad;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -1282,6 +1292,8 @@ __global__ void k_pad_cols(const T* __restrict__ src, long long rows, int k, int
 template <typename T>
 __global__ void k_gather_rows(const T* __restrict__ x, int c, const int* __restrict__ idx,
                               const int* __restrict__ tile_total, T* __restrict__ buf) {
+    pdl_wait();
+    pdl_trigger();
     const long long nelem = (long long)(*tile_total) * kItemM * c;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
          i += (long long)gridDim.x * blockDim.x) {
@@ -1298,6 +1310,8 @@ __global__ void k_gather_rows(const T* __restrict__ x, int c, const int* __restr
 __global__ void k_scatter_add(const float* __restrict__ buf, int c, const int* __restrict__ idx,
                               const int* __restrict__ tile_lo, const int* __restrict__ tile_hi,
                               float* __restrict__ y, int deterministic) {
+    pdl_wait();
+    pdl_trigger();
     const long long a = (long long)(*tile_lo) * kItemM, b = (long long)(*tile_hi) * kItemM;
     const long long nelem = (b - a) * c;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nelem;
@@ -1329,6 +1343,8 @@ __global__ void __launch_bounds__(256) k_wgrad_small_cin(const T* __restrict__ x
                                                          const int* __restrict__ ws_in,
                                                          const int* __restrict__ ws_out, int chunk,
                                                          float* __restrict__ dw) {
+    pdl_wait();
+    pdl_trigger();
     const int k = blockIdx.z;
     const long long b = ptr[k], e = ptr[k + 1];
     const long long p0 = b + (long long)blockIdx.x * chunk;
@@ -1388,6 +1404,8 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
                                                     const int* __restrict__ ws_in,
                                                     const int* __restrict__ ws_out, int chunk,
                                                     double* __restrict__ dw) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float xs[32][33];
     __shared__ float ds[32][33];
     const int k = blockIdx.z;
@@ -1425,6 +1443,8 @@ __global__ void __launch_bounds__(256) k_wgrad_simt(const T* __restrict__ x,
 // dw (fp32) = [dw +] dw64, rounded once
 __global__ void k_round_f64(const double* __restrict__ src, long long n, float* __restrict__ dw,
                             int accumulate) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         dw[i] = accumulate ? (float)((double)dw[i] + src[i]) : (float)src[i];
@@ -1467,6 +1487,8 @@ __device__ __forceinline__ int wg_offset_of(const int* tp, int kd, int t) {
 
 template <typename T>
 __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int stages) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t a_bytes = 2 * 8192;                   // 128 channels x 64 pairs
     const uint32_t b_bytes = (uint32_t)p.nblk_b * 8192;  // bn channels (64-blocks) x 64 pairs
@@ -1731,8 +1753,7 @@ void launch_tc_variant(const ConvArgs& a, const CUtensorMap& ta, const CUtensorM
                         kIdxRing * sizeof(CSlot<PW>);
     auto kern = k_gconv_tc<T, KC, TMA, SLABS, PW>;
     ensure_smem(reinterpret_cast<const void*>(kern), smem);
-    kern<<<grid, Roles<PW>::kThreads, smem, st>>>(ta, tb, a, stages, acc_bufs);
-    SK_LAUNCH_CHECK();
+    launch_pdl(kern, grid, Roles<PW>::kThreads, smem, st, ta, tb, a, stages, acc_bufs);
 }
 
 template <typename T, int KC>
@@ -1856,19 +1877,17 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
         if (dt == SK_F16) launch_tc<__half>(a, dt, grid, ctx->num_sms, st);
         else launch_tc<__nv_bfloat16>(a, dt, grid, ctx->num_sms, st);
     } else {
-        if (dt == SK_F32) k_gconv_simt<float><<<grid, 256, 0, st>>>(a);
-        else if (dt == SK_F16) k_gconv_simt<__half><<<grid, 256, 0, st>>>(a);
-        else k_gconv_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(a);
-        SK_LAUNCH_CHECK();
+        if (dt == SK_F32) launch_pdl(k_gconv_simt<float>, grid, 256, 0, st, a);
+        else if (dt == SK_F16) launch_pdl(k_gconv_simt<__half>, grid, 256, 0, st, a);
+        else launch_pdl(k_gconv_simt<__nv_bfloat16>, grid, 256, 0, st, a);
     }
 }
 
 template <typename T>
 void convert_out(const float* src, long long n, void* dst, const void* res, cudaStream_t st) {
     if (n <= 0) return;
-    k_convert_out<T><<<(int)ceil_div(n, 256), 256, 0, st>>>(src, n, static_cast<T*>(dst),
+    launch_pdl(k_convert_out<T>, (int)ceil_div(n, 256), 256, 0, st, src, n, static_cast<T*>(dst),
                                                               static_cast<const T*>(res));
-    SK_LAUNCH_CHECK();
 }
 
 // fp32 accumulator -> output dtype (+ fused residual)
@@ -1883,9 +1902,7 @@ template <typename T>
 void pad_cols(const void* src, long long rows, int k, int k_pad, void* dst, cudaStream_t st) {
     const long long n = rows * k_pad;
     if (n <= 0) return;
-    k_pad_cols<T><<<(int)std::min<long long>(ceil_div(n, 256), 148 * 32), 256, 0, st>>>(
-        static_cast<const T*>(src), rows, k, k_pad, static_cast<T*>(dst));
-    SK_LAUNCH_CHECK();
+    launch_pdl(k_pad_cols<T>, (int)std::min<long long>(ceil_div(n, 256), 148 * 32), 256, 0, st, static_cast<const T*>(src), rows, k, k_pad, static_cast<T*>(dst));
 }
 
 // Implicit GEMM on CUDA cores for tiny C_in (<= 8, the 4-channel stem):
@@ -1897,6 +1914,8 @@ template <typename T, int CI, int CO>
 __global__ void __launch_bounds__(256) k_conv_small_cin(
     const int* __restrict__ os, int n_out, int kd, const T* __restrict__ x, const T* __restrict__ w,
     T* __restrict__ y, const T* __restrict__ residual, float* __restrict__ y_accum) {
+    pdl_wait();
+    pdl_trigger();
     // persistent blocks: W staged once per block as fp32; 4 threads per output
     // row, each owning CO/4 output channels (latency hiding + short tails)
     constexpr int KD = 27, TPR = 4, CQ = CO / TPR;
@@ -1959,10 +1978,8 @@ bool conv_small_cin(const sk_kmap* m, int c_in, int c_out, const void* x, const 
         const size_t smem = (size_t)m->kd * c_in * c_out * 4;
         ensure_smem(reinterpret_cast<const void*>(kern), smem);
         const int grid = (int)std::min<int64_t>(ceil_div(m->n_out, 64), (int64_t)m->ctx->num_sms * 8);
-        kern<<<grid, 256, smem, st>>>(
-            m->os.as<int>(), m->n_out, m->kd, static_cast<const T*>(x), static_cast<const T*>(w),
+        launch_pdl(kern, grid, 256, smem, st, m->os.as<int>(), m->n_out, m->kd, static_cast<const T*>(x), static_cast<const T*>(w),
             static_cast<T*>(y), static_cast<const T*>(residual), y_accum);
-        SK_LAUNCH_CHECK();
         return true;
     };
     if (m->kd > 27) return false;
@@ -1983,9 +2000,8 @@ ConvArgs base_args() {
 template <typename T>
 void gather_rows(const void* x, int c, const int* idx, const int* tiles, void* buf, int g,
                  cudaStream_t st) {
-    k_gather_rows<T><<<g, 256, 0, st>>>(static_cast<const T*>(x), c, idx, tiles,
+    launch_pdl(k_gather_rows<T>, g, 256, 0, st, static_cast<const T*>(x), c, idx, tiles,
                                         static_cast<T*>(buf));
-    SK_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -2040,10 +2056,9 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         wt.alloc((size_t)m->kd * c_in * c_out * es, st);
         long long tot = (long long)m->kd * c_in * c_out;
         const int g = (int)ceil_div(tot, 256);
-        if (dt == SK_F32) k_transpose_w<float><<<g, 256, 0, st>>>((const float*)w, m->kd, c_in, c_out, wt.as<float>());
-        else if (dt == SK_F16) k_transpose_w<__half><<<g, 256, 0, st>>>((const __half*)w, m->kd, c_in, c_out, wt.as<__half>());
-        else k_transpose_w<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)w, m->kd, c_in, c_out, wt.as<__nv_bfloat16>());
-        SK_LAUNCH_CHECK();
+        if (dt == SK_F32) launch_pdl(k_transpose_w<float>, g, 256, 0, st, (const float*)w, m->kd, c_in, c_out, wt.as<float>());
+        else if (dt == SK_F16) launch_pdl(k_transpose_w<__half>, g, 256, 0, st, (const __half*)w, m->kd, c_in, c_out, wt.as<__half>());
+        else launch_pdl(k_transpose_w<__nv_bfloat16>, g, 256, 0, st, (const __nv_bfloat16*)w, m->kd, c_in, c_out, wt.as<__nv_bfloat16>());
         b = wt.p;
     }
     // tensor cores need 16 B operand rows: zero-pad C % 8 != 0 channel dims
@@ -2192,14 +2207,12 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
             launch_gconv(ctx, dt, a, st);
             if (det) {
                 for (int k = 0; k < m->kd; ++k) {
-                    k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.out_pad,
+                    launch_pdl(k_scatter_add, g, 256, 0, st, gc.as<float>(), n_total, a.out_pad,
                                                      tile_ptr + k, tile_ptr + k + 1, yf, 1);
-                    SK_LAUNCH_CHECK();
                 }
             } else {
-                k_scatter_add<<<g, 256, 0, st>>>(gc.as<float>(), n_total, a.out_pad, tile_ptr,
+                launch_pdl(k_scatter_add, g, 256, 0, st, gc.as<float>(), n_total, a.out_pad, tile_ptr,
                                                  tile_ptr + m->kd, yf, 0);
-                SK_LAUNCH_CHECK();
             }
         }
     }
@@ -2211,10 +2224,9 @@ void transpose_weights(sk_dtype dt, const void* w, int kd, int c_in, int c_out, 
     const long long tot = (long long)kd * c_in * c_out;
     if (tot == 0) return;
     const int g = (int)ceil_div(tot, 256);
-    if (dt == SK_F32) k_transpose_w<float><<<g, 256, 0, st>>>((const float*)w, kd, c_in, c_out, (float*)wt);
-    else if (dt == SK_F16) k_transpose_w<__half><<<g, 256, 0, st>>>((const __half*)w, kd, c_in, c_out, (__half*)wt);
-    else k_transpose_w<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)w, kd, c_in, c_out, (__nv_bfloat16*)wt);
-    SK_LAUNCH_CHECK();
+    if (dt == SK_F32) launch_pdl(k_transpose_w<float>, g, 256, 0, st, (const float*)w, kd, c_in, c_out, (float*)wt);
+    else if (dt == SK_F16) launch_pdl(k_transpose_w<__half>, g, 256, 0, st, (const __half*)w, kd, c_in, c_out, (__half*)wt);
+    else launch_pdl(k_transpose_w<__nv_bfloat16>, g, 256, 0, st, (const __nv_bfloat16*)w, kd, c_in, c_out, (__nv_bfloat16*)wt);
 }
 
 void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt, int c_in,
@@ -2246,8 +2258,7 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
         const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
         auto kern = dt == SK_F16 ? k_wgrad_tc<__half> : k_wgrad_tc<__nv_bfloat16>;
         ensure_smem(reinterpret_cast<const void*>(kern), smem);
-        kern<<<ctx->num_sms, kWgThreads, smem, st>>>(a, stages);
-        SK_LAUNCH_CHECK();
+        launch_pdl(kern, ctx->num_sms, kWgThreads, smem, st, a, stages);
         return;
     }
     if (dt != SK_F32 && !ctx->deterministic && c_in <= 8 && !m->graph) {
@@ -2260,8 +2271,7 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
         auto launch = [&](auto tag, auto ci) {
             using T = decltype(tag);
             constexpr int CI = decltype(ci)::value;
-            k_wgrad_small_cin<T, CI><<<grid, 256, 0, st>>>(
-                static_cast<const T*>(x), static_cast<const T*>(dy), c_out, ptr,
+            launch_pdl(k_wgrad_small_cin<T, CI>, grid, 256, 0, st, static_cast<const T*>(x), static_cast<const T*>(dy), c_out, ptr,
                 m->ws_in.as<int>(), m->ws_out.as<int>(), chunk, dw);
         };
         auto by_ci = [&](auto tag) {
@@ -2278,7 +2288,6 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
         };
         if (dt == SK_F16) by_ci(__half{});
         else by_ci(__nv_bfloat16{});
-        SK_LAUNCH_CHECK();
         return;
     }
     // pair chunking: enough blocks to fill the machine; deterministic mode
@@ -2296,21 +2305,17 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
     SK_CUDA(cudaMemsetAsync(dw64.p, 0, (size_t)cells * 8, st));
     double* d64 = dw64.as<double>();
     if (dt == SK_F32)
-        k_wgrad_simt<float><<<grid, 256, 0, st>>>((const float*)x, (const float*)dy, c_in, c_out,
+        launch_pdl(k_wgrad_simt<float>, grid, 256, 0, st, (const float*)x, (const float*)dy, c_in, c_out,
                                                   ptr, m->ws_in.as<int>(), m->ws_out.as<int>(),
                                                   chunk, d64);
     else if (dt == SK_F16)
-        k_wgrad_simt<__half><<<grid, 256, 0, st>>>((const __half*)x, (const __half*)dy, c_in,
+        launch_pdl(k_wgrad_simt<__half>, grid, 256, 0, st, (const __half*)x, (const __half*)dy, c_in,
                                                    c_out, ptr, m->ws_in.as<int>(),
                                                    m->ws_out.as<int>(), chunk, d64);
     else
-        k_wgrad_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(
-            (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, c_in, c_out, ptr,
+        launch_pdl(k_wgrad_simt<__nv_bfloat16>, grid, 256, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, c_in, c_out, ptr,
             m->ws_in.as<int>(), m->ws_out.as<int>(), chunk, d64);
-    SK_LAUNCH_CHECK();
-    k_round_f64<<<(int)std::min<long long>(ceil_div(cells, 256), 148 * 16), 256, 0, st>>>(
-        d64, cells, dw, accumulate ? 1 : 0);
-    SK_LAUNCH_CHECK();
+    launch_pdl(k_round_f64, (int)std::min<long long>(ceil_div(cells, 256), 148 * 16), 256, 0, st, d64, cells, dw, accumulate ? 1 : 0);
 }
 
 }  // namespace sk

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
     k_dense_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_r,
                const DenseArgs p) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int BN = p.bn;
@@ -434,7 +436,7 @@ bool launch_dense(sk_ctx* ctx, sk_dtype dt, DenseArgs a, const void* x, const vo
     SK_CUDA(cudaMemsetAsync(trbuf, 0, 64 * 8 * 8, st));
     a.trace = trbuf;
 #endif
-    kern<<<grid, kDenseThreads, smem, st>>>(ta, tb, ty, tr, a);
+    launch_pdl(kern, grid, kDenseThreads, smem, st, ta, tb, ty, tr, a);
 #ifdef SK_DENSE_TRACE
     {
         std::vector<long long> h(64 * 8);
@@ -451,7 +453,6 @@ bool launch_dense(sk_ctx* ctx, sk_dtype dt, DenseArgs a, const void* x, const vo
         }
     }
 #endif
-    SK_LAUNCH_CHECK();
     return true;
 }
 

@@ -59,6 +59,8 @@ __device__ __forceinline__ unsigned* slot_val(ulonglong2* t, uint64_t s) {
 __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
                               ulonglong2* __restrict__ table, uint64_t mask,
                               int* __restrict__ err) {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int4 c = coords[i];
@@ -82,6 +84,8 @@ __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, in
                               int dims, ulonglong2* __restrict__ table, uint64_t mask,
                               int* __restrict__ slot_out,
                               int4* __restrict__ q_out) {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int4 c = coords[i];
@@ -105,6 +109,8 @@ __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, in
 
 __global__ void k_down_flag(const int* __restrict__ slot, ulonglong2* __restrict__ table, int n,
                             int* __restrict__ flag) {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     flag[i] = *slot_val(table, slot[i]) == (unsigned)i ? 1 : 0;
@@ -113,6 +119,8 @@ __global__ void k_down_flag(const int* __restrict__ slot, ulonglong2* __restrict
 __global__ void k_down_compact(const int* __restrict__ flag, const int* __restrict__ pos,
                                const int* __restrict__ slot, const int4* __restrict__ q, int n,
                                ulonglong2* __restrict__ table, int4* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !flag[i]) return;
     int p = pos[i];
@@ -128,6 +136,8 @@ constexpr int kBlkEmpty = 0x7FFFFFFF;
 // others wait for the id. Cells keep the FIRST row (atomicMin), like emplace.
 __global__ void k_block_insert(const int4* __restrict__ coords, int n, ulonglong2* __restrict__ bt,
                                uint64_t mask, int* __restrict__ dense, int* __restrict__ count) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = i < n;
     const int4 c = live ? coords[i] : make_int4(0, 0, 0, 0);
@@ -189,6 +199,8 @@ __global__ void __launch_bounds__(kQB) k_kmap_query_blk(
     const int4* __restrict__ out_coords, int n_out, const ulonglong2* __restrict__ bt,
     uint64_t mask, const int* __restrict__ dense, int words, int* __restrict__ os,
     unsigned long long* __restrict__ masks, int* __restrict__ blk_counts) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int KD = K * K * K, H = K / 2;
     extern __shared__ int q_sh[];
     int* tile = q_sh;            // kQB x KD
@@ -264,6 +276,8 @@ __global__ void k_quant_insert(const double* __restrict__ raw, const int* __rest
                                ulonglong2* __restrict__ table, uint64_t mask,
                                int* __restrict__ slot_out, int4* __restrict__ q_out,
                                int* __restrict__ err) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     const double v[3] = {vx, vy, vz};
@@ -306,6 +320,8 @@ __global__ void k_quant_insert(const double* __restrict__ raw, const int* __rest
 // point -> output row (after compaction the table maps key -> out row)
 __global__ void k_point_rows(const int* __restrict__ slot, const ulonglong2* __restrict__ table,
                              int m, int* __restrict__ rows) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     rows[i] = (int)*slot_val(const_cast<ulonglong2*>(table), slot[i]);
@@ -313,6 +329,8 @@ __global__ void k_point_rows(const int* __restrict__ slot, const ulonglong2* __r
 
 // DedupRule::first: the first point of each row (min point index)
 __global__ void k_first_point(const int* __restrict__ rows, int m, int* __restrict__ first) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) atomicMin(first + rows[i], i);
 }
@@ -320,6 +338,8 @@ __global__ void k_first_point(const int* __restrict__ rows, int m, int* __restri
 template <typename T>
 __global__ void k_quant_feats_first(const double* __restrict__ feats, int channels,
                                     const int* __restrict__ first, int n, T* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)n * channels) return;
     const int r = (int)(t / channels), c = (int)(t % channels);
@@ -331,6 +351,8 @@ __global__ void k_quant_feats_first(const double* __restrict__ feats, int channe
 __global__ void k_quant_sum(const double* __restrict__ feats, int channels,
                             const int* __restrict__ rows, int m, double* __restrict__ sum,
                             int* __restrict__ count) {
+    pdl_wait();
+    pdl_trigger();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)m * channels) return;
     const int i = (int)(t / channels), c = (int)(t % channels);
@@ -341,6 +363,8 @@ __global__ void k_quant_sum(const double* __restrict__ feats, int channels,
 template <typename T>
 __global__ void k_quant_mean(const double* __restrict__ sum, const int* __restrict__ count,
                              int channels, int n, T* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)n * channels) return;
     out[t] = (T)(sum[t] / (double)count[t / channels]);
@@ -348,6 +372,8 @@ __global__ void k_quant_mean(const double* __restrict__ sum, const int* __restri
 
 template <typename T>
 __global__ void k_fill(T* __restrict__ out, long long n, double v) {
+    pdl_wait();
+    pdl_trigger();
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n) out[t] = (T)v;
 }
@@ -357,6 +383,8 @@ __global__ void k_fill(T* __restrict__ out, long long n, double v) {
 __global__ void k_edge_keys(const int* __restrict__ edges, int E, int R, int n_in, int n_out,
                             unsigned long long* __restrict__ keys, int* __restrict__ vals,
                             int* __restrict__ counts, int* __restrict__ err) {
+    pdl_wait();
+    pdl_trigger();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     const int src = edges[3 * e], dst = edges[3 * e + 1], rel = edges[3 * e + 2];
@@ -371,6 +399,8 @@ __global__ void k_edge_keys(const int* __restrict__ edges, int E, int R, int n_i
 // exclusive scans of the per-relation counts (pairs and 256-pair tiles); one thread
 __global__ void k_edge_scan(const int* __restrict__ counts, int R, long long* __restrict__ ptr,
                             int* __restrict__ tile_ptr) {
+    pdl_wait();
+    pdl_trigger();
     long long acc = 0;
     int tiles = 0;
     for (int r = 0; r < R; ++r) {
@@ -388,6 +418,8 @@ __global__ void k_edge_scatter(const int* __restrict__ edges, const unsigned lon
                                const int* __restrict__ tile_ptr, int* __restrict__ ws_in,
                                int* __restrict__ ws_out, int* __restrict__ in_pad,
                                int* __restrict__ out_pad) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E) return;
     const int e = order[i];
@@ -428,6 +460,8 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query_gen(
     uint64_t mask, const int4* __restrict__ offs, int KD, int dims, int sx, int sy, int sz,
     int transposed, int words, int* __restrict__ os, unsigned long long* __restrict__ masks,
     int* __restrict__ blk_counts) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int q_sh[];
     int* tile = q_sh;                                       // kQB x KD
     int* cnt = q_sh + kQB * KD;                             // KD
@@ -504,6 +538,8 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
     uint64_t mask, int K, int dims, int sx, int sy, int sz,
     int transposed, int words, int* __restrict__ os, unsigned long long* __restrict__ masks,
     int* __restrict__ blk_counts) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int q_sh[];
     int* tile = q_sh;            // kQB x KD
     int* cnt = q_sh + kQB * KD;  // KD
@@ -596,6 +632,8 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
 __global__ void __launch_bounds__(kQB) k_finalize(const int* __restrict__ os, int kd, int words,
                                                   unsigned long long* __restrict__ masks,
                                                   int* __restrict__ blk_counts) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int sh[];
     int* tile = sh;
     int* cnt = sh + kQB * kd;
@@ -628,6 +666,8 @@ __global__ void __launch_bounds__(1024) k_ws_scan(const int* __restrict__ blk_co
                                                   long long* __restrict__ blk_off,
                                                   long long* __restrict__ ptr,
                                                   int* __restrict__ tile_ptr) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ long long tot[128];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int k = warp; k < kd; k += 32) {
@@ -669,6 +709,8 @@ __global__ void __launch_bounds__(kQB) k_ws_scatter(const int* __restrict__ os, 
                                                     int* __restrict__ ws_out,
                                                     int* __restrict__ in_pad,
                                                     int* __restrict__ out_pad) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int sh[];
     int* tile = sh;
     __shared__ int wcnt[kQB / 32];
@@ -700,6 +742,8 @@ __global__ void __launch_bounds__(kQB) k_ws_scatter(const int* __restrict__ os, 
 }
 
 __global__ void k_transpose(const int* __restrict__ os, int n_out, int kd, int* __restrict__ ost) {
+    pdl_wait();
+    pdl_trigger();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long long)n_out * kd) return;
     int q = (int)(i / kd), k = (int)(i % kd);
@@ -714,6 +758,8 @@ __global__ void k_split_keys(const int* __restrict__ os, int n, int kd, int ns,
                              const int* __restrict__ begin, int W, int word,
                              const int* __restrict__ perm, unsigned long long* __restrict__ keys,
                              int* __restrict__ vals) {
+    pdl_wait();
+    pdl_trigger();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long long)n * ns) return;
     int s = (int)(i / n), r = (int)(i % n);
@@ -749,6 +795,8 @@ __global__ void __launch_bounds__(256) k_split_keygen32(
     const unsigned long long* __restrict__ masks, const SplitDesc sd, int dbits, int passes,
     unsigned* __restrict__ keys, int* __restrict__ vals, uint32_t* __restrict__ ghist,
     int* __restrict__ d_begin, int* __restrict__ d_woff) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint32_t hsh[];  // [passes][1 << dbits]
     const int D = 1 << dbits;
     for (int i = threadIdx.x; i < passes * D; i += blockDim.x) hsh[i] = 0;
@@ -783,6 +831,8 @@ __global__ void __launch_bounds__(256) k_split_keygen32(
 }
 
 __global__ void k_split_desc(const SplitDesc sd, int* __restrict__ d_begin, int* __restrict__ d_woff) {
+    pdl_wait();
+    pdl_trigger();
     for (int i = threadIdx.x; i <= sd.ns; i += blockDim.x) {
         d_begin[i] = sd.begin[i];
         d_woff[i] = sd.woff[i];
@@ -830,6 +880,8 @@ __global__ void __launch_bounds__(kTileM) k_split_reorder(
     const int* __restrict__ begin, const int* __restrict__ word_off, const int* __restrict__ order,
     int* __restrict__ entries, int* __restrict__ out_row, unsigned long long* __restrict__ masks,
     unsigned long long* __restrict__ tmask) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ unsigned long long red[2][kTileM / 32];
     const long long i = (long long)blockIdx.x * kTileM + threadIdx.x;  // rows_pad % 128 == 0
     const int s = (int)(i / rows_pad), p = (int)(i % rows_pad);
@@ -861,6 +913,8 @@ __global__ void __launch_bounds__(kTileM) k_split_reorder(
 __global__ void k_identity_map(int n_out, int rows_pad, int* __restrict__ os,
                                unsigned long long* __restrict__ masks,
                                int* __restrict__ blk_counts) {
+    pdl_wait();
+    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= rows_pad) return;
     os[q] = q < n_out ? q : -1;
@@ -869,6 +923,8 @@ __global__ void k_identity_map(int n_out, int rows_pad, int* __restrict__ os,
 }
 
 __global__ void k_iota(int* __restrict__ v, int n) {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = i;
 }
@@ -898,10 +954,8 @@ void coords_build_blocks(sk_coords* c, cudaStream_t st) {
     c->bcount.alloc(4, st);
     SK_CUDA(cudaMemsetAsync(c->bcount.p, 0, 4, st));
     if (c->n > 0) {
-        k_block_insert<<<(int)ceil_div(c->n, 256), 256, 0, st>>>(
-            c->coords.as<int4>(), c->n, c->btable.as<ulonglong2>(), (uint64_t)cap - 1,
+        launch_pdl(k_block_insert, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n, c->btable.as<ulonglong2>(), (uint64_t)cap - 1,
             c->bdense.as<int>(), c->bcount.as<int>());
-        SK_LAUNCH_CHECK();
     }
     c->has_blocks = true;
 }
@@ -924,11 +978,10 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
         const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
         auto run = [&](auto kern) {
             ensure_smem(reinterpret_cast<const void*>(kern), smem);
-            kern<<<grid, kQB, smem, st>>>(out_coords, m->n_out, in->btable.as<ulonglong2>(),
+            launch_pdl(kern, grid, kQB, smem, st, out_coords, m->n_out, in->btable.as<ulonglong2>(),
                                           (uint64_t)in->bcap - 1, in->bdense.as<int>(), m->words,
                                           m->os.as<int>(), m->masks.as<unsigned long long>(),
                                           m->blk_counts.as<int>());
-            SK_LAUNCH_CHECK();
         };
         if (m->kernel == 3) run(k_kmap_query_blk<3>);
         else run(k_kmap_query_blk<5>);
@@ -939,7 +992,7 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
     const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
 #define SK_Q(KDV, TPRV)                                                                      \
     ensure_smem(reinterpret_cast<const void*>(k_kmap_query<KDV, TPRV>), smem);               \
-    k_kmap_query<KDV, TPRV><<<grid, kQB * TPRV, smem, st>>>(                                 \
+    launch_pdl(k_kmap_query<KDV, TPRV>, grid, kQB * TPRV, smem, st, \
         out_coords, m->n_out, in->table.as<ulonglong2>(), mask,                              \
         m->kernel, m->dims, m->stride[0], m->stride[1], m->stride[2], m->transposed, m->words, \
         m->os.as<int>(), m->masks.as<unsigned long long>(), m->blk_counts.as<int>())
@@ -952,7 +1005,6 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
         default: fail(SK_ERR_VALIDATION, "unsupported kernel volume " + std::to_string(m->kd));
     }
 #undef SK_Q
-    SK_LAUNCH_CHECK();
 }
 
 void alloc_map(sk_kmap* m, cudaStream_t st) {
@@ -983,10 +1035,8 @@ void coords_build_table(sk_coords* c, cudaStream_t st) {
     err.alloc(4, st);
     SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
     if (c->n > 0) {
-        k_hash_insert<<<(int)ceil_div(c->n, 256), 256, 0, st>>>(
-            c->coords.as<int4>(), c->n, c->table.as<ulonglong2>(), (uint64_t)c->cap - 1,
+        launch_pdl(k_hash_insert, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n, c->table.as<ulonglong2>(), (uint64_t)c->cap - 1,
             err.as<int>());
-        SK_LAUNCH_CHECK();
     }
     int h_err = 0;
     read_back(st, {{err.p, 4}}, &h_err);
@@ -1016,22 +1066,19 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     flag.alloc((size_t)n * 4, st);
     pos.alloc((size_t)n * 4 + 4, st);
     const int g = (int)ceil_div(n, 256);
-    k_down_insert<<<g, 256, 0, st>>>(in->coords.as<int4>(), n, stride[0], stride[1],
+    launch_pdl(k_down_insert, g, 256, 0, st, in->coords.as<int4>(), n, stride[0], stride[1],
                                      in->dims == 3 ? stride[2] : 1, in->dims,
                                      out->table.as<ulonglong2>(), (uint64_t)out->cap - 1,
                                      slot.as<int>(), q.as<int4>());
-    SK_LAUNCH_CHECK();
-    k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), n, flag.as<int>());
-    SK_LAUNCH_CHECK();
+    launch_pdl(k_down_flag, g, 256, 0, st, slot.as<int>(), out->table.as<ulonglong2>(), n, flag.as<int>());
     scan_exclusive_i32(flag.as<int>(), pos.as<int>(), n, pos.as<int>() + n, st);
     int h_count = 0;
     read_back(st, {{pos.as<int>() + n, 4}}, &h_count);
     out->n = h_count;
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
-    k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(),
+    launch_pdl(k_down_compact, g, 256, 0, st, flag.as<int>(), pos.as<int>(), slot.as<int>(),
                                       q.as<int4>(), n, out->table.as<ulonglong2>(),
                                       out->coords.as<int4>());
-    SK_LAUNCH_CHECK();
     out->has_table = true;
     return out;
 }
@@ -1064,11 +1111,10 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
     err.alloc(4, st);
     SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
     const int g = (int)ceil_div(m, 256);
-    k_quant_insert<<<g, 256, 0, st>>>(raw, batch, m, dims, voxel[0], voxel[1],
+    launch_pdl(k_quant_insert, g, 256, 0, st, raw, batch, m, dims, voxel[0], voxel[1],
                                       dims == 3 ? voxel[2] : 1.0, out->table.as<ulonglong2>(),
                                       (uint64_t)out->cap - 1, slot.as<int>(), q.as<int4>(),
                                       err.as<int>());
-    SK_LAUNCH_CHECK();
     int h_err = 0;
     read_back(st, {{err.p, 4}}, &h_err);
     if (h_err) {
@@ -1077,20 +1123,17 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
         validate(false, "quantized coordinate outside the packable range "
                         "(batch [0,4096), xyz [-65536,65536))");
     }
-    k_down_flag<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), m, flag.as<int>());
-    SK_LAUNCH_CHECK();
+    launch_pdl(k_down_flag, g, 256, 0, st, slot.as<int>(), out->table.as<ulonglong2>(), m, flag.as<int>());
     scan_exclusive_i32(flag.as<int>(), pos.as<int>(), m, pos.as<int>() + m, st);
     int h_count = 0;
     read_back(st, {{pos.as<int>() + m, 4}}, &h_count);
     out->n = h_count;
     out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
-    k_down_compact<<<g, 256, 0, st>>>(flag.as<int>(), pos.as<int>(), slot.as<int>(), q.as<int4>(),
+    launch_pdl(k_down_compact, g, 256, 0, st, flag.as<int>(), pos.as<int>(), slot.as<int>(), q.as<int4>(),
                                       m, out->table.as<ulonglong2>(), out->coords.as<int4>());
-    SK_LAUNCH_CHECK();
     out->has_table = true;
     if (point_rows) {
-        k_point_rows<<<g, 256, 0, st>>>(slot.as<int>(), out->table.as<ulonglong2>(), m, point_rows);
-        SK_LAUNCH_CHECK();
+        launch_pdl(k_point_rows, g, 256, 0, st, slot.as<int>(), out->table.as<ulonglong2>(), m, point_rows);
     }
     return out;
 }
@@ -1105,8 +1148,7 @@ void quantize_features(int m, int channels, const double* feats, const int32_t* 
         using T = decltype(tag);
         T* o = static_cast<T*>(out);
         if (channels == 0) {  // occupancy: one channel of ones
-            k_fill<T><<<(int)ceil_div(n, 256), 256, 0, st>>>(o, n, 1.0);
-            SK_LAUNCH_CHECK();
+            launch_pdl(k_fill<T>, (int)ceil_div(n, 256), 256, 0, st, o, n, 1.0);
             return;
         }
         const long long tot = (long long)n * channels;
@@ -1115,21 +1157,16 @@ void quantize_features(int m, int channels, const double* feats, const int32_t* 
             DevBuf first;
             first.alloc((size_t)n * 4, st);
             SK_CUDA(cudaMemsetAsync(first.p, 0x7F, (size_t)n * 4, st));
-            k_first_point<<<(int)ceil_div(m, 256), 256, 0, st>>>(point_rows, m, first.as<int>());
-            SK_LAUNCH_CHECK();
-            k_quant_feats_first<T><<<g, 256, 0, st>>>(feats, channels, first.as<int>(), n, o);
-            SK_LAUNCH_CHECK();
+            launch_pdl(k_first_point, (int)ceil_div(m, 256), 256, 0, st, point_rows, m, first.as<int>());
+            launch_pdl(k_quant_feats_first<T>, g, 256, 0, st, feats, channels, first.as<int>(), n, o);
         } else {
             DevBuf sum, cnt;
             sum.alloc((size_t)tot * 8, st);
             cnt.alloc((size_t)n * 4, st);
             SK_CUDA(cudaMemsetAsync(sum.p, 0, sum.bytes, st));
             SK_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, st));
-            k_quant_sum<<<(int)ceil_div((long long)m * channels, 256), 256, 0, st>>>(
-                feats, channels, point_rows, m, sum.as<double>(), cnt.as<int>());
-            SK_LAUNCH_CHECK();
-            k_quant_mean<T><<<g, 256, 0, st>>>(sum.as<double>(), cnt.as<int>(), channels, n, o);
-            SK_LAUNCH_CHECK();
+            launch_pdl(k_quant_sum, (int)ceil_div((long long)m * channels, 256), 256, 0, st, feats, channels, point_rows, m, sum.as<double>(), cnt.as<int>());
+            launch_pdl(k_quant_mean<T>, g, 256, 0, st, sum.as<double>(), cnt.as<int>(), channels, n, o);
         }
     };
     if (dt == SK_F32) launch(float());
@@ -1173,9 +1210,8 @@ sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int 
         vals.alloc((size_t)E * 4, st);
         order.alloc((size_t)E * 4, st);
         const int g = (int)ceil_div(E, 256);
-        k_edge_keys<<<g, 256, 0, st>>>(d_edges, E, R, n_in, n_out, keys.as<unsigned long long>(),
+        launch_pdl(k_edge_keys, g, 256, 0, st, d_edges, E, R, n_in, n_out, keys.as<unsigned long long>(),
                                        vals.as<int>(), counts.as<int>(), err.as<int>());
-        SK_LAUNCH_CHECK();
         int h_err = 0;
         read_back(st, {{err.p, 4}}, &h_err);
         if (h_err) {
@@ -1193,18 +1229,15 @@ sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int 
             SK_CUDA(cudaMemcpyAsync(keys2.p, keys.p, (size_t)E * 8, cudaMemcpyDeviceToDevice, st));
             SK_CUDA(cudaMemcpyAsync(order.p, vals.p, (size_t)E * 4, cudaMemcpyDeviceToDevice, st));
         }
-        k_edge_scan<<<1, 1, 0, st>>>(counts.as<int>(), R, m->ws_ptr.as<long long>(),
+        launch_pdl(k_edge_scan, 1, 1, 0, st, counts.as<int>(), R, m->ws_ptr.as<long long>(),
                                      m->ws_tile_ptr.as<int>());
-        SK_LAUNCH_CHECK();
-        k_edge_scatter<<<g, 256, 0, st>>>(d_edges, keys2.as<unsigned long long>(), order.as<int>(),
+        launch_pdl(k_edge_scatter, g, 256, 0, st, d_edges, keys2.as<unsigned long long>(), order.as<int>(),
                                           E, m->ws_ptr.as<long long>(), m->ws_tile_ptr.as<int>(),
                                           m->ws_in.as<int>(), m->ws_out.as<int>(),
                                           m->ws_in_pad.as<int>(), m->ws_out_pad.as<int>());
-        SK_LAUNCH_CHECK();
     } else {
-        k_edge_scan<<<1, 1, 0, st>>>(counts.as<int>(), R, m->ws_ptr.as<long long>(),
+        launch_pdl(k_edge_scan, 1, 1, 0, st, counts.as<int>(), R, m->ws_ptr.as<long long>(),
                                      m->ws_tile_ptr.as<int>());
-        SK_LAUNCH_CHECK();
     }
     m->has_ws = true;
     m->ws_on.mark(st);
@@ -1233,10 +1266,8 @@ sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t str
                   m->stride[2] == 1;
     alloc_map(m, st);
     if (m->identity) {
-        k_identity_map<<<(int)ceil_div(m->rows_pad, 256), 256, 0, st>>>(
-            m->n_out, m->rows_pad, m->os.as<int>(), m->masks.as<unsigned long long>(),
+        launch_pdl(k_identity_map, (int)ceil_div(m->rows_pad, 256), 256, 0, st, m->n_out, m->rows_pad, m->os.as<int>(), m->masks.as<unsigned long long>(),
             m->blk_counts.as<int>());
-        SK_LAUNCH_CHECK();
     } else {
         launch_query(m, out->coords.as<int4>(), in, st);
     }
@@ -1286,11 +1317,9 @@ sk_kmap* kmap_build_ex(sk_coords* in, sk_coords* out, const int32_t kernel[3],
     constexpr int TPR = 4;
     const size_t smem = (size_t)(kQB * KD + ((KD + 3) & ~3)) * 4 + (size_t)KD * 16;
     ensure_smem(reinterpret_cast<const void*>(k_kmap_query_gen<TPR>), smem);
-    k_kmap_query_gen<TPR><<<m->rows_pad / kQB, kQB * TPR, smem, st>>>(
-        out->coords.as<int4>(), m->n_out, in->table.as<ulonglong2>(), (uint64_t)in->cap - 1,
+    launch_pdl(k_kmap_query_gen<TPR>, m->rows_pad / kQB, kQB * TPR, smem, st, out->coords.as<int4>(), m->n_out, in->table.as<ulonglong2>(), (uint64_t)in->cap - 1,
         offs.as<int4>(), KD, dims, m->stride[0], m->stride[1], m->stride[2], transposed, m->words,
         m->os.as<int>(), m->masks.as<unsigned long long>(), m->blk_counts.as<int>());
-    SK_LAUNCH_CHECK();
     // the offsets table must outlive the kernel: a stream-ordered free
     return m;
 }
@@ -1317,16 +1346,14 @@ sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
     SK_CUDA(cudaMemsetAsync(m->os.p, 0xFF, m->os.bytes, st));
     long long total = (long long)src->n_out * src->kd;
     if (total > 0) {
-        k_transpose<<<(int)ceil_div(total, 256), 256, 0, st>>>(src->os.as<int>(), src->n_out,
+        launch_pdl(k_transpose, (int)ceil_div(total, 256), 256, 0, st, src->os.as<int>(), src->n_out,
                                                                src->kd, m->os.as<int>());
-        SK_LAUNCH_CHECK();
     }
     size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
     ensure_smem(reinterpret_cast<const void*>(k_finalize), smem);
-    k_finalize<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd, m->words,
+    launch_pdl(k_finalize, m->n_blocks, kQB, smem, st, m->os.as<int>(), m->kd, m->words,
                                                m->masks.as<unsigned long long>(),
                                                m->blk_counts.as<int>());
-    SK_LAUNCH_CHECK();
     m->built_on.mark(st);
     src->transpose_cache = m;  // owned by src, released in ~sk_kmap
     return m;
@@ -1350,18 +1377,16 @@ void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
     m->ws_out_pad.alloc(cap_pad * 4, st);
     SK_CUDA(cudaMemsetAsync(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st));
     SK_CUDA(cudaMemsetAsync(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st));
-    k_ws_scan<<<1, 1024, 0, st>>>(m->blk_counts.as<int>(), m->n_blocks, m->kd,
+    launch_pdl(k_ws_scan, 1, 1024, 0, st, m->blk_counts.as<int>(), m->n_blocks, m->kd,
                                   m->blk_off.as<long long>(), m->ws_ptr.as<long long>(),
                                   m->ws_tile_ptr.as<int>());
-    SK_LAUNCH_CHECK();
     size_t smem = (size_t)kQB * m->kd * 4;
     ensure_smem(reinterpret_cast<const void*>(k_ws_scatter), smem);
-    k_ws_scatter<<<m->n_blocks, kQB, smem, st>>>(m->os.as<int>(), m->kd,
+    launch_pdl(k_ws_scatter, m->n_blocks, kQB, smem, st, m->os.as<int>(), m->kd,
                                                  m->blk_off.as<long long>(),
                                                  m->ws_ptr.as<long long>(), m->ws_tile_ptr.as<int>(),
                                                  m->ws_in.as<int>(), m->ws_out.as<int>(),
                                                  m->ws_in_pad.as<int>(), m->ws_out_pad.as<int>());
-    SK_LAUNCH_CHECK();
     m->has_ws = true;
 }
 
@@ -1441,8 +1466,7 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
     // the split bounds itself; every other path gets them from k_split_desc
     const bool fused32 = splits != 0 && n != 0 && kd <= 64 && W + (ns > 1 ? sbits : 0) <= 32;
     if (!fused32) {
-        k_split_desc<<<1, 128, 0, st>>>(sd, d_begin.as<int>(), d_woff.as<int>());
-        SK_LAUNCH_CHECK();
+        launch_pdl(k_split_desc, 1, 128, 0, st, sd, d_begin.as<int>(), d_woff.as<int>());
     }
 
     DevBuf order;
@@ -1450,8 +1474,7 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
     if (splits == 0 || n == 0) {
         // unsorted: identity order (split_and_sort(0) leaves the map unchanged)
         if (n) {
-            k_iota<<<(int)ceil_div(n, 256), 256, 0, st>>>(order.as<int>(), n);
-            SK_LAUNCH_CHECK();
+            launch_pdl(k_iota, (int)ceil_div(n, 256), 256, 0, st, order.as<int>(), n);
         }
     } else {
         const long long tot = (long long)n * ns;
@@ -1471,9 +1494,8 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
             SK_CUDA(cudaMemcpyAsync(dst, vb[r], (size_t)tot * 4, cudaMemcpyDeviceToDevice, st));
         };
         auto sort_pass = [&](int word, int end_bit, const int* perm, int* dst) {
-            k_split_keys<<<g, 256, 0, st>>>(m->os.as<int>(), n, kd, ns, d_begin.as<int>(), W, word,
+            launch_pdl(k_split_keys, g, 256, 0, st, m->os.as<int>(), n, kd, ns, d_begin.as<int>(), W, word,
                                             perm, k_in.as<unsigned long long>(), v_in.as<int>());
-            SK_LAUNCH_CHECK();
             sort_to((unsigned long long*)nullptr, end_bit, dst);
         };
         if (fused32) {
@@ -1490,10 +1512,9 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
             const size_t hsm = pl.hist_words * 4;
             ensure_smem(reinterpret_cast<const void*>(k_split_keygen32), hsm);
             const int kg = (int)std::min<long long>(ceil_div(tot, 256), 2 * 148);
-            k_split_keygen32<<<kg, 256, hsm, st>>>(m->masks.as<unsigned long long>(), sd, pl.dbits,
+            launch_pdl(k_split_keygen32, kg, 256, hsm, st, m->masks.as<unsigned long long>(), sd, pl.dbits,
                                                    pl.passes, kb[0], vb[0], scratch.as<uint32_t>(),
                                                    d_begin.as<int>(), d_woff.as<int>());
-            SK_LAUNCH_CHECK();
             const int r = radix_sort_run<unsigned>(kb, vb, (int)tot, 0, pl, scratch.as<uint32_t>(),
                                                    true, st);
             if (vb[r] != order.as<int>())  // fewer passes ran (n <= 1)
@@ -1511,11 +1532,9 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
     const long long tot_rows = (long long)p->rows_pad * ns;
     const int n_tiles = p->rows_pad / kTileM;
     p->tile_masks.alloc((size_t)n_tiles * ns * 16, st);
-    k_split_reorder<<<(int)(tot_rows / kTileM), kTileM, 0, st>>>(
-        m->os.as<int>(), n, kd, ns, p->rows_pad, d_begin.as<int>(), d_woff.as<int>(),
+    launch_pdl(k_split_reorder, (int)(tot_rows / kTileM), kTileM, 0, st, m->os.as<int>(), n, kd, ns, p->rows_pad, d_begin.as<int>(), d_woff.as<int>(),
         order.as<int>(), p->entries.as<int>(), p->out_row.as<int>(),
         p->masks.as<unsigned long long>(), p->tile_masks.as<unsigned long long>());
-    SK_LAUNCH_CHECK();
     Prepared* raw = p.get();
     raw->built_on.mark(st);
     m->prepared[key] = std::move(p);

@@ -237,12 +237,16 @@ __device__ __forceinline__ float cvt_f<float>(float v) { return v; }
 template <typename T>
 __global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, long long n,
                       T* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         y[i] = cvt_f<T>(ld_f(a, i) + ld_f(b, i));
 }
 template <typename T>
 __global__ void k_fill(T* __restrict__ y, long long n, float v) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         y[i] = cvt_f<T>(v);
@@ -250,12 +254,16 @@ __global__ void k_fill(T* __restrict__ y, long long n, float v) {
 // gradient accumulation: g (fp32) += dx
 template <typename T>
 __global__ void k_accum(float* __restrict__ g, const T* __restrict__ dx, long long n) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         g[i] += ld_f(dx, i);
 }
 template <typename T>
 __global__ void k_cast_from_f32(const float* __restrict__ g, long long n, T* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         y[i] = cvt_f<T>(g[i]);
@@ -362,6 +370,7 @@ struct sk_net {
     std::vector<DevBuf> gout;  // fp32 output grads (backward)
     int64_t map_builds = 0;
     bool overlap = true;                      // overlapped map builds (sk_net_set_overlap)
+    bool pdl = true;                          // programmatic dependent launch (sk_net_set_pdl)
     cudaStream_t map_stream = nullptr;        // overlapped map builds (run_forward)
     cudaStream_t cmp_stream = nullptr;        // overlapped forward's convs for legacy-stream callers
     std::vector<cudaEvent_t> map_ready;       // per layer: its maps are built on map_stream
@@ -610,9 +619,8 @@ void run_layers(sk_net* n, const void* feats, int channels, cudaStream_t st,
             void* y = n->xsum[i].p;
             by_dtype(n->dt, [&](auto tag) {
                 using T = decltype(tag);
-                k_add<T><<<grid_for(cnt), 256, 0, st>>>((const T*)a, (const T*)b, cnt, (T*)y);
+                launch_pdl(k_add<T>, grid_for(cnt), 256, 0, st, (const T*)a, (const T*)b, cnt, (T*)y);
             });
-            SK_LAUNCH_CHECK();
             x = y;
         }
         n->x_ptr[i] = x;
@@ -683,9 +691,11 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     const int dev = n->ctx->device;
     if (!n->worker) n->worker = std::make_unique<MapWorker>();
     MapWorker* builder = n->worker.get();
-    builder->post([&] {
+    const bool pdl = n->pdl;
+    builder->post([&, pdl] {
         try {
             SK_CUDA(cudaSetDevice(dev));
+            pdl_enabled() = pdl;
             for (size_t i = 0; i < L; ++i) {
                 build_layer_maps(n, root, i, ms);
                 const LayerSpec& l = n->spec.layers[i];
@@ -756,9 +766,8 @@ double measure(sk_net* n, sk_coords* root, const void* feats, int channels, bool
     dw.alloc(max_w * 4, st);
     by_dtype(n->dt, [&](auto tag) {
         using T = decltype(tag);
-        k_fill<T><<<grid_for((long long)max_out), 256, 0, st>>>((T*)ones.p, (long long)max_out, 1.f);
+        launch_pdl(k_fill<T>, grid_for((long long)max_out), 256, 0, st, (T*)ones.p, (long long)max_out, 1.f);
     });
-    SK_LAUNCH_CHECK();
     if (dg) {
         Timer t(st);
         for (size_t i = 0; i < L; ++i) {
@@ -833,9 +842,8 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
         const long long ni = (long long)n->in_set[i]->n * l.c_in;
         by_dtype(n->dt, [&](auto tag) {
             using T = decltype(tag);
-            k_cast_from_f32<T><<<grid_for(no), 256, 0, st>>>(n->gout[i].as<float>(), no, (T*)dy.p);
+            launch_pdl(k_cast_from_f32<T>, grid_for(no), 256, 0, st, n->gout[i].as<float>(), no, (T*)dy.p);
         });
-        SK_LAUNCH_CHECK();
         const int g = n->group_of[i];
         conv_wgrad(n->ctx, n->exec_map[i], layer_cfg(n, 2, i), n->dt, l.c_in, l.c_out, n->x_ptr[i],
                    dy.p, wgrad_flat + n->wgrad_off[i], st, accumulate);
@@ -854,9 +862,8 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
             const int j = n->spec.index(pn);
             by_dtype(n->dt, [&](auto tag) {
                 using T = decltype(tag);
-                k_accum<T><<<grid_for(ni), 256, 0, st>>>(n->gout[j].as<float>(), (const T*)dx.p, ni);
+                launch_pdl(k_accum<T>, grid_for(ni), 256, 0, st, n->gout[j].as<float>(), (const T*)dx.p, ni);
             });
-            SK_LAUNCH_CHECK();
         }
     }
 }
@@ -1006,6 +1013,7 @@ sk_status sk_net_forward(sk_net* n, sk_coords* in, const void* d_feats, int chan
                          void* stream, const void** d_out, int* n_out, double* mapping_ms,
                          double* kernel_ms) {
     return nguard([&] {
+        PdlScope pdl_scope(n && n->pdl);
         validate(n && in, "null argument");
         std::vector<double> mp(n->groups.size(), 0.0), kr(n->groups.size(), 0.0);
         const bool timed = mapping_ms || kernel_ms;
@@ -1024,6 +1032,7 @@ sk_status sk_net_forward(sk_net* n, sk_coords* in, const void* d_feats, int chan
 sk_status sk_net_forward_profiled(sk_net* n, sk_coords* in, const void* d_feats, int channels,
                                   void* stream, double* layer_ms, double* mapping_ms_total) {
     return nguard([&] {
+        PdlScope pdl_scope(n && n->pdl);
         std::vector<double> mp(n->groups.size(), 0.0), lm;
         run_forward(n, in, d_feats, channels, S(stream), &mp, nullptr, &lm);
         for (size_t i = 0; i < lm.size(); ++i) layer_ms[i] = lm[i];
@@ -1046,6 +1055,7 @@ sk_status sk_net_layer_output(sk_net* n, int layer, const void** d_out, int* row
 sk_status sk_net_measure(sk_net* n, sk_coords* in, const void* d_feats, int channels, int fwd,
                          int dgrad, int wgrad, void* stream, double* ms) {
     return nguard([&] {
+        PdlScope pdl_scope(n && n->pdl);
         *ms = measure(n, in, d_feats, channels, fwd != 0, dgrad != 0, wgrad != 0, S(stream));
     });
 }
@@ -1056,6 +1066,13 @@ sk_status sk_net_set_overlap(sk_net* n, int on) {
     return nguard([&] {
         sk::validate(n != nullptr, "null network");
         n->overlap = on != 0;
+    });
+}
+
+sk_status sk_net_set_pdl(sk_net* n, int on) {
+    return nguard([&] {
+        sk::validate(n != nullptr, "null network");
+        n->pdl = on != 0;
     });
 }
 
@@ -1075,6 +1092,7 @@ sk_status sk_net_group_traffic(sk_net* n, int group, const sk_dataflow_cfg* cfg,
 sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, int layer_hi,
                           int layer_lo, int accumulate, void* stream) {
     return nguard([&] {
+        PdlScope pdl_scope(n && n->pdl);
         const int L = (int)n->spec.layers.size();
         validate(layer_hi < L && layer_lo >= 0 && layer_lo <= layer_hi, "bad layer range");
         validate(n->root_id != 0 && !n->exec_map.empty() && n->exec_map.back() != nullptr,
@@ -1090,10 +1108,9 @@ sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, 
             const long long no = (long long)n->out_set[L - 1]->n * n->spec.layers[L - 1].c_out;
             by_dtype(n->dt, [&](auto tag) {
                 using T = decltype(tag);
-                k_accum<T><<<grid_for(no), 256, 0, st>>>(n->gout[L - 1].as<float>(),
+                launch_pdl(k_accum<T>, grid_for(no), 256, 0, st, n->gout[L - 1].as<float>(),
                                                          (const T*)d_grad_out, no);
             });
-            SK_LAUNCH_CHECK();
         }
         run_backward(n, layer_hi, layer_lo, wgrad_flat, accumulate != 0, st);
     });
@@ -1107,6 +1124,7 @@ sk_status sk_net_tune(sk_net* n, sk_coords* in, const void* d_feats, int channel
                       int warmup, int runs, void* stream, double* latency_ms, double* log,
                       int log_cap, int* log_len) {
     return nguard([&] {
+        PdlScope pdl_scope(n && n->pdl);
         cudaStream_t st = S(stream);
         const std::vector<sk_dataflow_cfg> space = default_space();
         const int G = (int)n->groups.size();

@@ -44,6 +44,14 @@ inline void contract(bool ok, const std::string& m) {
 // every library kernel launch is followed by SK_LAUNCH_CHECK(), which also
 // counts it (sk_kernel_launches: the bench's gpu_launches evidence)
 std::atomic<unsigned long long>& launch_counter();
+// programmatic dependent launch for this host thread's launches (launch_pdl);
+// a runner sets it from sk_net_set_pdl around its calls (capi.cu)
+bool& pdl_enabled();
+struct PdlScope {
+    bool prev;
+    explicit PdlScope(bool on) : prev(pdl_enabled()) { pdl_enabled() = on; }
+    ~PdlScope() { pdl_enabled() = prev; }
+};
 #define SK_LAUNCH_CHECK()                      \
     do {                                       \
         ::sk::launch_counter().fetch_add(1);   \
@@ -51,6 +59,27 @@ std::atomic<unsigned long long>& launch_counter();
     } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+#if defined(__CUDACC__)
+// Launch with programmatic stream serialization (see pdl_wait): the kernel's
+// launch latency and pre-wait prologue overlap the predecessor's tail.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+    launch_counter().fetch_add(1);
+}
+#endif
 
 // ---- device buffer (stream-ordered allocator + host-side block cache) -------
 // Freed blocks stay in a host-side cache per (stream, size class) and go back
@@ -283,6 +312,16 @@ __device__ __forceinline__ bool elect_one() {
         "}\n"
         : "=r"(pred));
     return pred != 0;
+}
+// Programmatic dependent launch (launch_pdl): a kernel launched with the
+// attribute may start while its stream predecessor is still running; it must
+// pass pdl_wait() (griddepcontrol.wait: the predecessor grid has completed and
+// its memory is visible) before touching any global memory the predecessor
+// reads or writes. pdl_trigger() lets the NEXT kernel begin launching.
+// Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),

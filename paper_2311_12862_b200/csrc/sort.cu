@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int* __res
                                                                 int* __restrict__ out, int n,
                                                                 uint32_t* __restrict__ status,
                                                                 int* __restrict__ total_out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int warp_sums[32];
     __shared__ int s_tile, s_prefix;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(status, 1u);
@@ -137,6 +139,8 @@ template <typename KT>
 __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const KT* __restrict__ keys, int n,
                                                             int begin_bit, int dbits, int passes,
                                                             uint32_t* __restrict__ ghist) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint32_t sh[];  // [passes][1 << dbits]
     const int D = 1 << dbits;
     for (int i = threadIdx.x; i < passes * D; i += blockDim.x) sh[i] = 0;
@@ -163,6 +167,8 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_pass(
     const KT* __restrict__ kin, const int* __restrict__ vin, KT* __restrict__ kout,
     int* __restrict__ vout, int n, int shift, int dbits, const uint32_t* __restrict__ ghist,
     uint32_t* __restrict__ status /* [0] counter, then [tiles][D] */) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int rs[];
     const int D = 1 << dbits;
     int* whist = rs;                      // [warps][D]: per-warp counts -> warp offsets
@@ -170,8 +176,8 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_pass(
     __shared__ int s_tile;
     __shared__ int wsum[kRsWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(status, 1u);
     for (int i = threadIdx.x; i < kRsWarps * D; i += kRsThreads) whist[i] = 0;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(status, 1u);
     __syncthreads();
     const int tile = s_tile;
     uint32_t* st = status + 1;
@@ -272,8 +278,7 @@ void scan_exclusive_i32(const int* in, int* out, int n, int* total_dev, cudaStre
     DevBuf status;
     status.alloc((size_t)(tiles + 1) * 4, st);
     SK_CUDA(cudaMemsetAsync(status.p, 0, status.bytes, st));
-    k_scan_lookback<<<tiles, kScanThreads, 0, st>>>(in, out, n, status.as<uint32_t>(), total_dev);
-    SK_LAUNCH_CHECK();
+    launch_pdl(k_scan_lookback, tiles, kScanThreads, 0, st, in, out, n, status.as<uint32_t>(), total_dev);
 }
 
 RadixPlan radix_plan(int n, int bits) {
@@ -299,19 +304,18 @@ int radix_sort_run(KT* keys[2], int* vals[2], int n, int begin_bit, const RadixP
         const size_t hsm = pl.hist_words * 4;
         ensure_smem(reinterpret_cast<const void*>(k_radix_hist<KT>), hsm);
         const int hg = (int)std::min<int64_t>(ceil_div(n, kRsThreads * 8), 148 * 4);
-        k_radix_hist<KT><<<hg, kRsThreads, hsm, st>>>(keys[0], n, begin_bit, pl.dbits, pl.passes,
+        launch_pdl(k_radix_hist<KT>, hg, kRsThreads, hsm, st, keys[0], n, begin_bit, pl.dbits, pl.passes,
                                                        scratch);
-        SK_LAUNCH_CHECK();
     }
     const size_t psm = (size_t)(kRsWarps + 1) * D * 4;
     ensure_smem(reinterpret_cast<const void*>(k_radix_pass<KT>), psm);
     uint32_t* status = scratch + pl.hist_words;
     int cur = 0;
     for (int p = 0; p < pl.passes; ++p) {
-        k_radix_pass<KT><<<pl.tiles, kRsThreads, psm, st>>>(
-            keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, begin_bit + p * pl.dbits,
-            pl.dbits, scratch + (size_t)p * D, status + (size_t)p * ((size_t)pl.tiles * D + 1));
-        SK_LAUNCH_CHECK();
+        launch_pdl(k_radix_pass<KT>, pl.tiles, kRsThreads, psm, st, (const KT*)keys[cur],
+                   (const int*)vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, begin_bit + p * pl.dbits,
+                   pl.dbits, (const uint32_t*)(scratch + (size_t)p * D),
+                   status + (size_t)p * ((size_t)pl.tiles * D + 1));
         cur ^= 1;
     }
     return cur;

@@ -184,6 +184,10 @@ class NetworkRunner:
         """Overlapped map build (sk_net_set_overlap; default on)."""
         check(lib().sk_net_set_overlap(self.ptr, int(bool(on))))
 
+    def set_pdl(self, on: bool) -> None:
+        """Programmatic dependent launch of the runner's kernels (sk_net_set_pdl; default on)."""
+        check(lib().sk_net_set_pdl(self.ptr, int(bool(on))))
+
     def map_build_count(self) -> int:
         return lib().sk_net_map_builds(self.ptr)
 

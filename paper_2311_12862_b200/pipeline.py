@@ -33,7 +33,9 @@ from . import sparse as _sk
 def replicate(net, count: int):
     """`count` runners: `net` plus copies with its weights and per-group,
     per-phase dataflow configs (so a tuned runner can serve as W workers).
-    With count > 1 every runner's overlapped map build is switched off: the
+    With count > 1 every runner's overlapped map build and programmatic
+    dependent launch are switched off (early-resident CTAs would hold shared
+    memory the other runners' kernels need: -7 % scans/s at 6 in flight); the
     other runners in flight fill the sync bubbles it hides, and its extra
     stream and helper thread cost more than they save (MinkUNet, 4 in flight:
     2.08 vs 1.88 ms/scan)."""
@@ -41,6 +43,7 @@ def replicate(net, count: int):
     out = [net]
     if count > 1:
         net.set_overlap(False)
+        net.set_pdl(False)
     for _ in range(count - 1):
         r = NetworkRunner(net.layers, dtype=net.dtype, dims=net.dims, ctx=net.ctx, weight_seed=None)
         for i in range(net.num_layers):
@@ -49,6 +52,7 @@ def replicate(net, count: int):
             for ph in ("forward", "dgrad", "wgrad"):
                 r.set_config(g, net.config(g, ph), ph)
         r.set_overlap(False)
+        r.set_pdl(False)
         out.append(r)
     return out
 
