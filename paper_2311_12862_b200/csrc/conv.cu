@@ -510,8 +510,6 @@ template <typename T, int KC, bool USE_TMA, int SLABS, int PW>
 __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
     k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const ConvArgs p, int stages, int acc_bufs) {
-    pdl_wait();
-    pdl_trigger();
     constexpr int kProducerWarps = Roles<PW>::kProducerWarps;
     constexpr int kGroupRows = Roles<PW>::kGroupRows;
     constexpr int kMmaWarp = Roles<PW>::kMmaWarp;
@@ -593,6 +591,9 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the prologue (barriers, tensor-map prefetch, TMEM) overlapped the
+    // predecessor's tail; global memory only after it has completed
+    pdl_wait();
     const int n_items = num_items(p);
     const int nchunks = (p.k_total + KC - 1) / KC;
     const T* __restrict__ A = static_cast<const T*>(p.a);
@@ -1134,6 +1135,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             mbar_arrive(&tempty[acc]);
         }
     }
+    pdl_trigger();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();

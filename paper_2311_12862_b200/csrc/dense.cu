@@ -75,8 +75,6 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
     k_dense_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_r,
                const DenseArgs p) {
-    pdl_wait();
-    pdl_trigger();
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int BN = p.bn;
@@ -126,6 +124,9 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the prologue (barriers, tensor-map prefetch, TMEM) overlapped the
+    // predecessor's tail; global memory only after it has completed
+    pdl_wait();
 #ifdef SK_DENSE_TRACE
     if (blockIdx.x == 0 && threadIdx.x == 0) p.trace[63 * 8] = clock64();
 #endif
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
         }
         if (p.staged && lane == 0) bulk_wait0();
     }
+    pdl_trigger();  // this CTA's work is done: let the next kernel launch
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
