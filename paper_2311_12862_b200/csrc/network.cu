@@ -287,9 +287,10 @@ using namespace sk;
 namespace sk {
 // The runner's map-builder thread (overlapped forward), created on first use
 // and kept for the runner's lifetime: one job per forward. After a job it
-// polls for the next one for a short while (back-to-back scans hand over in
-// microseconds), then sleeps on a condition variable; spawning a thread per
-// forward cost ~40 us of host latency before the first map kernel.
+// polls (yielding) for the next one for 5 ms, so back-to-back scans hand over
+// in microseconds (a condition-variable wake cost tens), then sleeps on a
+// condition variable; spawning a thread per forward cost ~40 us of host
+// latency before the first map kernel.
 struct MapWorker {
     std::thread t;
     std::mutex mu;
@@ -312,7 +313,7 @@ struct MapWorker {
     }
     void loop() {
         for (;;) {
-            const auto until = std::chrono::steady_clock::now() + std::chrono::microseconds(500);
+            const auto until = std::chrono::steady_clock::now() + std::chrono::milliseconds(5);
             while (!pending.load(std::memory_order_acquire) &&
                    std::chrono::steady_clock::now() < until)
                 std::this_thread::yield();
@@ -679,9 +680,15 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
     SK_CUDA(cudaEventRecord(n->map_ready[L], caller));  // the caller's prior work (root, feats)
     SK_CUDA(cudaStreamWaitEvent(ms, n->map_ready[L], 0));
     if (legacy) SK_CUDA(cudaStreamWaitEvent(st, n->map_ready[L], 0));
-    // release the previous scan's maps only now: their buffers go back to the
-    // map stream's cache / pool behind the wait above, i.e. after every conv
-    // of the previous scan that read them
+    // the previous scan's maps are released below, after the builder has its
+    // job (dropping ~200 references took ~20 us of the critical path): their
+    // buffers go back to the map stream's cache / pool behind the wait above,
+    // i.e. after every conv of the previous scan that read them
+    std::vector<sk_coords*> old_in, old_out;
+    std::vector<sk_kmap*> old_maps;
+    old_in.swap(n->in_set);
+    old_out.swap(n->out_set);
+    old_maps.swap(n->exec_map);
     reset_maps(n);
     // layer i's maps are ready once done > i; this thread spins (yielding) on
     // it: a condition-variable wake per layer added tens of microseconds
@@ -713,6 +720,9 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
         MapWorker* w;
         ~Join() { w->wait(); }
     } join{builder};
+    for (auto* c : old_in) if (c) sk_coords_release(c);
+    for (auto* c : old_out) if (c) sk_coords_release(c);
+    for (auto* m : old_maps) if (m) sk_kmap_release(m);
     refresh_wt(n, st);
     n->out.resize(L);
     n->xsum.resize(L);
