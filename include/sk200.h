@@ -63,7 +63,9 @@ typedef enum { SK_REORDER_OFFLINE = 0, SK_REORDER_ONLINE = 1 } sk_reorder;
  * reference's two presets plus the B200 variants below:
  *   cta_m      128: 128-row MMA tiles in 256-row items, two CTAs per SM
  *              (8 gather warps each) when C_out <= 128 and stages fit;
- *              256: one CTA per SM (16 gather warps, ~200 KB of stages)
+ *              256: one CTA per SM (16 gather warps, ~200 KB of stages);
+ *              64: implicit GEMM work items of ONE 128-row tile (twice the
+ *              items: small layers spread over more SMs)
  *   cta_n      C_out tile (multiple of 16, <= 256; 0 = whole C_out)
  *   cta_k      channels per pipeline stage: 0 = auto (64/32/16 dividing
  *              C_in; C_in = 96 as three 32-channel slabs), 16 / 32 / 64 =

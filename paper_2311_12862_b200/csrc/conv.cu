@@ -112,6 +112,7 @@ struct ConvArgs {
     int exp;          // SK_CONV_TRACE builds: SK_EXP bits 1 no A gathers, 2 no zeroing, 4 no MMA, 8 no B TMA
     int offset_only;  // >= 0: WS mode only tiles of this offset
     int* sched;       // dynamic item queue {next item, CTAs done} (self-resetting), or null
+    int single;       // OS mode: one 128-row tile per work item (cta_m 64) instead of two
     // tile preferences from the layer's TilePreset (include/sk200.h):
     int cta_m;        // 256: one CTA per SM; otherwise two per SM when C_out <= 128 fits
     int cta_k;        // channels per pipeline stage: 0 auto, 16 / 32 / 64, 96 = 3 x 32 slabs
@@ -191,17 +192,18 @@ __device__ Item decode(const ConvArgs& p, int item) {
         return it;
     }
     if (p.mode == 0) {
-        const int per = pairs_of(p.n_tiles) * p.n_ntiles;
+        const int tpi = p.single ? 1 : 2;  // 128-row tiles per item
+        const int per = (p.single ? p.n_tiles : pairs_of(p.n_tiles)) * p.n_ntiles;
         it.s = p.split_only >= 0 ? p.split_only : item / per;
         const int rem = p.split_only >= 0 ? item : item % per;
-        it.t2 = rem / p.n_ntiles;
+        it.t2 = rem / p.n_ntiles;  // item index within the split
         it.nt = rem % p.n_ntiles;
         it.col_begin = p.split_begin[it.s];
         it.w = p.split_begin[it.s + 1] - it.col_begin;
-        it.row0 = (long long)it.t2 * kItemM;
+        it.row0 = (long long)it.t2 * tpi * kTileM;
         it.k = -1;
-        it.halves = (2 * it.t2 + 1 < p.n_tiles) ? 2 : 1;
-        const unsigned long long* tm = p.tile_masks + ((size_t)it.s * p.n_tiles + 2 * it.t2) * 2;
+        it.halves = (!p.single && 2 * it.t2 + 1 < p.n_tiles) ? 2 : 1;
+        const unsigned long long* tm = p.tile_masks + ((size_t)it.s * p.n_tiles + tpi * it.t2) * 2;
         it.m0 = tm[0];
         it.m1 = tm[1];
         if (it.halves == 2) {
@@ -256,7 +258,7 @@ __device__ __forceinline__ int next_col(unsigned long long& m0, unsigned long lo
 __device__ __forceinline__ const int* idx_column(const ConvArgs& p, const Item& it, int j, int h) {
     if (p.mode == 0) {
         if (h >= it.halves) return nullptr;
-        const long long t = 2 * (long long)it.t2 + h;
+        const long long t = (p.single ? 1 : 2) * (long long)it.t2 + h;
         return p.entries + (size_t)p.rows_pad * it.col_begin + ((size_t)t * it.w + j) * kTileM;
     }
     return p.in_pad + it.row0 + h * kTileM;
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             const uint64_t r1 = it.bw1 > 0 ? (__brevll(it.m1) >> (64 - it.bw1)) : 0ull;
             const int n0 = __popcll(r0), n = n0 + __popcll(r1);
             const int* tile0 = p.entries + (size_t)p.rows_pad * it.col_begin +
-                               (size_t)(2 * it.t2) * it.w * kTileM;
+                               (size_t)((p.single ? 1 : 2) * it.t2) * it.w * kTileM;
             const int half1 = it.halves == 2 ? it.w * kTileM : -1;  // offset of half 1's column
             for (int base = 0; base < n; base += 32) {
                 const int k = base + lane;
@@ -656,6 +658,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
                     }
                     if (lane == 0) {
                         descs[slot].brow = brow;
+                        descs[slot].pad0 = half1 >= 0 ? 2 : 1;  // MMA halves of the step
                         mbar_expect_tx(&ifull[slot], (half1 >= 0 ? 2 : 1) * kTileM * 4);
                     }
                     __syncwarp();
@@ -743,6 +746,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
 #endif
             if (lane == 0) {
                 descs[slot].brow = kb * p.n_total + cur.it.nt * BN;
+                descs[slot].pad0 = (ident || c1) ? 2 : 1;  // MMA halves of the step
                 if (ident) mbar_arrive(&ifull[slot]);
                 else mbar_expect_tx(&ifull[slot], (c1 ? 2 : 1) * kTileM * 4);
             }
@@ -961,6 +965,9 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             mbar_wait_sleep(&cfull[slot], ph);
             SK_TZ(1);
             const int brow = descs[slot].brow;
+            // a one-half step never feeds the MMA's second half: zero warp 1
+            // (rows 128-255) leaves those stale rows (and their dirty marks) alone
+            const bool idle = zw * GROUPS * 32 >= kTileM && descs[slot].pad0 < 2;
             uint32_t real[GROUPS];
 #pragma unroll
             for (int g = 0; g < GROUPS; ++g) real[g] = cslots[slot].zmask[zw * GROUPS + g];
@@ -977,7 +984,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
                     if (lane == g) my_real = real[g];
 #pragma unroll
                 for (int k = 0; k < kMaxStages; ++k)
-                    if (k == stage) {
+                    if (k == stage && !idle) {
                         mine = ~my_real & dreg[k];
                         dreg[k] = my_real;
                     }
@@ -1054,6 +1061,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             const uint32_t d0 = tmem + (uint32_t)(acc * 2 * BN);  // half 0; half 1 at +BN
             // the MMA needs only the step count: A and B come from the stage
             const int nsteps = (__popcll(it.m0) + __popcll(it.m1)) * (nchunks / NSL);
+            const uint32_t two = it.halves == 2 ? 1u : 0u;  // one-tile items: no second-half MMAs
             uint32_t accumulate = 0;
             for (int st = 0; st < nsteps; ++st) {
                 SK_TR(3, lane == 0);
@@ -1070,13 +1078,13 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
                         const uint64_t ds = da + ((uint64_t)(sl * a_bytes) >> 4);
                         tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, ds, ds + (a_half >> 4),
                                             da + ((uint64_t)(a_all + sl * b_bytes) >> 4), idesc,
-                                            accumulate, nullptr);
+                                            accumulate, nullptr, two);
                         accumulate = 1;
                     }
                     const uint64_t ds = da + ((uint64_t)((NSL - 1) * a_bytes) >> 4);
                     tc_mma_step_f16<KC>(d0, d0 + (uint32_t)BN, ds, ds + (a_half >> 4),
                                         da + ((uint64_t)(a_all + (NSL - 1) * b_bytes) >> 4), idesc,
-                                        accumulate, &empty[stage]);
+                                        accumulate, &empty[stage], two);
                 }
                 SK_TR(5, lane == 0);
 #ifdef SK_CONV_TRACE
@@ -1114,7 +1122,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
             const bool empty_tile = (it.m0 | it.m1) == 0;
             const int n0 = it.nt * BN;
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < it.halves; ++h) {
                 for (int c0 = 0; c0 < BN; c0 += 16) {
                     uint32_t v[16];
                     if (!empty_tile) {
@@ -2094,6 +2102,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     pick_n_tiling(n_total, cfg.tile.cta_n, tc, a.bn, a.n_ntiles);
     a.cta_m = cfg.tile.cta_m;
     a.cta_k = cfg.tile.cta_k;
+    a.single = cfg.tile.cta_m == 64 ? 1 : 0;
     a.tma_gather = cfg.tile.load_width == 1 ? 1 : 0;
     const bool det = ctx->deterministic;
 
@@ -2124,7 +2133,8 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         a.rows_pad = pr->rows_pad;
         a.n_tiles = pr->rows_pad / kTileM;
         a.n_rows_valid = m->n_out;
-        const int pairs = (a.n_tiles + 1) / 2;  // 256-row items
+        // work items: 256 rows (two MMA tiles), or one 128-row tile (cta_m 64)
+        const int pairs = a.single ? a.n_tiles : (a.n_tiles + 1) / 2;
         if (pr->num_splits == 1) {
             a.items = pairs * a.n_ntiles;
             a.y = y_accum ? (void*)y_accum : y;

@@ -882,7 +882,8 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
 // tuner.cpp:9-26's 12 entries, then the B200 kernel variants the reference's
 // presets cannot name (include/sk200.h sk_tile): one CTA per SM (cta_m 256),
 // TMA tile::gather4 producers (load_width 1) and single-slab 32-channel
-// stages (cta_k 32) for the sorted implicit GEMM at 1-2 splits
+// stages (cta_k 32) for the sorted implicit GEMM at 1-2 splits, and one
+// 128-row tile per work item (cta_m 64) at 1-3 splits
 std::vector<sk_dataflow_cfg> default_space() {
     std::vector<sk_dataflow_cfg> sp;
     sk_dataflow_cfg c = default_cfg();
@@ -909,6 +910,14 @@ std::vector<sk_dataflow_cfg> default_space() {
         sp.push_back(ig);
         ig.tile.load_width = 4;
         ig.tile.cta_k = 32;  // single-slab 32-channel stages
+        sp.push_back(ig);
+    }
+    for (int s = 1; s <= 3; ++s) {  // one 128-row tile per work item: small layers fill more SMs
+        sk_dataflow_cfg ig = default_cfg();
+        ig.kind = SK_IMPLICIT_GEMM;
+        ig.splits = s;
+        ig.tile.cta_m = 64;
+        ig.tile.cta_n = 64;
         sp.push_back(ig);
     }
     return sp;

@@ -139,22 +139,24 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 // One K step of both 128-row halves (KC/16 MMAs each, interleaved so they
 // share the B stage), then commit -> bar. Called by the whole warp with
 // uniform operands; elect.sync picks the issuing lane.
+// two == 0: only the first half (an item of one 128-row tile).
 template <int KC>
 __device__ __forceinline__ void tc_mma_step_f16(uint32_t d0, uint32_t d1, uint64_t a0, uint64_t a1,
                                                 uint64_t b, uint32_t idesc, uint32_t accumulate,
-                                                uint64_t* bar) {
+                                                uint64_t* bar, uint32_t two = 1) {
 #pragma unroll
     for (int kk = 0; kk < KC / 16; ++kk) {
         const uint32_t acc = (kk > 0 || accumulate) ? 1u : 0u;
         asm volatile(
-            "{\n.reg .pred E, p;\n"
+            "{\n.reg .pred E, p, q, E2;\n"
             "elect.sync _|E, 0xffffffff;\n"
             "setp.ne.b32 p, %6, 0;\n"
+            "setp.ne.and.b32 E2, %7, 0, E;\n"
             "@E tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, p;\n"
-            "@E tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %5, p;\n"
+            "@E2 tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %5, p;\n"
             "}\n" ::"r"(d0),
             "r"(d1), "l"(a0 + (uint64_t)(kk * 2)), "l"(a1 + (uint64_t)(kk * 2)),
-            "l"(b + (uint64_t)(kk * 2)), "r"(idesc), "r"(acc)
+            "l"(b + (uint64_t)(kk * 2)), "r"(idesc), "r"(acc), "r"(two)
             : "memory");
     }
     if (bar)

@@ -175,9 +175,10 @@ def test_tuner_contracts(env):
     x = torch.randn(cs.n, 1, device="cuda").half()
     space = N.default_space()
     # the reference's 12 entries (tuner.cpp:9-26) first, then the B200
-    # kernel variants (sk_tile: one CTA per SM, TMA gather4, 32-channel slabs)
-    assert len(space) == 18
-    assert all(c.kind == sk.IMPLICIT_GEMM and c.splits in (1, 2) for c in space[12:])
+    # kernel variants (sk_tile: one CTA per SM, TMA gather4, 32-channel
+    # slabs, one-tile work items)
+    assert len(space) == 21
+    assert all(c.kind == sk.IMPLICIT_GEMM and c.splits in (1, 2, 3) for c in space[12:])
     assert len({(c.kind, c.splits, c.tile) for c in space}) == len(space)
     lat, log = net.tune(cs, x, training=0, warmup=1, runs=3)
     G = net.num_groups

@@ -88,7 +88,9 @@ def main():
             names[k] = names.get(k, 0.0) + (e_ - s_)
         ms = sorted(round(e_ - s_, 1) for s_, e_, n in iv if "Memset" in n)
         gaps = np.array(gaps) if gaps else np.zeros(1)
-        r = {"gap_list": gl, "memsets_us": ms, "span_us": t1 - t0, "busy_us": busy, "idle_us": (t1 - t0) - busy,
+        inst = [(round(e_ - s_, 1), n.replace("void ", "").replace("sk::(anonymous namespace)::", "").split("(")[0][:40])
+                for s_, e_, n in iv]
+        r = {"instances": inst, "gap_list": gl, "memsets_us": ms, "span_us": t1 - t0, "busy_us": busy, "idle_us": (t1 - t0) - busy,
              "kernels": len(iv), "gaps_over_5us": int((gaps > 5).sum()),
              "largest_gaps_us": sorted(gaps.tolist())[-8:], "by_class_us": cls,
              "by_kernel_us": dict(sorted(((k, round(v, 1)) for k, v in names.items()),
