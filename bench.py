@@ -379,7 +379,7 @@ def main():
     net_tflops = group_flops.sum() / (float(np.sum(kr)) / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and wl == "infer":  # the capture is of MinkUNet's group-0 kernel
         traffic = json.load(open(tpath)).get("dominant_dram_bytes_per_launch")
 
     kmap_roof = kmap_roofline(sk, pk) if rank == 0 else None
