@@ -334,3 +334,24 @@ def test_traffic_model_matches_reference(env, reference, which):
             assert got == want, (g, kind, s, large, got, want)
             checked += 1
     assert checked >= net.num_groups * 4
+
+
+def test_pdl_and_overlap_settings_do_not_change_results(env):
+    """Programmatic dependent launch (sk_net_set_pdl) and the overlapped map
+    build (sk_net_set_overlap) only change when kernels may start: a forward
+    and a chained backward are bitwise identical with each on or off
+    (store-only dataflow, no float atomics)."""
+    torch, sk, N, M = env
+    net = N.NetworkRunner(M.minkunet18(), dtype=torch.float16, weight_seed=4)
+    net.set_all(sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large()))
+    c = torch.from_numpy(scan(20000, seed=31)).cuda()
+    x = torch.randn(c.shape[0], 4, device="cuda", generator=torch.Generator("cuda").manual_seed(1)).half()
+    outs = []
+    for pdl, overlap in ((True, True), (False, True), (True, False), (False, False)):
+        net.set_pdl(pdl)
+        net.set_overlap(overlap)
+        y, _ = net.forward(sk.CoordSet.create(c), x)
+        torch.cuda.synchronize()
+        outs.append(y.cpu())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
