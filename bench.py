@@ -13,7 +13,7 @@ Prints ONE JSON line (rank 0). Under torchrun each rank runs its own scans
 region is bracketed by barrier + synchronize and the max over ranks is taken.
 
   value       scans/s over all ranks, inputs already in HBM, --concurrency
-              (default 6) scans in flight per GPU; config.latency_ms_per_scan
+              (default 8) scans in flight per GPU; config.latency_ms_per_scan
               is the one-scan-at-a-time latency
   e2e         scans/s through the public API (pipeline.ScanPipeline) from
               pinned HOST coords+feats to the output features in pinned host
@@ -194,7 +194,7 @@ def main():
                     help="infer: configs[1] MinkUNet inference (default); second: configs[2] "
                          "SECOND encoder inference; train: configs[3] mixed-precision DP "
                          "training step, global batch 8 scans")
-    ap.add_argument("--concurrency", type=int, default=6,
+    ap.add_argument("--concurrency", type=int, default=8,
                     help="scans in flight (host threads x CUDA streams x NetworkRunners); "
                          "1 = one scan at a time")
     ap.add_argument("--no-tune", action="store_true",
