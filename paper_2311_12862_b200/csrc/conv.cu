@@ -1931,7 +1931,20 @@ __global__ void __launch_bounds__(256) k_conv_small_cin(
     constexpr int KD = 27, TPR = 4, CQ = CO / TPR;
     extern __shared__ float4 wsh4[];  // [kd][CI][CO/4] fp32
     float* wsh = reinterpret_cast<float*>(wsh4);
-    for (int i = threadIdx.x; i < kd * CI * CO; i += blockDim.x) wsh[i] = to_f(w[i]);
+    {  // stage W with every element's load in flight at once (one latency, not ~14)
+        constexpr int PER = (KD * CI * CO + 255) / 256;
+        float v[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * 256;
+            v[j] = i < kd * CI * CO ? to_f(w[i]) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * 256;
+            if (i < kd * CI * CO) wsh[i] = v[j];
+        }
+    }
     __syncthreads();
     const int sub = threadIdx.x % TPR;
     for (int row = (blockIdx.x * blockDim.x + threadIdx.x) / TPR; row < n_out;
@@ -1943,12 +1956,20 @@ __global__ void __launch_bounds__(256) k_conv_small_cin(
         int nb[KD];
 #pragma unroll
         for (int k = 0; k < KD; ++k) nb[k] = k < kd ? __ldg(e + k) : -1;
+        // all neighbour rows in flight at once (one load latency per row, not
+        // 27 dependent ones: 67 -> ~15 us for the MinkUNet stem)
+        uint2 xr[KD];
+        if constexpr (CI == 4 && sizeof(T) == 2) {
+#pragma unroll
+            for (int k = 0; k < KD; ++k)
+                xr[k] = nb[k] >= 0 ? __ldg(reinterpret_cast<const uint2*>(x) + nb[k]) : make_uint2(0, 0);
+        }
 #pragma unroll
         for (int k = 0; k < KD; ++k) {
             if (nb[k] < 0) continue;
             float xv[CI];
             if constexpr (CI == 4 && sizeof(T) == 2) {
-                const uint2 u = __ldg(reinterpret_cast<const uint2*>(x) + nb[k]);
+                const uint2 u = xr[k];
                 const float2 a = unpack2(u.x, (T*)nullptr), b = unpack2(u.y, (T*)nullptr);
                 xv[0] = a.x; xv[1] = a.y; xv[2] = b.x; xv[3] = b.y;
             } else {
@@ -1981,13 +2002,71 @@ __global__ void __launch_bounds__(256) k_conv_small_cin(
     }
 }
 
+// Tiny-C_in layers (the stem) as ONE dense tensor-core GEMM: gather every
+// output row's K^D neighbour rows into A[row][k*CI + c] (zeros for missing
+// neighbours and the pad to K_pad, a multiple of 16), so that
+// y = A [n_out x K_pad] . Wc [K_pad x C_out] with Wc[k*CI + c][co] = W[k][c][co]
+// runs on k_dense_tc. The CUDA-core path spent ~60 us on the MinkUNet stem
+// (low occupancy, LDS-latency-bound FMA chains); the gather writes n_out x
+// K_pad halves once and the GEMM streams them.
+template <typename T, int CI>
+__global__ void __launch_bounds__(256) k_im2col_small(const int* __restrict__ os, int n_out, int kd,
+                                                      const T* __restrict__ x, int k_pad,
+                                                      T* __restrict__ a) {
+    pdl_wait();
+    pdl_trigger();
+    const long long tot = (long long)n_out * (k_pad / CI);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(i / (k_pad / CI)), k = (int)(i % (k_pad / CI));
+        const int nb = k < kd ? __ldg(os + (size_t)row * kd + k) : -1;
+        T* dst = a + (size_t)row * k_pad + k * CI;
+        if constexpr (CI == 4 && sizeof(T) == 2) {
+            *reinterpret_cast<uint2*>(dst) =
+                nb >= 0 ? __ldg(reinterpret_cast<const uint2*>(x) + nb) : make_uint2(0, 0);
+        } else {
+#pragma unroll
+            for (int c = 0; c < CI; ++c) dst[c] = nb >= 0 ? x[(size_t)nb * CI + c] : from_f<T>(0.f);
+        }
+    }
+}
+// Wc^T, K-major: b[co][k*CI + c] = W[k][c][co]; zero pad columns
+template <typename T>
+__global__ void k_small_cin_weights(const T* __restrict__ w, int kd, int ci, int co, int k_pad,
+                                    T* __restrict__ b) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= co * k_pad) return;
+    const int o = i / k_pad, kk = i % k_pad;
+    const int k = kk / ci, c = kk % ci;
+    b[i] = k < kd ? w[((size_t)k * ci + c) * co + o] : from_f<T>(0.f);
+}
+
+template <typename T>
+bool conv_small_cin_dense(sk_ctx* ctx, sk_dtype dt, const sk_kmap* m, int c_in, int c_out,
+                          const void* x, const void* w, void* y, int cta_n, cudaStream_t st) {
+    if (c_in != 4 || c_out % 16 != 0) return false;
+    const int k_pad = (int)ceil_div((long long)m->kd * c_in, 16) * 16;
+    DevBuf a, b;
+    a.alloc((size_t)m->n_out * k_pad * sizeof(T), st);
+    b.alloc((size_t)c_out * k_pad * sizeof(T), st);
+    const long long tot = (long long)m->n_out * (k_pad / c_in);
+    launch_pdl(k_im2col_small<T, 4>, (int)std::min<long long>(ceil_div(tot, 256), (long long)ctx->num_sms * 16),
+               256, 0, st, m->os.as<int>(), m->n_out, m->kd, static_cast<const T*>(x), k_pad, a.as<T>());
+    launch_pdl(k_small_cin_weights<T>, (int)ceil_div((long long)c_out * k_pad, 256), 256, 0, st,
+               static_cast<const T*>(w), m->kd, c_in, c_out, k_pad, b.as<T>());
+    return dense_identity_tc(ctx, dt, m->n_out, k_pad, c_out, a.p, b.p, y, nullptr, nullptr, cta_n, st);
+}
+
 template <typename T>
 bool conv_small_cin(const sk_kmap* m, int c_in, int c_out, const void* x, const void* w, void* y,
                     const void* residual, float* y_accum, cudaStream_t st) {
     auto launch = [&](auto kern) {
         const size_t smem = (size_t)m->kd * c_in * c_out * 4;
         ensure_smem(reinterpret_cast<const void*>(kern), smem);
-        const int grid = (int)std::min<int64_t>(ceil_div(m->n_out, 64), (int64_t)m->ctx->num_sms * 8);
+        // persistent: each block stages W once, then walks many rows
+        const int grid = (int)std::min<int64_t>(ceil_div(m->n_out, 64), (int64_t)m->ctx->num_sms * 2);
         launch_pdl(kern, grid, 256, smem, st, m->os.as<int>(), m->n_out, m->kd, static_cast<const T*>(x), static_cast<const T*>(w),
             static_cast<T*>(y), static_cast<const T*>(residual), y_accum);
         return true;
@@ -2046,6 +2125,16 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
     const size_t es = elem_size(dt);
     const long long y_elems = (long long)m->n_out * n_total;
     if (m->n_out == 0) return;
+    if (cfg.kind == SK_IMPLICIT_GEMM && !dgrad && dt != SK_F32 && !residual && !y_accum &&
+        !ctx->deterministic && m->kd <= 27) {
+        // tiny C_in (the 4-channel stem): neighbour gather + one dense tcgen05 GEMM
+        const bool done = dt == SK_F16
+                              ? conv_small_cin_dense<__half>(ctx, dt, m, c_in, c_out, x, w, y,
+                                                             cfg.tile.cta_n, st)
+                              : conv_small_cin_dense<__nv_bfloat16>(ctx, dt, m, c_in, c_out, x, w,
+                                                                    y, cfg.tile.cta_n, st);
+        if (done) return;
+    }
     if (cfg.kind == SK_IMPLICIT_GEMM && !dgrad && dt != SK_F32) {
         // tiny C_in (the 4-channel stem): implicit GEMM on CUDA cores, raw OS map
         const bool done = dt == SK_F16
