@@ -859,12 +859,21 @@ __device__ void row_reorder(const int* __restrict__ os, int n, int kd, int rows_
     int src = order[(size_t)s * n + p];
     const int* row = os + (size_t)src * kd + b;
     unsigned long long m[2] = {0, 0};
-    for (int j = 0; j < w; ++j) {
-        int v = row[j];
-        dst[(size_t)j * kTileM] = v;
-        if (v >= 0) {
-            int wi = j / 64, biw = min(64, w - wi * 64);
-            m[wi] |= 1ull << (biw - 1 - (j - wi * 64));
+    // 16 loads in flight per batch (a load -> store chain per column paid one
+    // L2 latency per entry)
+    for (int j0 = 0; j0 < w; j0 += 16) {
+        int v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = j0 + u < w ? __ldg(row + j0 + u) : -1;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int j = j0 + u;
+            if (j >= w) break;
+            dst[(size_t)j * kTileM] = v[u];
+            if (v[u] >= 0) {
+                const int wi = j / 64, biw = min(64, w - wi * 64);
+                m[wi] |= 1ull << (biw - 1 - (j - wi * 64));
+            }
         }
     }
     out_row[(size_t)s * rows_pad + p] = src;
