@@ -1496,7 +1496,7 @@ __device__ __forceinline__ int wg_offset_of(const int* tp, int kd, int t) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(const WgArgs p, int stages) {
+__global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(const WgArgs p, int stages) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -2351,15 +2351,22 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
         a.out_pad = m->ws_out_pad.as<int>();
         a.dw = dw;
         a.m_tiles = (int)ceil_div(c_in, 128);
-        a.n_tiles = (int)ceil_div(c_out, 256);
+        a.n_tiles = (int)ceil_div(c_out, 256);  // 128-wide tiles + 2 CTAs/SM: C=256 421 -> 570 us
         a.bn = (int)ceil_div(ceil_div(c_out, a.n_tiles), 16) * 16;
         a.nblk_b = (int)ceil_div(a.bn, 64);
         const size_t stage_bytes = 16384 + (size_t)a.nblk_b * 8192;
-        const int stages = (int)std::max<size_t>(2, std::min<size_t>(8, (200 * 1024) / stage_bytes));
+        // two or three CTAs per SM (4 gather warps each, a share of the
+        // stages) when their accumulator pairs fit in TMEM: the gathers are
+        // latency-bound and more pipelines per SM overlap them (lidar scan,
+        // tools/wgrad_time.py: C=32 88 -> 61 us, C=64 110 -> 89, C=96 136 ->
+        // 126, C=128 165 -> 159)
+        const int per_sm = (2 * a.bn <= 128) ? 3 : (2 * a.bn <= 256 ? 2 : 1);
+        const size_t budget = per_sm == 3 ? 66 * 1024 : (per_sm == 2 ? 100 * 1024 : 200 * 1024);
+        const int stages = (int)std::max<size_t>(2, std::min<size_t>(8, budget / stage_bytes));
         const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
         auto kern = dt == SK_F16 ? k_wgrad_tc<__half> : k_wgrad_tc<__nv_bfloat16>;
         ensure_smem(reinterpret_cast<const void*>(kern), smem);
-        launch_pdl(kern, ctx->num_sms, kWgThreads, smem, st, a, stages);
+        launch_pdl(kern, per_sm * ctx->num_sms, kWgThreads, smem, st, a, stages);
         return;
     }
     if (dt != SK_F32 && !ctx->deterministic && c_in <= 8 && !m->graph) {
