@@ -509,7 +509,7 @@ struct alignas(16) StepDesc {
 // warp 0 loads B with one 2D TMA tile. USE_TMA = false: warps 0-7 gather with
 // 16 B cp.async (reference path, kept for A/B measurement).
 template <typename T, int KC, bool USE_TMA, int SLABS, int PW>
-__global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : 2)
+__global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : (PW == 8 ? 2 : 3))
     k_gconv_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                const ConvArgs p, int stages, int acc_bufs) {
     constexpr int kProducerWarps = Roles<PW>::kProducerWarps;
@@ -1787,6 +1787,17 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStr
     else memset(&ta, 0, sizeof(ta));
     tb = make_tmap(a.b, dt, a.k_total, (long long)a.kd * a.n_total, KC, bn);
     const bool slab3 = a.cta_k != 32 && !tma && KC == 32 && nchunks == 3;
+    if (!tma && two_cta && bn <= 32 && !slab3) {
+        // three CTAs per SM (4 gather warps each, ~64 KB of stages) for
+        // C_out <= 32: a third independent pipeline per SM (C=32 lidar layer
+        // 44.0 -> 39.9 us; C_out = 64 needs more TMEM / smem than a third fits)
+        const int stages = (int)std::min<size_t>(kMaxStages, (64 * 1024) / slab_bytes);
+        if (stages >= 2) {
+            const int g3 = a.mode == 1 ? 3 * num_sms : std::min(a.items, 3 * num_sms);
+            launch_tc_variant<T, KC, false, 1, 4>(a, ta, tb, std::max(1, g3), stages, 2, slab_bytes, st);
+            return;
+        }
+    }
     if (!tma && two_cta && bn <= 128 && !slab3) {
         // TMEM per CTA <= 256 columns: double-buffer only up to BN = 64
         const int acc_bufs = 4 * bn <= 256 ? 2 : 1;
