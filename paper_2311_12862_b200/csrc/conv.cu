@@ -1790,11 +1790,13 @@ void launch_tc_kc(const ConvArgs& a, sk_dtype dt, int grid, int num_sms, cudaStr
     if (!tma && two_cta && bn <= 32 && !slab3) {
         // three CTAs per SM (4 gather warps each, ~64 KB of stages) for
         // C_out <= 32: a third independent pipeline per SM (C=32 lidar layer
-        // 44.0 -> 39.9 us; C_out = 64 needs more TMEM / smem than a third fits)
+        // 44.0 -> 39.9 us). C_out = 64 with 32-channel stages on this path:
+        // 58.4 -> 70.6 us (one accumulator pair; measured, not used)
         const int stages = (int)std::min<size_t>(kMaxStages, (64 * 1024) / slab_bytes);
         if (stages >= 2) {
+            const int acc3 = 4 * bn <= 128 ? 2 : 1;
             const int g3 = a.mode == 1 ? 3 * num_sms : std::min(a.items, 3 * num_sms);
-            launch_tc_variant<T, KC, false, 1, 4>(a, ta, tb, std::max(1, g3), stages, 2, slab_bytes, st);
+            launch_tc_variant<T, KC, false, 1, 4>(a, ta, tb, std::max(1, g3), stages, acc3, slab_bytes, st);
             return;
         }
     }

@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--splits", type=int, nargs="+", default=[1])
     ap.add_argument("--dgrad", action="store_true")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--cta-k", type=int, default=0, help="TilePreset cta_k (0 auto, 32 = 32-channel stages)")
     a = ap.parse_args()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json"))).get("bf16_tflops", 1675.9)
@@ -66,7 +67,7 @@ def main():
         for C in a.c:
             x = torch.randn(n, C, device="cuda", generator=g).half()
             w = (torch.randn(27, C, C, device="cuda", generator=g) / 40).half()
-            cfg = sk.DataflowConfig(sk.IMPLICIT_GEMM, s, sk.tile_large())
+            cfg = sk.DataflowConfig(sk.IMPLICIT_GEMM, s, sk.TilePreset(128, 0, a.cta_k, 128, 4))
             fl = 2.0 * pairs * C * C
             t = timeit(lambda: sk.conv_forward(m, x, w, cfg))
             steps = rows / 256
