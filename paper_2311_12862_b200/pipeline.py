@@ -73,6 +73,7 @@ class _Worker:
                       for _ in range(depth)]
         self.h_out = [torch.empty((max_voxels, c_out), dtype=dt).pin_memory() for _ in range(depth)]
         self.ev_in = [torch.cuda.Event() for _ in range(depth)]
+        self.cs = [None] * depth
         self.ev_used = [None] * depth
         self.ev_out = [torch.cuda.Event() for _ in range(depth)]
         self.d2h_bytes = 0
@@ -87,6 +88,10 @@ class _Worker:
         with torch.cuda.stream(self.s_in):
             self.d_c[slot][:n].copy_(coords, non_blocking=True)
             self.d_f[slot][:n].copy_(feats, non_blocking=True)
+            # the coordinate set (hash insert + its validation read-back) is
+            # built on the copy-in stream: the read-back then waits for this
+            # scan's H2D only, not for the previous forward on the compute stream
+            self.cs[slot] = _sk.CoordSet.create(self.d_c[slot][:n])
         self.ev_in[slot].record(self.s_in)
         self.h2d_bytes += coords.numel() * coords.element_size() + feats.numel() * feats.element_size()
 
@@ -116,7 +121,7 @@ class _Worker:
                         before_scan(j)
                     self.s_cmp.wait_event(self.ev_in[slot])
                     n = coords.shape[0]
-                    cs = _sk.CoordSet.create(self.d_c[slot][:n])
+                    cs, self.cs[slot] = self.cs[slot], None
                     # the device output slot is free once its previous D2H landed
                     self.s_cmp.wait_event(self.ev_out[slot])
                     y, _ = self.net.forward(cs, self.d_f[slot][:n], out=self.d_out[slot])
