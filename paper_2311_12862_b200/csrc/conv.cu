@@ -2112,9 +2112,9 @@ void conv_forward_prepare(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, s
                           int c_in, int c_out, cudaStream_t st) {
     if (m->n_out == 0 || m->graph) return;
     // mirrors conv_forward's (dgrad = false) dispatch below
-    if (cfg.kind == SK_IMPLICIT_GEMM && dt != SK_F32 && m->kd <= 27 && c_out == 32 &&
-        (c_in == 4 || c_in == 3 || c_in == 1))
-        return;  // conv_small_cin reads the raw OS map
+    if (cfg.kind == SK_IMPLICIT_GEMM && dt != SK_F32 && m->kd <= 27 &&
+        ((c_in == 4 && c_out % 16 == 0) || (c_out == 32 && (c_in == 3 || c_in == 1))))
+        return;  // the small-C_in paths (im2col + dense GEMM, CUDA cores) read the raw OS map
     int k_eff = c_in;
     if (dt != SK_F32 && c_in % 8 != 0 && c_out % 16 == 0) k_eff = (c_in + 7) / 8 * 8;
     if (m->identity && tc_ok(dt, k_eff, c_out) && !ctx->deterministic) return;  // dense GEMM
