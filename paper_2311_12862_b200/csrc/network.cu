@@ -260,11 +260,46 @@ __global__ void k_accum(float* __restrict__ g, const T* __restrict__ dx, long lo
          i += (long long)gridDim.x * blockDim.x)
         g[i] += ld_f(dx, i);
 }
+// g1 += dx and g2 += dx (a two-input layer's gradient to both producers, dx
+// read once); 4 elements per thread when n % 4 == 0
+template <typename T>
+__global__ void k_accum2(float* __restrict__ g1, float* __restrict__ g2, const T* __restrict__ dx,
+                         long long n) {
+    pdl_wait();
+    pdl_trigger();
+    const long long n4 = n / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float a = ld_f(dx, 4 * i), b = ld_f(dx, 4 * i + 1), c = ld_f(dx, 4 * i + 2),
+                    d = ld_f(dx, 4 * i + 3);
+        float4 u = reinterpret_cast<float4*>(g1)[i];
+        u.x += a; u.y += b; u.z += c; u.w += d;
+        reinterpret_cast<float4*>(g1)[i] = u;
+        float4 v = reinterpret_cast<float4*>(g2)[i];
+        v.x += a; v.y += b; v.z += c; v.w += d;
+        reinterpret_cast<float4*>(g2)[i] = v;
+    }
+    for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float a = ld_f(dx, i);
+        g1[i] += a;
+        g2[i] += a;
+    }
+}
 template <typename T>
 __global__ void k_cast_from_f32(const float* __restrict__ g, long long n, T* __restrict__ y) {
     pdl_wait();
     pdl_trigger();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+    const long long n4 = n / 4;  // float4 in, 4 elements out per iteration
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(g)[i];
+        y[4 * i] = cvt_f<T>(v.x);
+        y[4 * i + 1] = cvt_f<T>(v.y);
+        y[4 * i + 2] = cvt_f<T>(v.z);
+        y[4 * i + 3] = cvt_f<T>(v.w);
+    }
+    for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         y[i] = cvt_f<T>(g[i]);
 }
@@ -368,7 +403,8 @@ struct sk_net {
     std::vector<char> fused_input;  // L's xsum is produced by a fused producer
     std::vector<size_t> wgrad_off;
     size_t wgrad_total = 0;
-    std::vector<DevBuf> gout;  // fp32 output grads (backward)
+    DevBuf gout_slab;              // fp32 output grads of every layer (backward), one slab
+    std::vector<float*> gout;      // layer i's [n_out x c_out] view into gout_slab
     int64_t map_builds = 0;
     bool overlap = true;                      // overlapped map builds (sk_net_set_overlap)
     bool pdl = true;                          // programmatic dependent launch (sk_net_set_pdl)
@@ -846,33 +882,48 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
     DevBuf dy, dx;
     dy.alloc(std::max<size_t>(max_out, 1) * n->es(), st);
     dx.alloc(std::max<size_t>(max_in, 1) * n->es(), st);
+    if (!accumulate) {  // the range's weight gradients are contiguous: one fill, not one per layer
+        const size_t a = n->wgrad_off[lo];
+        const size_t b = n->wgrad_off[hi] + (size_t)n->kd[hi] * n->spec.layers[hi].c_in *
+                                                n->spec.layers[hi].c_out;
+        SK_CUDA(cudaMemsetAsync(wgrad_flat + a, 0, (b - a) * 4, st));
+    }
     for (int i = hi; i >= lo; --i) {
         const LayerSpec& l = n->spec.layers[i];
         const long long no = (long long)n->out_set[i]->n * l.c_out;
         const long long ni = (long long)n->in_set[i]->n * l.c_in;
         by_dtype(n->dt, [&](auto tag) {
             using T = decltype(tag);
-            launch_pdl(k_cast_from_f32<T>, grid_for(no), 256, 0, st, n->gout[i].as<float>(), no, (T*)dy.p);
+            launch_pdl(k_cast_from_f32<T>, grid_for((no + 3) / 4), 256, 0, st, n->gout[i], no, (T*)dy.p);
         });
         const int g = n->group_of[i];
         conv_wgrad(n->ctx, n->exec_map[i], layer_cfg(n, 2, i), n->dt, l.c_in, l.c_out, n->x_ptr[i],
-                   dy.p, wgrad_flat + n->wgrad_off[i], st, accumulate);
+                   dy.p, wgrad_flat + n->wgrad_off[i], st, true);  // range zeroed above
         if (l.inputs.empty()) continue;  // no gradient w.r.t. the network input
         if (l.inputs.size() == 1) {
             // single producer: dgrad accumulates straight into its fp32 gradient
             // sum in the conv epilogue (no dx round trip, no k_accum launch)
             const int j = n->spec.index(l.inputs[0]);
             conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, i), n->dt, l.c_in, l.c_out, dy.p,
-                         n->w[i].p, nullptr, true, st, nullptr, nullptr, n->gout[j].as<float>());
+                         n->w[i].p, nullptr, true, st, nullptr, nullptr, n->gout[j]);
             continue;
         }
         conv_forward(n->ctx, n->exec_map[i], layer_cfg(n, 1, i), n->dt, l.c_in, l.c_out, dy.p,
                      n->w[i].p, dx.p, true, st);
+        if (l.inputs.size() == 2) {  // both producers in one pass over dx
+            const int j1 = n->spec.index(l.inputs[0]), j2 = n->spec.index(l.inputs[1]);
+            by_dtype(n->dt, [&](auto tag) {
+                using T = decltype(tag);
+                launch_pdl(k_accum2<T>, grid_for((ni + 3) / 4), 256, 0, st, n->gout[j1], n->gout[j2],
+                           (const T*)dx.p, ni);
+            });
+            continue;
+        }
         for (const std::string& pn : l.inputs) {
             const int j = n->spec.index(pn);
             by_dtype(n->dt, [&](auto tag) {
                 using T = decltype(tag);
-                launch_pdl(k_accum<T>, grid_for(ni), 256, 0, st, n->gout[j].as<float>(), (const T*)dx.p, ni);
+                launch_pdl(k_accum<T>, grid_for(ni), 256, 0, st, n->gout[j], (const T*)dx.p, ni);
             });
         }
     }
@@ -1118,16 +1169,19 @@ sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, 
                  "backward before a successful forward");
         cudaStream_t st = S(stream);
         if (layer_hi == L - 1) {
-            n->gout.resize(L);
-            for (int i = 0; i < L; ++i) {
-                size_t b = (size_t)std::max(n->out_set[i]->n, 1) * n->spec.layers[i].c_out * 4;
-                if (n->gout[i].bytes != b) n->gout[i].alloc(b, st);
-                SK_CUDA(cudaMemsetAsync(n->gout[i].p, 0, b, st));
-            }
+            // every layer's fp32 output gradient in one slab, zeroed by one fill
+            std::vector<size_t> off(L + 1, 0);
+            for (int i = 0; i < L; ++i)
+                off[i + 1] = off[i] + ((size_t)std::max(n->out_set[i]->n, 1) *
+                                           n->spec.layers[i].c_out + 3) / 4 * 4;  // 16 B aligned
+            if (n->gout_slab.bytes < off[L] * 4) n->gout_slab.alloc(off[L] * 4, st);
+            SK_CUDA(cudaMemsetAsync(n->gout_slab.p, 0, off[L] * 4, st));
+            n->gout.assign(L, nullptr);
+            for (int i = 0; i < L; ++i) n->gout[i] = n->gout_slab.as<float>() + off[i];
             const long long no = (long long)n->out_set[L - 1]->n * n->spec.layers[L - 1].c_out;
             by_dtype(n->dt, [&](auto tag) {
                 using T = decltype(tag);
-                launch_pdl(k_accum<T>, grid_for(no), 256, 0, st, n->gout[L - 1].as<float>(),
+                launch_pdl(k_accum<T>, grid_for(no), 256, 0, st, n->gout[L - 1],
                                                          (const T*)d_grad_out, no);
             });
         }
