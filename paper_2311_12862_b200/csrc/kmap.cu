@@ -1081,13 +1081,16 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
                                      slot.as<int>(), q.as<int4>());
     launch_pdl(k_down_flag, g, 256, 0, st, slot.as<int>(), out->table.as<ulonglong2>(), n, flag.as<int>());
     scan_exclusive_i32(flag.as<int>(), pos.as<int>(), n, pos.as<int>() + n, st);
-    int h_count = 0;
-    read_back(st, {{pos.as<int>() + n, 4}}, &h_count);
-    out->n = h_count;
-    out->coords.alloc((size_t)std::max(out->n, 1) * 16, st);
+    // the output coordinates are sized by the upper bound (n_out <= n), so the
+    // compaction is queued before the count read-back and runs while the host
+    // waits, instead of after it on the map stream's critical path
+    out->coords.alloc((size_t)n * 16, st);
     launch_pdl(k_down_compact, g, 256, 0, st, flag.as<int>(), pos.as<int>(), slot.as<int>(),
                                       q.as<int4>(), n, out->table.as<ulonglong2>(),
                                       out->coords.as<int4>());
+    int h_count = 0;
+    read_back(st, {{pos.as<int>() + n, 4}}, &h_count);
+    out->n = h_count;
     out->has_table = true;
     return out;
 }
