@@ -52,3 +52,23 @@ def test_cubin_is_sm100a_with_tcgen05():
     assert "sm_100a" in out
     assert "UTCHMMA" in out or "UTCMMA" in out  # tcgen05.mma
     assert "LDTM" in out                           # tcgen05.ld
+
+
+def test_tuner_space_without_gpu():
+    """default_space (tuner.cpp:9-26) is host code: the reference's 12 configs
+    in its order, then the B200 kernel variants the TilePreset fields select
+    (one CTA per SM, TMA gather4, 32-channel stages, one-tile work items)."""
+    from paper_2311_12862_b200.network import default_space
+    from paper_2311_12862_b200 import sparse as sk
+    space = default_space()
+    ref = [sk.DataflowConfig(sk.GATHER_GEMM_SCATTER), sk.DataflowConfig(sk.FETCH_ON_DEMAND)]
+    for s in range(5):
+        for t in (sk.tile_small(), sk.tile_large()):
+            ref.append(sk.DataflowConfig(sk.IMPLICIT_GEMM, s, t))
+    assert space[:12] == ref
+    extra = space[12:]
+    assert len(extra) == 9 and all(c.kind == sk.IMPLICIT_GEMM for c in extra)
+    assert {c.tile.cta_m for c in extra} == {64, 128, 256}
+    assert any(c.tile.load_width == 1 for c in extra)      # TMA gather4
+    assert any(c.tile.cta_k == 32 for c in extra)          # single-slab 32-channel stages
+    assert len({c.name() for c in space}) == len(space)    # names tell the variants apart
