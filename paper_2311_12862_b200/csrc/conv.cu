@@ -113,7 +113,6 @@ struct ConvArgs {
     int offset_only;  // >= 0: WS mode only tiles of this offset
     int* sched;       // dynamic item queue {next item, CTAs done} (self-resetting), or null
     int single;       // OS mode: one 128-row tile per work item (cta_m 64) instead of two
-    int col_chunks;   // OS mode: each tile's columns split over this many items (red.add)
     // tile preferences from the layer's TilePreset (include/sk200.h):
     int cta_m;        // 256: one CTA per SM; otherwise two per SM when C_out <= 128 fits
     int cta_k;        // channels per pipeline stage: 0 auto, 16 / 32 / 64, 96 = 3 x 32 slabs
@@ -194,13 +193,11 @@ __device__ Item decode(const ConvArgs& p, int item) {
     }
     if (p.mode == 0) {
         const int tpi = p.single ? 1 : 2;  // 128-row tiles per item
-        const int cc = p.col_chunks > 1 ? p.col_chunks : 1;
-        const int per = (p.single ? p.n_tiles : pairs_of(p.n_tiles)) * p.n_ntiles * cc;
+        const int per = (p.single ? p.n_tiles : pairs_of(p.n_tiles)) * p.n_ntiles;
         it.s = p.split_only >= 0 ? p.split_only : item / per;
         const int rem = p.split_only >= 0 ? item : item % per;
+        it.t2 = rem / p.n_ntiles;  // item index within the split
         it.nt = rem % p.n_ntiles;
-        const int q = (rem / p.n_ntiles) % cc;  // column chunk
-        it.t2 = rem / p.n_ntiles / cc;          // item index within the split
         it.col_begin = p.split_begin[it.s];
         it.w = p.split_begin[it.s + 1] - it.col_begin;
         it.row0 = (long long)it.t2 * tpi * kTileM;
@@ -215,21 +212,6 @@ __device__ Item decode(const ConvArgs& p, int item) {
         }
         it.biw0 = it.w < 64 ? it.w : 64;
         it.bw1 = it.w - 64;
-        if (cc > 1) {
-            // keep columns [lo, hi) of the split: column j < 64 is bit biw0-1-j
-            // of m0, column j >= 64 bit bw1-1-(j-64) of m1 (big-endian words)
-            const int lo = q * it.w / cc, hi = (q + 1) * it.w / cc;
-            auto keep = [](int width, int a, int b) -> unsigned long long {  // columns [a,b) of a word
-                a = max(0, min(a, width));
-                b = max(0, min(b, width));
-                if (b <= a) return 0ull;
-                const int n = b - a;
-                const unsigned long long ones = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
-                return ones << (width - b);
-            };
-            it.m0 &= keep(it.biw0, lo, hi);
-            it.m1 &= it.bw1 > 0 ? keep(it.bw1, lo - 64, hi - 64) : 0ull;
-        }
     } else {
         int tile = item / p.n_ntiles;
         it.nt = item % p.n_ntiles;
@@ -1139,9 +1121,8 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, PW == 16 ? 1 : (PW == 8 ?
             tc_fence_after();
             const bool empty_tile = (it.m0 | it.m1) == 0;
             const int n0 = it.nt * BN;
-            const int hn = (empty_tile && p.out_mode == 2) ? 0 : it.halves;  // nothing to add
 #pragma unroll 1
-            for (int h = 0; h < hn; ++h) {
+            for (int h = 0; h < it.halves; ++h) {
                 for (int c0 = 0; c0 < BN; c0 += 16) {
                     uint32_t v[16];
                     if (!empty_tile) {
@@ -2256,19 +2237,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         a.n_rows_valid = m->n_out;
         // work items: 256 rows (two MMA tiles), or one 128-row tile (cta_m 64)
         const int pairs = a.single ? a.n_tiles : (a.n_tiles + 1) / 2;
-        // Small layers (deep levels, strided maps): fewer work items than
-        // resident CTAs, each walking up to K^D columns serially. Then each
-        // tile's columns are split over up to 4 items that accumulate with
-        // fp32 red.add (split-K over the offsets, keeping the prepared row
-        // order: no re-sort, unlike splits), so more SMs share the layer.
-        // (MinkUNet: tuned warm-map forward 1.816 -> 1.791 ms, per-layer sum
-        // 2.145 -> 2.119 ms, tools/layer_times.py)
-        int cc = 1;
-        const int base_items = pr->num_splits * pairs * a.n_ntiles;
-        if (tc && !det && base_items <= ctx->num_sms)
-            cc = std::min(4, std::max(1, (2 * ctx->num_sms) / std::max(1, base_items)));
-        a.col_chunks = cc;
-        if (pr->num_splits == 1 && cc == 1) {
+        if (pr->num_splits == 1) {
             a.items = pairs * a.n_ntiles;
             a.y = y_accum ? (void*)y_accum : y;
             a.residual = y_accum ? nullptr : residual;
@@ -2294,7 +2263,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
                 }
             } else {
                 a.out_mode = 2;
-                a.items = pr->num_splits * pairs * a.n_ntiles * cc;
+                a.items = pr->num_splits * pairs * a.n_ntiles;
                 launch_gconv(ctx, dt, a, st);
             }
             if (!y_accum && (dt != SK_F32 || residual))
