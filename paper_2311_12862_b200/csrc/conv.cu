@@ -2059,7 +2059,8 @@ __global__ void k_small_cin_weights(const T* __restrict__ w, int kd, int ci, int
 template <typename T>
 bool conv_small_cin_dense(sk_ctx* ctx, sk_dtype dt, const sk_kmap* m, int c_in, int c_out,
                           const void* x, const void* w, void* y, int cta_n, cudaStream_t st) {
-    if (c_in != 4 || c_out % 16 != 0) return false;
+    // 8 B neighbour-row loads: the feature rows (4 halves) must be 8 B aligned
+    if (c_in != 4 || c_out % 16 != 0 || (reinterpret_cast<uintptr_t>(x) & 7) != 0) return false;
     const int k_pad = (int)ceil_div((long long)m->kd * c_in, 16) * 16;
     DevBuf a, b;
     a.alloc((size_t)m->n_out * k_pad * sizeof(T), st);
@@ -2085,7 +2086,9 @@ bool conv_small_cin(const sk_kmap* m, int c_in, int c_out, const void* x, const 
         return true;
     };
     if (m->kd > 27) return false;
-    if (c_in == 4 && c_out == 32) return launch(k_conv_small_cin<T, 4, 32>);
+    // CI = 4 half rows are read as 8 B vectors: the feature base must be 8 B aligned
+    if (c_in == 4 && c_out == 32 && (reinterpret_cast<uintptr_t>(x) & 7) == 0)
+        return launch(k_conv_small_cin<T, 4, 32>);
     if (c_in == 3 && c_out == 32) return launch(k_conv_small_cin<T, 3, 32>);
     if (c_in == 1 && c_out == 32) return launch(k_conv_small_cin<T, 1, 32>);
     return false;
