@@ -195,3 +195,26 @@ def test_identity_k1_dense_path(env, restatement, cin, cout, dtype):
         assert max_rel_err(y.double().cpu().numpy(), y_ref) <= TOL_HALF, cfg.name()
         dx = sk.conv_dgrad(m, dy.cuda(), w.cuda(), cfg)
         assert max_rel_err(dx.double().cpu().numpy(), dx_ref) <= TOL_HALF, cfg.name()
+
+
+def test_stem_paths_and_misaligned_features(env, restatement):
+    """The 4-channel stem runs as a neighbour gather + one dense tcgen05 GEMM
+    (8 B row loads); a feature base that is not 8 B aligned takes the general
+    path. Both match the oracle."""
+    torch, sk = env
+    c, o, m = make(sk, torch, 91, 4000, 1)
+    ent, _ = m.os()
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(m.n_in, 4, generator=g).half()
+    w = (torch.randn(27, 4, 64, generator=g) / 10).half()
+    y_ref = restatement.conv(ent, x.double().numpy(), w.double().numpy())
+    cfg = sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large())
+    y = sk.conv_forward(m, x.cuda(), w.cuda(), cfg)
+    buf = torch.empty(m.n_in * 4 + 1, dtype=torch.float16, device="cuda")
+    xm = buf[1:].view(m.n_in, 4)  # base 2 B past an 8 B boundary
+    xm.copy_(x.cuda())
+    assert xm.data_ptr() % 8 != 0
+    y2 = sk.conv_forward(m, xm, w.cuda(), cfg)
+    torch.cuda.synchronize()
+    assert max_rel_err(y.double().cpu().numpy(), y_ref) <= TOL_HALF
+    assert max_rel_err(y2.double().cpu().numpy(), y_ref) <= TOL_HALF
