@@ -22,8 +22,9 @@ def timeit(fn, warm=3, reps=10):
 c = sk.CoordSet.create(torch.from_numpy(lidar_scan(200_000, seed=1)).cuda())
 m = sk.build_kmap(c, c, 3, 1)
 tiles = {"large": sk.tile_large(), "m256": sk.TilePreset(256, 0, 0, 128, 4),
-         "k32": sk.TilePreset(128, 0, 32, 128, 4), "tma": sk.TilePreset(128, 0, 0, 128, 1)}
-for ci, co in [(32, 96), (128, 96), (64, 128), (96, 96), (32, 64)]:
+         "k32": sk.TilePreset(128, 0, 32, 128, 4), "tma": sk.TilePreset(128, 0, 0, 128, 1),
+         "m64": sk.TilePreset(64, 0, 0, 128, 4), "m64k32": sk.TilePreset(64, 0, 32, 128, 4)}
+for ci, co in [(96, 96), (32, 96), (64, 64), (128, 128)]:
     x = torch.randn(m.n_in, ci, device="cuda").half()
     w = (torch.randn(27, ci, co, device="cuda") / 40).half()
     y = torch.empty(m.n_out, co, device="cuda").half()
