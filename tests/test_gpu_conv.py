@@ -218,3 +218,24 @@ def test_stem_paths_and_misaligned_features(env, restatement):
     torch.cuda.synchronize()
     assert max_rel_err(y.double().cpu().numpy(), y_ref) <= TOL_HALF
     assert max_rel_err(y2.double().cpu().numpy(), y_ref) <= TOL_HALF
+
+
+def test_dynamic_item_queue_slots_wrap(env, restatement):
+    """Every tensor-core conv launch takes one of the context's 16384 dynamic
+    item-queue counters and its last CTA re-zeroes it: more launches than
+    slots (the ring wraps) still give the oracle's result every time."""
+    torch, sk = env
+    c, o, m = make(sk, torch, 123, 600, 1)
+    ent, _ = m.os()
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(m.n_in, 16, generator=g).half()
+    w = (torch.randn(27, 16, 16, generator=g) / 20).half()
+    y_ref = restatement.conv(ent, x.double().numpy(), w.double().numpy())
+    xd, wd = x.cuda(), w.cuda()
+    cfg = sk.DataflowConfig(sk.IMPLICIT_GEMM, 1, sk.tile_large())
+    y = torch.empty(m.n_out, 16, device="cuda", dtype=torch.float16)
+    for i in range(17000):
+        sk.conv_forward(m, xd, wd, cfg, out=y)
+        if i % 4250 == 0 or i == 16999:
+            torch.cuda.synchronize()
+            assert max_rel_err(y.double().cpu().numpy(), y_ref) <= TOL_HALF, i
