@@ -51,14 +51,23 @@ def timeit(fn, warm=2, reps=5):
 
 
 def space():
-    out = [sk.DataflowConfig(sk.GATHER_GEMM_SCATTER), sk.DataflowConfig(sk.FETCH_ON_DEMAND)]
-    for s in range(5):
-        for t in (sk.tile_small(), sk.tile_large()):
-            out.append(sk.DataflowConfig(sk.IMPLICIT_GEMM, s, t))
-    return out
+    """The tuner's whole space: the reference's 12 dataflow configs
+    (tuner.cpp:9-26) then the B200 kernel variants (sk_tune_space_entry)."""
+    from paper_2311_12862_b200.network import default_space
+    return default_space()
+
+
+PEAK = 1675.9  # MEASURED_PEAKS.json bf16_tflops (burst), overridden in main()
 
 
 def main():
+    global PEAK
+    try:
+        import json
+        PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                           "MEASURED_PEAKS.json")))["bf16_tflops"]
+    except Exception:
+        pass
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="fewer points (CI / smoke)")
     ap.add_argument("--out", default=None)
@@ -104,13 +113,13 @@ def main():
              "2*pairs*C^2 / best time (padded MACs not credited).", "",
              "| N | K | mode | C | pairs | " + " | ".join(n.replace("implicit_gemm_", "ig_")
                                                       .replace("_offline", "") for n in names)
-             + " | autotuned (best) | TF/s | best / default GGS |",
-             "|" + "---|" * (len(names) + 9)]
+             + " | autotuned (best) | TF/s | frac | best / default GGS |",
+             "|" + "---|" * (len(names) + 10)]
     for n, K, mode, C, pairs, res, best, flops in rows:
         lines.append(f"| {n} | {K} | {mode} | {C} | {pairs} | "
                      + " | ".join(f"{res[nm]:.4f}" for nm in names)
                      + f" | {best.replace('implicit_gemm_', 'ig_').replace('_offline', '')} "
-                       f"{res[best]:.4f} | {flops / res[best] / 1e9:.1f} | "
+                       f"{res[best]:.4f} | {flops / res[best] / 1e9:.1f} | {flops / res[best] / 1e9 / PEAK:.3f} | "
                        f"{res[best] / res[names[0]]:.2f} |")
     txt = "\n".join(lines) + "\n"
     if a.out:
