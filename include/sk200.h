@@ -211,7 +211,11 @@ sk_status sk_kmap_export_split(sk_kmap* map, int splits, int pad_multiple, int s
 /* ---- dataflows (exec.hpp:86-124) ---------------------------------------------
  * dtype: SK_F16/SK_BF16 -> tcgen05 tensor cores (fp32 accumulate in TMEM);
  * SK_F32 -> fp32 SIMT path (the 1e-5 parity path). x: [n_in][c_in],
- * w: [K^D][c_in][c_out], y: [n_out][c_out], all `dtype`. */
+ * w: [K^D][c_in][c_out], y: [n_out][c_out], all `dtype`. Kernels are launched
+ * with programmatic stream serialization (each waits for its predecessor on
+ * the stream before touching memory; a runner turns this off with
+ * sk_net_set_pdl, direct calls always use it): ordering and results are those
+ * of plain stream order. */
 
 /* conv_forward (exec.cpp:368-383) — dispatches on cfg->kind; implicit GEMM
  * with reorder=offline prepares (cached) the map for cfg->splits. */
