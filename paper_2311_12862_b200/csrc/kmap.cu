@@ -131,49 +131,68 @@ __global__ void k_down_compact(const int* __restrict__ flag, const int* __restri
 // ---- 4x4x4 block index (stride-1 query path) ---------------------------------
 constexpr int kBlkEmpty = 0x7FFFFFFF;
 
-// one thread per voxel: the first thread of a block claims it (CAS on the key),
-// takes an id, fills its 64 cells with kBlkEmpty and publishes the id; the
-// others wait for the id. Cells keep the FIRST row (atomicMin), like emplace.
-__global__ void k_block_insert(const int4* __restrict__ coords, int n, ulonglong2* __restrict__ bt,
-                               uint64_t mask, int* __restrict__ dense, int* __restrict__ count) {
+// Two passes, no cross-warp waiting. k_block_claim: one lane per distinct
+// block key in the warp inserts it (CAS); the winner takes an id from the
+// counter, publishes it in the slot and fills the block's 64 cells with
+// kBlkEmpty. k_block_fill (next launch: every id is published) looks the id up
+// and keeps the FIRST row per cell (atomicMin), like emplace.
+__global__ void k_block_claim(const int4* __restrict__ coords, int n, ulonglong2* __restrict__ bt,
+                              uint64_t mask, int* __restrict__ dense, int* __restrict__ count) {
     pdl_wait();
     pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = i < n;
     const int4 c = live ? coords[i] : make_int4(0, 0, 0, 0);
     const unsigned long long key = live ? pack_key(c.x, c.y >> 2, c.z >> 2, c.w >> 2) : kEmpty;
-    // neighbouring voxels mostly share a block: one lane per distinct key in
-    // the warp inserts, the others take its id (cuts CAS/spin contention)
+    // neighbouring voxels mostly share a block: one CAS per distinct key
     const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(peers) - 1;
     const int lane = threadIdx.x & 31;
-    unsigned bid = 0;
-    if (live && lane == leader) {
-        uint64_t s = hash_slot(key, mask);
+    bool win = false;
+    uint64_t s = hash_slot(key, mask);
+    if (live && lane == __ffs(peers) - 1) {
         for (;;) {
+            // ~8 warps claim each block: an L2 read finds most keys already
+            // there, so only the first claim pays the (same-address) CAS
+            const unsigned long long seen = __ldcg(slot_key(bt, s));
+            if (seen == key) break;
+            if (seen != (unsigned long long)kEmpty) {
+                s = (s + 1) & mask;
+                continue;
+            }
             const unsigned long long prev = atomicCAS(slot_key(bt, s), (unsigned long long)kEmpty, key);
             if (prev == (unsigned long long)kEmpty) {
-                bid = (unsigned)atomicAdd(count, 1);
-                int4* d = reinterpret_cast<int4*>(dense + (size_t)bid * 64);
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    d[j] = make_int4(kBlkEmpty, kBlkEmpty, kBlkEmpty, kBlkEmpty);
-                __threadfence();
-                atomicExch(slot_val(bt, s), bid);
+                win = true;
                 break;
             }
-            if (prev == key) {
-                volatile unsigned* v = slot_val(bt, s);
-                while ((bid = *v) == 0xFFFFFFFFu) {
-                }
-                __threadfence();
-                break;
-            }
+            if (prev == key) break;
             s = (s + 1) & mask;
         }
     }
-    bid = __shfl_sync(0xffffffffu, bid, leader);
-    if (!live) return;
+    // ids: one counter add per warp (a per-block add serialised on the counter)
+    const unsigned wins = __ballot_sync(0xffffffffu, win);
+    if (!wins) return;
+    unsigned base = 0;
+    if (lane == __ffs(wins) - 1) base = (unsigned)atomicAdd(count, __popc(wins));
+    base = __shfl_sync(0xffffffffu, base, __ffs(wins) - 1);
+    if (!win) return;
+    const unsigned bid = base + __popc(wins & ((1u << lane) - 1));
+    int4* d = reinterpret_cast<int4*>(dense + (size_t)bid * 64);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) d[j] = make_int4(kBlkEmpty, kBlkEmpty, kBlkEmpty, kBlkEmpty);
+    *slot_val(bt, s) = bid;
+}
+
+__device__ __forceinline__ int block_lookup(const ulonglong2* __restrict__ bt, uint64_t mask,
+                                            unsigned long long key);
+
+__global__ void k_block_fill(const int4* __restrict__ coords, int n, const ulonglong2* __restrict__ bt,
+                             uint64_t mask, int* __restrict__ dense) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 c = coords[i];
+    const int bid = block_lookup(bt, mask, pack_key(c.x, c.y >> 2, c.z >> 2, c.w >> 2));
     const int local = ((c.y & 3) << 4) | ((c.z & 3) << 2) | (c.w & 3);
     atomicMin(dense + (size_t)bid * 64 + local, i);
 }
@@ -190,10 +209,13 @@ __device__ __forceinline__ int block_lookup(const ulonglong2* __restrict__ bt, u
 }
 
 // Stride-1 (submanifold or generative) query over the input's block index:
-// one thread per output row; the row's neighbour blocks (at most 2 per axis
-// for K=3, 3 for K=5) are looked up once, then every offset is a 4 B load from
-// a 256 B block array that neighbouring rows share (L1). Same outputs as
-// k_kmap_query: OS tile via smem, big-endian masks, per-block counts.
+// one thread per output row. Per axis the K neighbours span one or two
+// blocks (lo, lo+1); the row's 2x2x2 neighbour-block ids are looked up once
+// (only distinct ones probe the table). A block's cells are z-minor, so for
+// each (x, y) offset the K z-neighbours are read as one or two aligned 16 B
+// z-rows (K=3: 9-18 loads per row instead of 27 scattered 4 B loads; K=5: 50
+// instead of 125). Same outputs as k_kmap_query: OS tile via smem, big-endian
+// masks, per-block counts.
 template <int K>
 __global__ void __launch_bounds__(kQB) k_kmap_query_blk(
     const int4* __restrict__ out_coords, int n_out, const ulonglong2* __restrict__ bt,
@@ -210,55 +232,61 @@ __global__ void __launch_bounds__(kQB) k_kmap_query_blk(
     for (int k = t; k < KD; k += kQB) cnt[k] = 0;
     __syncthreads();
     unsigned long long m0 = 0, m1 = 0;
-    if (row < n_out) {
-        const int4 q = out_coords[row];
+    // every lane runs the (unrolled) offset loop so the per-offset counts are
+    // warp ballots, not 32-way contended shared atomics; rows past n_out see
+    // no blocks
+    const bool live = row < n_out;
+    {
+        const int4 q = live ? out_coords[row] : make_int4(0, 0, 0, 0);
         const int lx = q.y & 3, ly = q.z & 3, lz = q.w & 3;
         const int bx = q.y >> 2, by = q.z >> 2, bz = q.w >> 2;
-        // neighbour-block ids, index (dx+1)*9 + (dy+1)*3 + (dz+1); -1 = absent
-        int bid[27];
+        const int lox = (lx - H) >> 2, loy = (ly - H) >> 2, loz = (lz - H) >> 2;  // -1 or 0
+        const int nx = ((lx + H) >> 2) - lox, ny = ((ly + H) >> 2) - loy, nz = ((lz + H) >> 2) - loz;
+        // bid[ix][iy][iz]: block (lo+i) per axis, -1 = absent or not needed
+        // (an axis whose neighbours stay in one block never selects i = 1)
+        int bid[2][2][2];
 #pragma unroll
-        for (int dx = -1; dx <= 1; ++dx)
+        for (int ix = 0; ix < 2; ++ix)
 #pragma unroll
-            for (int dy = -1; dy <= 1; ++dy)
+            for (int iy = 0; iy < 2; ++iy)
 #pragma unroll
-                for (int dz = -1; dz <= 1; ++dz) {
-                    const bool need = ((lx - H) >> 2) <= dx && dx <= ((lx + H) >> 2) &&
-                                      ((ly - H) >> 2) <= dy && dy <= ((ly + H) >> 2) &&
-                                      ((lz - H) >> 2) <= dz && dz <= ((lz + H) >> 2);
-                    int id = -1;
-                    if (need && packable(q.x, bx + dx, by + dy, bz + dz))
-                        id = block_lookup(bt, mask, pack_key(q.x, bx + dx, by + dy, bz + dz));
-                    bid[(dx + 1) * 9 + (dy + 1) * 3 + (dz + 1)] = id;
+                for (int iz = 0; iz < 2; ++iz) {
+                    const int x = bx + lox + ix, y = by + loy + iy, z = bz + loz + iz;
+                    bid[ix][iy][iz] = (live && ix <= nx && iy <= ny && iz <= nz && packable(q.x, x, y, z))
+                                          ? block_lookup(bt, mask, pack_key(q.x, x, y, z)) : -1;
                 }
+        // the z window: concat(row at lo, row at lo+1)[zb + c], c = 0..K-1
+        const int zb = lz - H - 4 * loz;  // 0..3
+        const int4 kE = make_int4(kBlkEmpty, kBlkEmpty, kBlkEmpty, kBlkEmpty);
 #pragma unroll
-        for (int a = -H; a <= H; ++a)
+        for (int a = 0; a < K; ++a)
 #pragma unroll
-            for (int b = -H; b <= H; ++b)
+            for (int b = 0; b < K; ++b) {
+                const int px = lx + a - H, py = ly + b - H;
+                const int ix = (px >> 2) - lox, iy = (py >> 2) - loy;
+                const int id0 = ix ? (iy ? bid[1][1][0] : bid[1][0][0]) : (iy ? bid[0][1][0] : bid[0][0][0]);
+                const int id1 = ix ? (iy ? bid[1][1][1] : bid[1][0][1]) : (iy ? bid[0][1][1] : bid[0][0][1]);
+                const int zrow = ((px & 3) << 4) | ((py & 3) << 2);
+                const int4 r0 = id0 >= 0 ? __ldg(reinterpret_cast<const int4*>(dense + (size_t)id0 * 64 + zrow)) : kE;
+                const int4 r1 = id1 >= 0 ? __ldg(reinterpret_cast<const int4*>(dense + (size_t)id1 * 64 + zrow)) : kE;
+                const int w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
-                for (int c = -H; c <= H; ++c) {
-                    const int k = ((a + H) * K + (b + H)) * K + (c + H);  // lexicographic
-                    const int px = lx + a, py = ly + b, pz = lz + c;
-                    const int sx = px >> 2, sy = py >> 2, sz = pz >> 2;  // -1, 0, +1
-                    // 27-way select keeps the ids in registers (compile-time indices)
-                    int id = -1;
+                for (int c = 0; c < K; ++c) {
+                    int v = w[c];
 #pragma unroll
-                    for (int u = 0; u < 27; ++u)
-                        if (u == (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1)) id = bid[u];
-                    int j = -1;
-                    if (id >= 0) {
-                        const int v = __ldg(dense + (size_t)id * 64 + ((px & 3) << 4) +
-                                            ((py & 3) << 2) + (pz & 3));
-                        j = v == kBlkEmpty ? -1 : v;
-                    }
+                    for (int s2 = 1; s2 < 4; ++s2)
+                        if (zb == s2) v = w[s2 + c];
+                    const int k = (a * K + b) * K + c;  // lexicographic
+                    const int j = v == kBlkEmpty ? -1 : v;
                     tile[t * KD + k] = j;
+                    const unsigned hit = __ballot_sync(0xffffffffu, j >= 0);
+                    if ((t & 31) == 0 && hit) atomicAdd(&cnt[k], __popc(hit));
                     if (j >= 0) {
-                        atomicAdd(&cnt[k], 1);
                         if (k < 64) m0 |= 1ull << ((KD < 64 ? KD : 64) - 1 - k);
                         else m1 |= 1ull << (KD - 64 - 1 - (k - 64));
                     }
                 }
-    } else {
-        for (int k = 0; k < KD; ++k) tile[t * KD + k] = -1;
+            }
     }
     __syncthreads();
     int* dst = os + (size_t)blockIdx.x * kQB * KD;
@@ -598,14 +626,22 @@ __global__ void __launch_bounds__(kQB * TPR) k_kmap_query(
         first[u] = __ldg(&table[slot[u]]);  // PER independent 16 B loads in flight
     }
     unsigned long long m0 = 0, m1 = 0;
+    // lanes sub, sub + TPR, ... of a warp share offset k: one ballot per u and
+    // one shared add per (warp, k) instead of TPR-strided contended atomics
+    constexpr unsigned kSubLanes = TPR == 1 ? 0xffffffffu : TPR == 2 ? 0x55555555u
+                                   : TPR == 4 ? 0x11111111u : 0x01010101u;
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
         const int k = sub + u * TPR;
-        if (k >= KD) continue;
-        const int j = ok[u] ? probe(table, mask, key[u], slot[u], first[u]) : -1;
-        tile[rl * KD + k] = j;
+        const int j = (k < KD && ok[u]) ? probe(table, mask, key[u], slot[u], first[u]) : -1;
+        if (k < KD) tile[rl * KD + k] = j;
+        const unsigned hit = __ballot_sync(0xffffffffu, j >= 0);
+        const int lane = t & 31;
+        if (lane < TPR && k < KD) {
+            const int c = __popc(hit & (kSubLanes << lane));
+            if (c) atomicAdd(&cnt[k], c);
+        }
         if (j >= 0) {
-            atomicAdd(&cnt[k], 1);
             // big-endian bit order (kmap.cpp:38-45)
             if (k < 64) m0 |= 1ull << ((KD < 64 ? KD : 64) - 1 - k);
             else m1 |= 1ull << (KD - 64 - 1 - (k - 64));
@@ -963,8 +999,10 @@ void coords_build_blocks(sk_coords* c, cudaStream_t st) {
     c->bcount.alloc(4, st);
     SK_CUDA(cudaMemsetAsync(c->bcount.p, 0, 4, st));
     if (c->n > 0) {
-        launch_pdl(k_block_insert, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n, c->btable.as<ulonglong2>(), (uint64_t)cap - 1,
-            c->bdense.as<int>(), c->bcount.as<int>());
+        launch_pdl(k_block_claim, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n,
+                   c->btable.as<ulonglong2>(), (uint64_t)cap - 1, c->bdense.as<int>(), c->bcount.as<int>());
+        launch_pdl(k_block_fill, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n,
+                   (const ulonglong2*)c->btable.as<ulonglong2>(), (uint64_t)cap - 1, c->bdense.as<int>());
     }
     c->has_blocks = true;
 }
