@@ -1862,7 +1862,7 @@ void launch_gconv(sk_ctx* ctx, sk_dtype dt, const ConvArgs& a_in, cudaStream_t s
     const char* tpath = getenv("SK_TRACE");
     if (tpath) {
         tbuf.alloc((4096 * 16 + 4 * 1024) * 8, st);
-        SK_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, st));
+        fill_async(tbuf.p, 0, tbuf.bytes, st);
         a.trace = tbuf.as<long long>();
     }
     a.exp = getenv("SK_EXP") ? atoi(getenv("SK_EXP")) : 0;
@@ -2253,7 +2253,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
                 acc.alloc((size_t)y_elems * 4, st);
                 yf = acc.as<float>();
             }
-            if (!y_accum) SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
+            if (!y_accum) fill_async(yf, 0, (size_t)y_elems * 4, st);
             a.y = yf;
             if (det) {
                 // splits accumulate in order so partial sums telescope
@@ -2283,7 +2283,7 @@ void conv_forward(sk_ctx* ctx, sk_kmap* m_fwd, const sk_dataflow_cfg& cfg, sk_dt
         acc.alloc((size_t)y_elems * 4, st);
         yf = acc.as<float>();
     }
-    if (!y_accum) SK_CUDA(cudaMemsetAsync(yf, 0, (size_t)y_elems * 4, st));
+    if (!y_accum) fill_async(yf, 0, (size_t)y_elems * 4, st);
     a.mode = 1;
     a.ws_tile_ptr = m->ws_tile_ptr.as<int>();
     a.in_pad = m->ws_in_pad.as<int>();
@@ -2352,7 +2352,7 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
     (void)cfg;  // conv_wgrad ignores cfg.kind in the reference (exec.cpp:398-414)
     validate(c_in >= 1 && c_out >= 1, "channel counts must be >= 1");
     kmap_ensure_ws(m, st);
-    if (!accumulate) SK_CUDA(cudaMemsetAsync(dw, 0, (size_t)m->kd * c_in * c_out * 4, st));
+    if (!accumulate) fill_async(dw, 0, (size_t)m->kd * c_in * c_out * 4, st);
     if (m->n_out == 0 || m->n_in == 0) return;
     if (dt != SK_F32 && !ctx->deterministic && c_in % 8 == 0 && c_out % 8 == 0) {
         // tcgen05 path (fp32 accumulate in TMEM, fp32 red.add flush)
@@ -2426,7 +2426,7 @@ void conv_wgrad(sk_ctx* ctx, sk_kmap* m, const sk_dataflow_cfg& cfg, sk_dtype dt
     const long long cells = (long long)m->kd * c_in * c_out;
     DevBuf dw64;
     dw64.alloc((size_t)cells * 8, st);
-    SK_CUDA(cudaMemsetAsync(dw64.p, 0, (size_t)cells * 8, st));
+    fill_async(dw64.p, 0, (size_t)cells * 8, st);
     double* d64 = dw64.as<double>();
     if (dt == SK_F32)
         launch_pdl(k_wgrad_simt<float>, grid, 256, 0, st, (const float*)x, (const float*)dy, c_in, c_out,

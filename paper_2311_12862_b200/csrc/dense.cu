@@ -435,7 +435,7 @@ bool launch_dense(sk_ctx* ctx, sk_dtype dt, DenseArgs a, const void* x, const vo
 #ifdef SK_DENSE_TRACE
     static long long* trbuf = nullptr;
     if (!trbuf) SK_CUDA(cudaMalloc(&trbuf, 64 * 8 * 8));
-    SK_CUDA(cudaMemsetAsync(trbuf, 0, 64 * 8 * 8, st));
+    fill_async(trbuf, 0, 64 * 8 * 8, st);
     a.trace = trbuf;
 #endif
     launch_pdl(kern, grid, kDenseThreads, smem, st, ta, tb, ty, tr, a);

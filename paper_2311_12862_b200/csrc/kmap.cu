@@ -994,10 +994,10 @@ void coords_build_blocks(sk_coords* c, cudaStream_t st) {
     while (cap < 2 * (int64_t)c->n) cap <<= 1;  // n_blocks <= n: load <= 1/2 worst case
     c->bcap = cap;
     c->btable.alloc((size_t)cap * 16, st);
-    SK_CUDA(cudaMemsetAsync(c->btable.p, 0xFF, c->btable.bytes, st));
+    fill_async(c->btable.p, 0xFF, c->btable.bytes, st);
     c->bdense.alloc((size_t)std::max(c->n, 1) * 64 * 4, st);  // cells initialised per block
     c->bcount.alloc(4, st);
-    SK_CUDA(cudaMemsetAsync(c->bcount.p, 0, 4, st));
+    fill_async(c->bcount.p, 0, 4, st);
     if (c->n > 0) {
         launch_pdl(k_block_claim, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n,
                    c->btable.as<ulonglong2>(), (uint64_t)cap - 1, c->bdense.as<int>(), c->bcount.as<int>());
@@ -1077,10 +1077,10 @@ void coords_build_table(sk_coords* c, cudaStream_t st) {
     if (c->has_table) return;
     c->cap = pow2_cap(c->n);
     c->table.alloc((size_t)c->cap * 16, st);
-    SK_CUDA(cudaMemsetAsync(c->table.p, 0xFF, c->table.bytes, st));  // empty key, row = UINT_MAX
+    fill_async(c->table.p, 0xFF, c->table.bytes, st);  // empty key, row = UINT_MAX
     DevBuf err;
     err.alloc(4, st);
-    SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    fill_async(err.p, 0, 4, st);
     if (c->n > 0) {
         launch_pdl(k_hash_insert, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n, c->table.as<ulonglong2>(), (uint64_t)c->cap - 1,
             err.as<int>());
@@ -1101,7 +1101,7 @@ sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_
     for (int d = 0; d < 3; ++d) out->stride_tag[d] = in->stride_tag[d] * (d < in->dims ? stride[d] : 1);
     out->cap = pow2_cap(n);
     out->table.alloc((size_t)out->cap * 16, st);
-    SK_CUDA(cudaMemsetAsync(out->table.p, 0xFF, out->table.bytes, st));
+    fill_async(out->table.p, 0xFF, out->table.bytes, st);
     if (n == 0) {
         out->n = 0;
         out->has_table = true;
@@ -1146,7 +1146,7 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
     out->id = next_coord_set_id();
     out->cap = pow2_cap(m);
     out->table.alloc((size_t)out->cap * 16, st);
-    SK_CUDA(cudaMemsetAsync(out->table.p, 0xFF, out->table.bytes, st));
+    fill_async(out->table.p, 0xFF, out->table.bytes, st);
     if (m == 0) {
         out->n = 0;
         out->coords.alloc(16, st);
@@ -1159,7 +1159,7 @@ sk_coords* coords_quantize(sk_ctx* ctx, int dims, int m, const double* raw, cons
     flag.alloc((size_t)m * 4, st);
     pos.alloc((size_t)m * 4 + 4, st);
     err.alloc(4, st);
-    SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    fill_async(err.p, 0, 4, st);
     const int g = (int)ceil_div(m, 256);
     launch_pdl(k_quant_insert, g, 256, 0, st, raw, batch, m, dims, voxel[0], voxel[1],
                                       dims == 3 ? voxel[2] : 1.0, out->table.as<ulonglong2>(),
@@ -1206,15 +1206,15 @@ void quantize_features(int m, int channels, const double* feats, const int32_t* 
         if (rule == 0) {
             DevBuf first;
             first.alloc((size_t)n * 4, st);
-            SK_CUDA(cudaMemsetAsync(first.p, 0x7F, (size_t)n * 4, st));
+            fill_async(first.p, 0x7F, (size_t)n * 4, st);
             launch_pdl(k_first_point, (int)ceil_div(m, 256), 256, 0, st, point_rows, m, first.as<int>());
             launch_pdl(k_quant_feats_first<T>, g, 256, 0, st, feats, channels, first.as<int>(), n, o);
         } else {
             DevBuf sum, cnt;
             sum.alloc((size_t)tot * 8, st);
             cnt.alloc((size_t)n * 4, st);
-            SK_CUDA(cudaMemsetAsync(sum.p, 0, sum.bytes, st));
-            SK_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, st));
+            fill_async(sum.p, 0, sum.bytes, st);
+            fill_async(cnt.p, 0, cnt.bytes, st);
             launch_pdl(k_quant_sum, (int)ceil_div((long long)m * channels, 256), 256, 0, st, feats, channels, point_rows, m, sum.as<double>(), cnt.as<int>());
             launch_pdl(k_quant_mean<T>, g, 256, 0, st, sum.as<double>(), cnt.as<int>(), channels, n, o);
         }
@@ -1247,13 +1247,13 @@ sk_kmap* kmap_from_edges(sk_ctx* ctx, const int32_t* d_edges, int E, int R, int 
     const size_t cap_pad = (size_t)E + (size_t)R * kTileWS;
     m->ws_in_pad.alloc(cap_pad * 4, st);
     m->ws_out_pad.alloc(cap_pad * 4, st);
-    SK_CUDA(cudaMemsetAsync(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st));
-    SK_CUDA(cudaMemsetAsync(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st));
+    fill_async(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st);
+    fill_async(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st);
     DevBuf counts, err, keys, keys2, vals, order, tmp;
     counts.alloc((size_t)R * 4, st);
     err.alloc(4, st);
-    SK_CUDA(cudaMemsetAsync(counts.p, 0, counts.bytes, st));
-    SK_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    fill_async(counts.p, 0, counts.bytes, st);
+    fill_async(err.p, 0, 4, st);
     if (E > 0) {
         keys.alloc((size_t)E * 8, st);
         keys2.alloc((size_t)E * 8, st);
@@ -1393,7 +1393,7 @@ sk_kmap* kmap_transpose(sk_kmap* src, cudaStream_t st) {
     m->n_out = src->n_in;
     m->identity = src->identity;
     alloc_map(m, st);
-    SK_CUDA(cudaMemsetAsync(m->os.p, 0xFF, m->os.bytes, st));
+    fill_async(m->os.p, 0xFF, m->os.bytes, st);
     long long total = (long long)src->n_out * src->kd;
     if (total > 0) {
         launch_pdl(k_transpose, (int)ceil_div(total, 256), 256, 0, st, src->os.as<int>(), src->n_out,
@@ -1425,8 +1425,8 @@ void kmap_ensure_ws(sk_kmap* m, cudaStream_t st) {
     const size_t cap_pad = cap + (size_t)m->kd * kTileWS;
     m->ws_in_pad.alloc(cap_pad * 4, st);
     m->ws_out_pad.alloc(cap_pad * 4, st);
-    SK_CUDA(cudaMemsetAsync(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st));
-    SK_CUDA(cudaMemsetAsync(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st));
+    fill_async(m->ws_in_pad.p, 0xFF, m->ws_in_pad.bytes, st);
+    fill_async(m->ws_out_pad.p, 0xFF, m->ws_out_pad.bytes, st);
     launch_pdl(k_ws_scan, 1, 1024, 0, st, m->blk_counts.as<int>(), m->n_blocks, m->kd,
                                   m->blk_off.as<long long>(), m->ws_ptr.as<long long>(),
                                   m->ws_tile_ptr.as<int>());
@@ -1553,7 +1553,7 @@ Prepared* kmap_prepare(sk_kmap* m, int splits, int pad, cudaStream_t st) {
             const RadixPlan pl = radix_plan((int)tot, end_bit);
             DevBuf scratch;
             scratch.alloc(pl.scratch_words * 4, st);
-            SK_CUDA(cudaMemsetAsync(scratch.p, 0, scratch.bytes, st));
+            fill_async(scratch.p, 0, scratch.bytes, st);
             // values start in the buffer that makes the last pass land in order
             int* vb[2];
             vb[pl.passes % 2] = order.as<int>();

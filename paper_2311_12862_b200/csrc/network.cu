@@ -886,7 +886,7 @@ void run_backward(sk_net* n, int hi, int lo, float* wgrad_flat, bool accumulate,
         const size_t a = n->wgrad_off[lo];
         const size_t b = n->wgrad_off[hi] + (size_t)n->kd[hi] * n->spec.layers[hi].c_in *
                                                 n->spec.layers[hi].c_out;
-        SK_CUDA(cudaMemsetAsync(wgrad_flat + a, 0, (b - a) * 4, st));
+        fill_async(wgrad_flat + a, 0, (b - a) * 4, st);
     }
     for (int i = hi; i >= lo; --i) {
         const LayerSpec& l = n->spec.layers[i];
@@ -1175,7 +1175,7 @@ sk_status sk_net_backward(sk_net* n, const void* d_grad_out, float* wgrad_flat, 
                 off[i + 1] = off[i] + ((size_t)std::max(n->out_set[i]->n, 1) *
                                            n->spec.layers[i].c_out + 3) / 4 * 4;  // 16 B aligned
             if (n->gout_slab.bytes < off[L] * 4) n->gout_slab.alloc(off[L] * 4, st);
-            SK_CUDA(cudaMemsetAsync(n->gout_slab.p, 0, off[L] * 4, st));
+            fill_async(n->gout_slab.p, 0, off[L] * 4, st);
             n->gout.assign(L, nullptr);
             for (int i = 0; i < L; ++i) n->gout[i] = n->gout_slab.as<float>() + off[i];
             const long long no = (long long)n->out_set[L - 1]->n * n->spec.layers[L - 1].c_out;

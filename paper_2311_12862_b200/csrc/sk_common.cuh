@@ -59,6 +59,10 @@ struct PdlScope {
     } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// small fills as a library kernel launched with launch_pdl when PDL is on: a
+// memset node is a full drain point on both sides (no programmatic overlap
+// with the kernels around it) in a map pipeline of short kernels (capi.cu)
+void fill_async(void* p, int byte, size_t bytes, cudaStream_t st);
 
 #if defined(__CUDACC__)
 // Launch with programmatic stream serialization (see pdl_wait): the kernel's

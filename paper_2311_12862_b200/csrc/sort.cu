@@ -271,13 +271,13 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_pass(
 
 void scan_exclusive_i32(const int* in, int* out, int n, int* total_dev, cudaStream_t st) {
     if (n <= 0) {
-        if (total_dev) SK_CUDA(cudaMemsetAsync(total_dev, 0, 4, st));
+        if (total_dev) fill_async(total_dev, 0, 4, st);
         return;
     }
     const int tiles = (int)ceil_div(n, kScanTile);
     DevBuf status;
     status.alloc((size_t)(tiles + 1) * 4, st);
-    SK_CUDA(cudaMemsetAsync(status.p, 0, status.bytes, st));
+    fill_async(status.p, 0, status.bytes, st);
     launch_pdl(k_scan_lookback, tiles, kScanThreads, 0, st, in, out, n, status.as<uint32_t>(), total_dev);
 }
 
@@ -327,7 +327,7 @@ int radix_sort_pairs(KT* keys[2], int* vals[2], int n, int begin_bit, int end_bi
     const RadixPlan pl = radix_plan(n, end_bit - begin_bit);
     DevBuf scratch;
     scratch.alloc(pl.scratch_words * 4, st);
-    SK_CUDA(cudaMemsetAsync(scratch.p, 0, scratch.bytes, st));
+    fill_async(scratch.p, 0, scratch.bytes, st);
     return radix_sort_run<KT>(keys, vals, n, begin_bit, pl, scratch.as<uint32_t>(), false, st);
 }
 
