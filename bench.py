@@ -612,7 +612,7 @@ def kmap_roofline(sk, pk):
     """Kernel-map build on the C5 1M-voxel sweep point (10 disjoint tiles of
     the planar n=160k / 2.5 cm recipe): coordinate set creation
     (copy + hash insert) and the K=3 submanifold map (block-index query at
-    this size: k_block_insert + k_kmap_query_blk; OS, masks). Algorithmic bytes are SURVEY §8(d)'s contract: 100 + 4*K^D =
+    this size: k_block_claim + k_block_fill + k_kmap_query_blk; OS, masks). Algorithmic bytes are SURVEY §8(d)'s contract: 100 + 4*K^D =
     208 B per voxel (coords, the table charged at 2N x 16 B for the insert and
     again for the query, out coords, OS and masks)."""
     import torch
@@ -644,7 +644,7 @@ def kmap_roofline(sk, pk):
             "voxels": int(n), "insert_ms": t_ins, "query_ms": t_q,
             "algorithmic_bytes": int(algo),
             "bytes_contract": "SURVEY 8(d): 208 B/voxel at K=3 (table at 2N x 16 B)",
-            "kernel": "k_hash_insert + k_block_insert + k_kmap_query_blk<3> "
+            "kernel": "k_hash_insert + k_block_claim + k_block_fill + k_kmap_query_blk<3> "
                       "(1M-voxel C5 sweep point)"}
 
 
