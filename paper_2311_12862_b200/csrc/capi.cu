@@ -266,7 +266,7 @@ sk_coords* make_coords(sk_ctx* ctx, int dims, int n, const int32_t* src, bool ho
         if (n)
             SK_CUDA(cudaMemcpyAsync(c->coords.p, src, (size_t)n * 16,
                                     host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
-        sk::coords_build_table(c, st);  // validates the packable range
+        sk::coords_validate(c, st);  // the packable range; the hash table is built on first use
     } catch (...) {
         delete c;
         throw;

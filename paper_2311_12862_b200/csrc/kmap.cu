@@ -64,8 +64,8 @@ __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int4 c = coords[i];
-    if (!packable(c.x, c.y, c.z, c.w)) {
-        atomicOr(err, 1);
+    if (!packable(c.x, c.y, c.z, c.w)) {  // root sets were range-checked at creation
+        if (err) atomicOr(err, 1);
         return;
     }
     unsigned long long key = pack_key(c.x, c.y, c.z, c.w);
@@ -78,6 +78,15 @@ __global__ void k_hash_insert(const int4* __restrict__ coords, int n,
         }
         s = (s + 1) & mask;
     }
+}
+
+__global__ void k_coords_check(const int4* __restrict__ coords, int n, int* __restrict__ err) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 c = coords[i];
+    if (!packable(c.x, c.y, c.z, c.w)) atomicOr(err, 1);
 }
 
 __global__ void k_down_insert(const int4* __restrict__ coords, int n, int sx, int sy, int sz,
@@ -1034,6 +1043,7 @@ void launch_query(sk_kmap* m, const int4* out_coords, sk_coords* in, cudaStream_
         else run(k_kmap_query_blk<5>);
         return;
     }
+    coords_build_table(in, st);  // first hash query on this set builds its table
     const int grid = m->rows_pad / kQB;
     const uint64_t mask = (uint64_t)in->cap - 1;
     const size_t smem = (size_t)(kQB * m->kd + m->kd) * 4;
@@ -1072,24 +1082,51 @@ uint64_t next_coord_set_id() {
 
 void coords_check_range(sk_ctx*, const int32_t*, int, cudaStream_t) {}
 
-void coords_build_table(sk_coords* c, cudaStream_t st) {
-    std::lock_guard<std::mutex> lock(c->mu);
-    if (c->has_table) return;
+namespace {
+void build_table_locked(sk_coords* c, cudaStream_t st, int* err) {
+    c->table_on.mark(st);
     c->cap = pow2_cap(c->n);
     c->table.alloc((size_t)c->cap * 16, st);
     fill_async(c->table.p, 0xFF, c->table.bytes, st);  // empty key, row = UINT_MAX
+    if (c->n > 0) {
+        launch_pdl(k_hash_insert, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n,
+                   c->table.as<ulonglong2>(), (uint64_t)c->cap - 1, err);
+    }
+    c->has_table = true;
+}
+}  // namespace
+
+// creation-time validation of a root set (the packable range; the reference
+// throws at construction), one 4 B read-back. Sets below the block-query
+// threshold get their hash table here (the insert checks the range; callers
+// like the ScanPipeline build it on their copy stream, off the forward's
+// path); larger sets run a check kernel only and build the table on first
+// use (coords_build_table): their stride-1 maps read only the block index.
+void coords_validate(sk_coords* c, cudaStream_t st) {
+    if (c->n == 0) return;
     DevBuf err;
     err.alloc(4, st);
     fill_async(err.p, 0, 4, st);
-    if (c->n > 0) {
-        launch_pdl(k_hash_insert, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n, c->table.as<ulonglong2>(), (uint64_t)c->cap - 1,
-            err.as<int>());
+    if (c->n < c->ctx->kmap_block_rows) {
+        std::lock_guard<std::mutex> lock(c->mu);
+        build_table_locked(c, st, err.as<int>());
+    } else {
+        launch_pdl(k_coords_check, (int)ceil_div(c->n, 256), 256, 0, st, c->coords.as<int4>(), c->n,
+                   err.as<int>());
     }
     int h_err = 0;
     read_back(st, {{err.p, 4}}, &h_err);
     validate(h_err == 0,
              "coordinate outside the packable range (batch [0,4096), xyz [-65536,65536))");
-    c->has_table = true;
+}
+
+void coords_build_table(sk_coords* c, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (c->has_table) {
+        stream_after(c->table_on, st);
+        return;
+    }
+    build_table_locked(c, st, nullptr);
 }
 
 sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_t st) {
@@ -1302,7 +1339,6 @@ sk_kmap* kmap_build(sk_coords* in, sk_coords* out, int kernel, const int32_t str
     validate(kernel >= 1 && kernel % 2 == 1, "kernel size must be odd (even kernels unsupported)");
     validate(kernel <= 5, "kernel size > 5 unsupported");
     for (int d = 0; d < in->dims; ++d) validate(stride[d] >= 1, "stride components must be >= 1");
-    coords_build_table(in, st);
     auto* m = new sk_kmap();
     m->ctx = in->ctx;
     m->dims = in->dims;

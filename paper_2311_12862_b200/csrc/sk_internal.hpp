@@ -67,6 +67,7 @@ struct sk_coords : sk::Refcounted {
     std::mutex mu;
     sk::BuiltOn built_on;   // stream of a lazily built (down-sampled / quantized) set
     sk::BuiltOn blocks_on;  // stream the block index was built on
+    sk::BuiltOn table_on;   // stream a root set's hash table was built on (first use)
     // children: downsampled sets by stride (owned), maps by key (owned)
     std::map<std::tuple<int, int, int>, sk_coords*> down;
     // key: (out id, kernel code, stride xyz, transposed, dilation code)
@@ -111,6 +112,7 @@ constexpr int kTileWS = 256; // pairs per FOD/GGS tile (padded per offset)
 
 // kmap.cu
 void coords_build_table(sk_coords* c, cudaStream_t st);
+void coords_validate(sk_coords* c, cudaStream_t st);
 void coords_check_range(sk_ctx* ctx, const int32_t* d, int n, cudaStream_t st);
 sk_coords* coords_downsample(sk_coords* in, const int32_t stride[3], cudaStream_t st);
 // quantize (tensor.cpp:87-142): coordinates in first-appearance order and the
