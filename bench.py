@@ -644,7 +644,7 @@ def kmap_roofline(sk, pk):
             "voxels": int(n), "insert_ms": t_ins, "query_ms": t_q,
             "algorithmic_bytes": int(algo),
             "bytes_contract": "SURVEY 8(d): 208 B/voxel at K=3 (table at 2N x 16 B)",
-            "kernel": "k_hash_insert + k_block_claim + k_block_fill + k_kmap_query_blk<3> "
+            "kernel": "k_coords_check + k_block_claim + k_block_fill + k_kmap_query_blk<3> "
                       "(1M-voxel C5 sweep point)"}
 
 
