@@ -177,13 +177,19 @@ __global__ void k_block_claim(const int4* __restrict__ coords, int n, ulonglong2
             s = (s + 1) & mask;
         }
     }
-    // ids: one counter add per warp (a per-block add serialised on the counter)
+    // ids: one counter add per CTA (per-warp adds serialised on the counter)
+    __shared__ unsigned cta_cnt, cta_base;
+    if (threadIdx.x == 0) cta_cnt = 0;
+    __syncthreads();
     const unsigned wins = __ballot_sync(0xffffffffu, win);
-    if (!wins) return;
-    unsigned base = 0;
-    if (lane == __ffs(wins) - 1) base = (unsigned)atomicAdd(count, __popc(wins));
-    base = __shfl_sync(0xffffffffu, base, __ffs(wins) - 1);
+    unsigned woff = 0;
+    if (lane == 0 && wins) woff = atomicAdd(&cta_cnt, (unsigned)__popc(wins));
+    woff = __shfl_sync(0xffffffffu, woff, 0);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_cnt) cta_base = (unsigned)atomicAdd(count, (int)cta_cnt);
+    __syncthreads();
     if (!win) return;
+    const unsigned base = cta_base + woff;
     const unsigned bid = base + __popc(wins & ((1u << lane) - 1));
     int4* d = reinterpret_cast<int4*>(dense + (size_t)bid * 64);
 #pragma unroll
