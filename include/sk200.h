@@ -108,7 +108,7 @@ sk_status sk_ctx_destroy(sk_ctx* ctx);
  * dataflow accumulates splits/offsets in a fixed order (no float atomics). */
 sk_status sk_ctx_set_deterministic(sk_ctx* ctx, int on);
 /* Stride-1 3-D K = 3 / 5 kernel maps over input sets of at least min_rows
- * voxels are queried through a 4x4x4 block index (default 1 << 19; a tuning
+ * voxels are queried through a 4x4x4 block index (default 1 << 16; a tuning
  * knob of the build, results are identical either way). */
 sk_status sk_ctx_set_kmap_block_rows(sk_ctx* ctx, int min_rows);
 

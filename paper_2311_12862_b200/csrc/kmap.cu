@@ -1022,11 +1022,11 @@ void coords_build_blocks(sk_coords* c, cudaStream_t st) {
     c->has_blocks = true;
 }
 
-// stride-1, non-transposed, 3-D, K in {3, 5}, large input sets: the block-
-// index query. Measured: its extra build pass costs more than it saves below
-// ~0.5M input voxels (MinkUNet scan: maps 0.72 -> 0.82 ms), above it the query
-// is ~12% faster (1M-voxel sweep point). The threshold is a context setting
-// (sk_ctx_set_kmap_block_rows, default 1 << 19).
+// stride-1, non-transposed, 3-D, K in {3, 5}, input sets >= 64k voxels: the
+// block-index query (with z-row loads and the claim/fill build it is faster
+// than the per-voxel probes from ~50k voxels: SECOND scan 2122 -> 2188 scans/s,
+// 0.68 -> 0.61 ms per scan; 1M voxels 2x). The threshold is a context setting
+// (sk_ctx_set_kmap_block_rows, default 1 << 16).
 bool use_block_query(const sk_kmap* m, const sk_coords* in) {
     const bool shape = !m->transposed && m->dims == 3 && (m->kernel == 3 || m->kernel == 5) &&
                        m->stride[0] == 1 && m->stride[1] == 1 && m->stride[2] == 1;
@@ -1108,12 +1108,18 @@ void build_table_locked(sk_coords* c, cudaStream_t st, int* err) {
 // like the ScanPipeline build it on their copy stream, off the forward's
 // path); larger sets run a check kernel only and build the table on first
 // use (coords_build_table): their stride-1 maps read only the block index.
+// below this many voxels the table is built at creation even when the set's
+// stride-1 maps use the block index: its strided maps / down-sampling need it
+// anyway, and building it with the creation keeps it off the forward's path
+// (ScanPipeline: copy stream); measured e2e -2.5 % with it lazy at 125k voxels
+constexpr int kLazyTableRows = 1 << 19;
+
 void coords_validate(sk_coords* c, cudaStream_t st) {
     if (c->n == 0) return;
     DevBuf err;
     err.alloc(4, st);
     fill_async(err.p, 0, 4, st);
-    if (c->n < c->ctx->kmap_block_rows) {
+    if (c->n < std::max(c->ctx->kmap_block_rows, kLazyTableRows)) {
         std::lock_guard<std::mutex> lock(c->mu);
         build_table_locked(c, st, err.as<int>());
     } else {

@@ -8,7 +8,7 @@ struct sk_ctx {
     int device = 0;
     int num_sms = 148;
     bool deterministic = false;
-    int kmap_block_rows = 1 << 19;  // sk_ctx_set_kmap_block_rows
+    int kmap_block_rows = 1 << 16;  // sk_ctx_set_kmap_block_rows
     size_t smem_optin = 227 * 1024;
     // dynamic work queues of the persistent conv kernels: kSchedSlots pairs
     // {next item, CTAs done}, zeroed once; a launch takes the next slot and

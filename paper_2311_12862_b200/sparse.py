@@ -79,7 +79,7 @@ class Context:
 
     def set_kmap_block_rows(self, min_rows: int) -> None:
         """Stride-1 3-D K=3/5 maps over input sets of >= min_rows voxels are
-        queried through a 4x4x4 block index (default 1 << 19; identical
+        queried through a 4x4x4 block index (default 1 << 16; identical
         results)."""
         check(lib().sk_ctx_set_kmap_block_rows(self.ptr, int(min_rows)))
 

@@ -17,8 +17,8 @@ tcs = sk.CoordSet.create(dc[0]); net.tune(tcs, df[0], training=0, warmup=1, runs
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 yout = torch.empty(max(len(c) for c in scans), net.layer_shapes[-1][2], dtype=torch.float16, device="cuda")
 s = torch.cuda.Stream()
-for rep in range(2):
-    for thr in (1 << 19, 1 << 16, 1 << 14, 1 << 12):
+for rep in range(3):
+    for thr in (1 << 19, 1 << 16, 1 << 14):
         sk.Context.get().set_kmap_block_rows(thr)
         with torch.cuda.stream(s):
             for i in range(4):
