@@ -199,7 +199,14 @@ def main():
                          "1 = one scan at a time")
     ap.add_argument("--no-tune", action="store_true",
                     help="skip the per-group autotuner; use implicit GEMM --splits everywhere")
+    ap.add_argument("--tune", default=os.environ.get("SK_BENCH_TUNE"), choices=["warm", "cold"],
+                    help="warm: the reference tuner (probes on cached maps); cold: every probe "
+                         "builds the maps of a fresh copy of the tuning scan (sk_net_set_tune_cold). "
+                         "Default: cold for the map-bound SECOND encoder (0.65-0.70 -> 0.55-0.58 "
+                         "ms per scan), warm for MinkUNet (within noise either way)")
     args = ap.parse_args()
+    if args.tune is None:
+        args.tune = "cold" if args.workload == "second" else "warm"
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -235,8 +242,10 @@ def main():
         tcs = sk.CoordSet.create(torch.from_numpy(tscan).cuda())
         tf = torch.from_numpy(rng.standard_normal((len(tscan), 4)).astype(np.float16)).cuda()
         t0 = time.perf_counter()
+        net.set_tune_cold(args.tune == "cold")
         lat, _ = net.tune(tcs, tf, training=0, warmup=1, runs=3)
-        tuned = {"tune_s": time.perf_counter() - t0, "tuned_forward_ms": lat,
+        net.set_tune_cold(False)
+        tuned = {"tune_s": time.perf_counter() - t0, "tuned_forward_ms": lat, "tune": args.tune,
                  "configs": [net.config(g).name() for g in range(net.num_groups)]}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()

@@ -29,7 +29,7 @@ SYMBOLS = [
     "sk_net_group_of_layer", "sk_net_layer_info", "sk_net_num_params", "sk_net_weight_ptr",
     "sk_net_set_config", "sk_net_get_config", "sk_net_forward", "sk_net_layer_output",
     "sk_net_forward_profiled",
-    "sk_net_measure", "sk_net_map_builds", "sk_net_set_overlap", "sk_net_set_pdl", "sk_net_group_traffic", "sk_net_backward",
+    "sk_net_measure", "sk_net_map_builds", "sk_net_set_overlap", "sk_net_set_pdl", "sk_net_set_tune_cold", "sk_net_group_traffic", "sk_net_backward",
     "sk_net_tune", "sk_tune_space_size", "sk_tune_space_entry",
 ]
 
@@ -140,6 +140,7 @@ def lib():
         "sk_net_map_builds": ([vp], C.c_int64),
         "sk_net_set_overlap": ([vp, C.c_int], C.c_int),
         "sk_net_set_pdl": ([vp, C.c_int], C.c_int),
+        "sk_net_set_tune_cold": ([vp, C.c_int], C.c_int),
         "sk_net_group_traffic": ([vp, C.c_int, C.POINTER(DataflowCfg), vp,
                                   C.POINTER(C.c_double)], C.c_int),
         "sk_net_backward": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, vp], C.c_int),

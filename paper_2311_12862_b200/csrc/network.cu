@@ -408,6 +408,7 @@ struct sk_net {
     int64_t map_builds = 0;
     bool overlap = true;                      // overlapped map builds (sk_net_set_overlap)
     bool pdl = true;                          // programmatic dependent launch (sk_net_set_pdl)
+    bool tune_cold = false;                   // tuner probes on fresh sets (sk_net_set_tune_cold)
     cudaStream_t map_stream = nullptr;        // overlapped map builds (run_forward)
     cudaStream_t cmp_stream = nullptr;        // overlapped forward's convs for legacy-stream callers
     std::vector<cudaEvent_t> map_ready;       // per layer: its maps are built on map_stream
@@ -790,6 +791,24 @@ void run_forward(sk_net* n, sk_coords* root, const void* feats, int channels, cu
 double measure(sk_net* n, sk_coords* root, const void* feats, int channels, bool fwd, bool dg,
                bool wg, cudaStream_t st) {
     double total = 0;
+    if (n->tune_cold && fwd && !dg && !wg) {
+        // a fresh copy of the set: every map (and its split/sort or pair
+        // lists for the candidate configs) is built inside the timed forward
+        sk_coords* fresh = nullptr;
+        const sk_status rc = sk_coords_create(n->ctx, root->dims, root->n,
+                                              root->coords.as<int32_t>(), root->stride_tag, st, &fresh);
+        if (rc) fail(rc, sk_last_error());
+        Timer t(st);
+        try {
+            run_forward(n, fresh, feats, channels, st, nullptr, nullptr);
+        } catch (...) {
+            sk_coords_release(fresh);
+            throw;
+        }
+        total += t.stop();
+        sk_coords_release(fresh);
+        return total;
+    }
     {
         Timer t(st);
         run_forward(n, root, feats, channels, st, nullptr, nullptr);
@@ -1143,6 +1162,13 @@ sk_status sk_net_set_pdl(sk_net* n, int on) {
     return nguard([&] {
         sk::validate(n != nullptr, "null network");
         n->pdl = on != 0;
+    });
+}
+
+sk_status sk_net_set_tune_cold(sk_net* n, int on) {
+    return nguard([&] {
+        sk::validate(n != nullptr, "null network");
+        n->tune_cold = on != 0;
     });
 }
 

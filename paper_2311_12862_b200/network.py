@@ -188,6 +188,11 @@ class NetworkRunner:
         """Programmatic dependent launch of the runner's kernels (sk_net_set_pdl; default on)."""
         check(lib().sk_net_set_pdl(self.ptr, int(bool(on))))
 
+    def set_tune_cold(self, on: bool) -> None:
+        """Tuner probes on fresh copies of the tuning set, so map preparation
+        is timed with each candidate (sk_net_set_tune_cold; default off)."""
+        check(lib().sk_net_set_tune_cold(self.ptr, int(bool(on))))
+
     def map_build_count(self) -> int:
         return lib().sk_net_map_builds(self.ptr)
 

@@ -191,6 +191,34 @@ def test_tuner_contracts(env):
     assert len(log2) == 2 * G * len(space)
 
 
+def test_cold_map_tuning(env):
+    """sk_net_set_tune_cold: every probe builds the maps of a fresh copy of the
+    tuning set (map preparation timed with each candidate); same call counts
+    and argmin contract, the tuning set's own maps untouched, and the tuned
+    runner's output equals the same configs installed by hand."""
+    torch, sk, N, M = env
+    net = N.NetworkRunner(M.toy_unet(), dtype=torch.float16, weight_seed=5)
+    cs = sk.CoordSet.create(scan(3000, seed=19))
+    x = torch.randn(cs.n, 1, device="cuda").half()
+    space = N.default_space()
+    net.set_tune_cold(True)
+    builds0 = net.map_build_count()
+    lat, log = net.tune(cs, x, training=0, warmup=1, runs=2)
+    net.set_tune_cold(False)
+    G = net.num_groups
+    assert len(log) == G * len(space) and lat > 0
+    for g in range(G):
+        rows = log[log[:, 1] == g]
+        assert net.config(g) == space[int(rows[np.argmin(rows[:, 3]), 2])]
+    assert net.map_build_count() > builds0  # maps were rebuilt per probe
+    y, _ = net.forward(cs, x)
+    ref = N.NetworkRunner(M.toy_unet(), dtype=torch.float16, weight_seed=5)
+    for g in range(G):
+        ref.set_config(g, net.config(g))
+    y2, _ = ref.forward(sk.CoordSet.create(scan(3000, seed=19)), x)
+    assert torch.allclose(y.float(), y2.float(), atol=1e-2, rtol=1e-2)
+
+
 def test_tune_result_and_tspw_weights_roundtrip(env, tmp_path):
     """A tuned assignment and the weights leave one runner as reference-format
     files (TuneResult JSON, TSPW) and reproduce the same network in another."""
