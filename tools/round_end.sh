@@ -6,4 +6,4 @@ timeout 600 python bench.py > gpurun_out/re_infer.log 2>&1
 timeout 600 python bench.py --workload second > gpurun_out/re_second.log 2>&1
 timeout 900 python bench.py --workload train > gpurun_out/re_train.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/re_ref.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/re_launches.csv python bench.py --steps 2 --warmup 3 --concurrency 1 --no-cpu-baseline > gpurun_out/re_ncu.log 2>&1
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/re_launches.csv python tools/one_forward.py > gpurun_out/re_ncu.log 2>&1
