@@ -294,11 +294,13 @@ sk_status sk_net_set_overlap(sk_net* net, int on);
  * scans/s at 6 in flight). No reference counterpart (sk200 runtime). */
 sk_status sk_net_set_pdl(sk_net* net, int on);
 /* Cold-map tuning (default off = the reference's tuner: every probe runs on
- * the tuning set's cached maps). On: every sk_net_tune probe runs the forward
- * on a fresh copy of the coordinate set, so a candidate's map preparation
- * (split + sort, pair lists) is timed with its convolutions -- the objective
- * of a workload whose maps are new every scan. Same call counts. No
- * reference counterpart (sk200 runtime). */
+ * the tuning set's cached maps). On: every forward-only probe (inference
+ * tuning, training = 0, and the forward pass of sparse_mapping) runs on a
+ * fresh copy of the coordinate set, so a candidate's map preparation (split +
+ * sort, pair lists) is timed with its convolutions -- the objective of a
+ * workload whose maps are new every scan; probes that include dgrad / wgrad
+ * keep the cached maps. Same call counts. No reference counterpart (sk200
+ * runtime). */
 sk_status sk_net_set_tune_cold(sk_net* net, int on);
 /* modeled_group_traffic (network.cpp:453-471) */
 sk_status sk_net_group_traffic(sk_net* net, int group, const sk_dataflow_cfg* cfg, void* stream,
