@@ -273,3 +273,31 @@ def test_block_query_matches_reference(reference, min_rows):
     r = subprocess.run([sys.executable, "-c", BLOCK_CHECK, root, str(min_rows)],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "blocks ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_large_set_lazy_table(sk, reference):
+    """Sets of >= 2^19 voxels are range-checked by a check kernel at creation
+    and get their hash table on first use (strided maps, down-sampling): the
+    packable-range error still comes from CoordSet.create, and maps that read
+    the lazily built table (strided, transposed) plus the block-index
+    submanifold map are bit-exact against the reference."""
+    from paper_2311_12862_b200.synth import uniform_voxels
+    c_np = uniform_voxels(620_000, 160, seed=4)
+    assert len(c_np) >= 1 << 19
+    bad = c_np.copy()
+    bad[len(bad) // 2, 1] = 70000
+    with pytest.raises(sk.ValidationError):
+        sk.CoordSet.create(bad)
+    c = sk.CoordSet.create(c_np)
+    m = sk.build_kmap(c, c, 3, 1)  # block index only
+    rm = reference.kmap(3, 3, c_np, c_np, [1, 1, 1])
+    assert np.array_equal(m.os()[0], rm.os()[0]) and np.array_equal(m.os()[1], rm.os()[1])
+    o = sk.build_out_coords(c, 2)
+    o_np = o.numpy()
+    assert np.array_equal(o_np, reference.out_coords(3, c_np, [2, 2, 2]))
+    ms = sk.build_kmap(c, o, 3, 2)  # first hash query on c: builds its table
+    rms = reference.kmap(3, 3, c_np, o_np, [2, 2, 2])
+    assert np.array_equal(ms.os()[0], rms.os()[0]) and np.array_equal(ms.os()[1], rms.os()[1])
+    mt = sk.build_kmap(o, c, 3, 2, transposed=True)
+    rmt = reference.kmap(3, 3, o_np, c_np, [2, 2, 2], transposed=True)
+    assert np.array_equal(mt.os()[0], rmt.os()[0]) and np.array_equal(mt.os()[1], rmt.os()[1])
